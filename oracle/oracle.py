@@ -1,0 +1,227 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes front end of the fp64 CPU oracle.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and ``--impl reference``) may import this module.  The
+product path (``paper_1911_13252_b200``) never imports it and shares no code
+with it: the oracle regenerates the weights with its own implementation of the
+counter-based generator and computes in fp64.
+
+Paper: El Zini, Rizk, Awad, arXiv 1911.13252 ("P:n" = PAPER.md line n).
+  * ``build_H``  -- Alg. 1 line 2 with Eqs. 5-10 read as
+    DESIGN.md readings R3-R14 state.
+  * ``lstsq``    -- S4.2: Householder QR of [H | Y], z = Q^T Y,
+    back substitution; rank check + ridge fallback (R19).
+  * ``predict``  -- Eq. 4, no output bias (R16).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "elm_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+ARCHS = {"elman": 0, "jordan": 1, "narmax": 2, "fc": 3, "lstm": 4, "gru": 5}
+GATES = {"lstm": ("o", "c", "lambda", "in"), "gru": ("z", "r", "f")}
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (plain C, -O2 -ffp-contract=off, OpenMP row split)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fopenmp", "-shared", "-fPIC",
+               "-o", _LIB + ".tmp", _SRC, "-lm"]
+        subprocess.run(cmd, check=True)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        L = _lib
+        i64, i32, u64 = ctypes.c_int64, ctypes.c_int, ctypes.c_uint64
+        vp = ctypes.c_void_p
+        L.orc_gen_block.argtypes = [i32] * 9 + [u64, i32, vp]
+        L.orc_gen_block.restype = i32
+        L.orc_block_len.argtypes = [i32] * 8
+        L.orc_block_len.restype = i64
+        L.orc_num_blocks.argtypes = [i32]
+        L.orc_num_blocks.restype = i32
+        L.orc_build_H.argtypes = [i32] * 8 + [vp, vp, i64, vp, i64, i64, vp, i64, i32]
+        L.orc_build_H.restype = i32
+        L.orc_lstsq.argtypes = [vp, i64, vp, i64, i32, vp, vp, vp]
+        L.orc_lstsq.restype = i32
+        L.orc_solve_from_R.argtypes = [vp, i32, i64, vp, vp]
+        L.orc_solve_from_R.restype = i32
+        L.orc_predict.argtypes = [vp, i64, i64, i32, vp, vp]
+        L.orc_predict.restype = None
+        L.orc_rng_u64.argtypes = [u64]
+        L.orc_rng_u64.restype = u64
+        L.orc_max_threads.argtypes = []
+        L.orc_max_threads.restype = i32
+    return _lib
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("rho", ctypes.c_double), ("rmse", ctypes.c_double),
+                ("rdiag_min_abs", ctypes.c_double), ("rdiag_max_abs", ctypes.c_double),
+                ("ridge_lambda", ctypes.c_double), ("rank_flag", ctypes.c_int),
+                ("n_total", ctypes.c_int64)]
+
+
+@dataclass
+class Net:
+    """Architecture + hyper-parameters (Table 1; opts of DESIGN.md)."""
+    arch: str
+    S: int
+    M: int
+    Q: int
+    F: int = -1          # NARMAX output lags (default Q, reading R8)
+    R: int = -1          # NARMAX error lags (default Q)
+    act: int = 0         # 0 sigmoid, 1 tanh for g (Elman/Jordan/NARMAX/FC)
+    fc_lags: int = -1    # FC lags (default Q, prose reading R9)
+    rec_scale: int = 0   # 0 = 1/sqrt(fan_in) on blocks multiplying h; 1 = unit
+    weight_grid: int = 0  # 0 fp32, 1 fp16-grid, 2 tf32-grid (MMA blocks only)
+
+    def __post_init__(self):
+        if self.F < 0:
+            self.F = self.Q
+        if self.R < 0:
+            self.R = self.Q
+        if self.fc_lags < 0:
+            self.fc_lags = self.Q
+
+    @property
+    def code(self) -> int:
+        return ARCHS[self.arch]
+
+    def _dims(self):
+        return (self.code, self.S, self.M, self.Q, self.F, self.R, self.fc_lags)
+
+
+def num_blocks(arch: str) -> int:
+    return lib().orc_num_blocks(ARCHS[arch])
+
+
+def block_shape(net: Net, block_id: int):
+    """Logical shape of a weight block."""
+    a, S, M, Q, F, R, L = net.arch, net.S, net.M, net.Q, net.F, net.R, net.fc_lags
+    if a in ("elman", "jordan"):
+        return [(S, M), (M,), (M, Q)][block_id]
+    if a == "narmax":
+        return [(S, M), (M,), (M, F), (M, R)][block_id]
+    if a == "fc":
+        return [(S, M), (M,), (L, M, M)][block_id]
+    return [(S, M), (M, M), (M,)][block_id % 3]
+
+
+def gen_weights(net: Net, seed: int):
+    """Regenerate all weight blocks (fp32 numpy arrays in logical layout)."""
+    L = lib()
+    out = []
+    for b in range(num_blocks(net.arch)):
+        n = L.orc_block_len(*net._dims(), b)
+        arr = np.empty(n, dtype=np.float32)
+        rc = L.orc_gen_block(*net._dims(), net.rec_scale, net.weight_grid,
+                             ctypes.c_uint64(seed & (2**64 - 1)), b, arr.ctypes.data)
+        assert rc == 0
+        out.append(arr.reshape(block_shape(net, b)))
+    return out
+
+
+def build_H(net: Net, blocks, X, Yfb=None, threads: int = 1) -> np.ndarray:
+    """fp64 H(Q) [N][M] for fp32 X [N][Q][S] (or [N][Q*S]) and optional Yfb [N][Q]."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    N = X.shape[0]
+    X2 = X.reshape(N, -1)
+    assert X2.shape[1] >= net.Q * net.S
+    blks = [np.ascontiguousarray(b, dtype=np.float32) for b in blocks]
+    assert len(blks) == num_blocks(net.arch)
+    ptrs = (ctypes.c_void_p * len(blks))(*[b.ctypes.data for b in blks])
+    H = np.zeros((N, net.M), dtype=np.float64)
+    ydata, ldy = None, 0
+    if Yfb is not None:
+        Yfb = np.ascontiguousarray(Yfb, dtype=np.float32).reshape(N, -1)
+        ydata, ldy = Yfb.ctypes.data, Yfb.shape[1]
+    if N == 0:
+        return H
+    rc = lib().orc_build_H(net.code, net.S, net.M, net.Q, net.F, net.R, net.act, net.fc_lags,
+                           ctypes.cast(ptrs, ctypes.c_void_p), X2.ctypes.data, X2.shape[1],
+                           ydata, ldy, N, H.ctypes.data, net.M, threads)
+    assert rc == 0
+    return H
+
+
+@dataclass
+class SolveInfo:
+    rho: float
+    rmse: float
+    rdiag_min_abs: float
+    rdiag_max_abs: float
+    ridge_lambda: float
+    rank_flag: int
+    n_total: int
+    status: int
+    R: np.ndarray
+
+
+def lstsq(H, Y):
+    """beta = argmin ||H beta - Y|| by unblocked Householder QR on [H | Y] (fp64).
+
+    Returns (beta, SolveInfo).  status: 0 ok, 1 ridge fallback, -3
+    underdetermined (N < M), -4 non-finite input."""
+    H = np.ascontiguousarray(H, dtype=np.float64)
+    N, M = H.shape
+    Y = np.ascontiguousarray(np.asarray(Y, dtype=np.float64).reshape(N))
+    beta = np.zeros(M, dtype=np.float64)
+    info = _Info()
+    R = np.zeros((M + 1, M + 1), dtype=np.float64)
+    rc = lib().orc_lstsq(H.ctypes.data, M, Y.ctypes.data, N, M, beta.ctypes.data,
+                         ctypes.addressof(info), R.ctypes.data)
+    return beta, SolveInfo(info.rho, info.rmse, info.rdiag_min_abs, info.rdiag_max_abs,
+                           info.ridge_lambda, info.rank_flag, info.n_total, rc, R)
+
+
+def solve_from_R(R, M: int, n_total: int):
+    """beta from an (M+1)x(M+1) upper-triangular R of [H | Y] (sign-normalised in a copy)."""
+    Rf = np.array(R, dtype=np.float64, copy=True, order="C")
+    beta = np.zeros(M, dtype=np.float64)
+    info = _Info()
+    rc = lib().orc_solve_from_R(Rf.ctypes.data, M, n_total, beta.ctypes.data, ctypes.addressof(info))
+    return beta, SolveInfo(info.rho, info.rmse, info.rdiag_min_abs, info.rdiag_max_abs,
+                           info.ridge_lambda, info.rank_flag, info.n_total, rc, Rf)
+
+
+def predict(H, beta) -> np.ndarray:
+    H = np.ascontiguousarray(H, dtype=np.float64)
+    N, M = H.shape
+    beta = np.ascontiguousarray(beta, dtype=np.float64)
+    out = np.zeros(N, dtype=np.float64)
+    lib().orc_predict(H.ctypes.data, M, N, M, beta.ctypes.data, out.ctypes.data)
+    return out
+
+
+def train(net: Net, seed: int, X, Y, Yfb=None, threads: int = 1):
+    """Alg. 1 end to end: weights -> H(Q) -> beta."""
+    blocks = gen_weights(net, seed)
+    H = build_H(net, blocks, X, Yfb, threads=threads)
+    beta, info = lstsq(H, Y)
+    return H, beta, info
+
+
+def rng_u64(z: int) -> int:
+    """splitmix64 mix of DESIGN.md "Weights" (for the known-answer test)."""
+    return lib().orc_rng_u64(ctypes.c_uint64(z & (2**64 - 1)))
+
+
+def max_threads() -> int:
+    return lib().orc_max_threads()
