@@ -1,0 +1,180 @@
+/*
+ * elmrnn.h -- C ABI of the B200-native ELM-RNN trainer (libelmrnn.so).
+ *
+ * Implements the data-parallel hot path of El Zini, Rizk & Awad,
+ * "An Optimized and Energy-Efficient Parallel Implementation of
+ * Non-Iteratively Trained Recurrent Neural Networks" (arXiv 1911.13252),
+ * Alg. 1 "S-RELM":
+ *   1. randomly assign the fixed weights             -> elmrnn_init
+ *   2. compute H(t), t = 1..Q, keep H(Q) in R^{N x M} -> elmrnn_build_H
+ *   3. beta = H(Q)^+ Y by Householder QR, z = Q^T Y,
+ *      back substitution (S4.2)           -> elmrnn_solve_beta
+ * and the readout of Eq. 4               -> elmrnn_predict.
+ * "P:n" cites /root/reference/PAPER.md line n; readings R1..R25 of the paper's
+ * silent or garbled points are listed in DESIGN.md.
+ *
+ * Conventions (all calls):
+ *  - Pointers marked "dev" are CUDA device pointers on the handle's device,
+ *    owned by the caller; "host" pointers are ordinary host memory.  The
+ *    library owns its weights and workspace (freed by elmrnn_destroy).
+ *  - Work is enqueued on the handle's stream (elmrnn_set_stream; default the
+ *    legacy stream 0) and the call returns without synchronising, except where
+ *    a host-side output (info) is requested: then the call synchronises that
+ *    stream before returning.
+ *  - Arguments are validated on the host before anything is launched: an
+ *    error status means nothing was enqueued.  Handles are not thread safe.
+ *  - Row-major layouts with explicit leading dimensions (in elements).
+ *  - No CPU fallback: every arithmetic step runs in this library's CUDA
+ *    kernels (sm_100a).  A missing/failed device returns ELMRNN_ERR_CUDA.
+ */
+#ifndef ELMRNN_H
+#define ELMRNN_H
+
+#if defined(__GNUC__)
+#define ELMRNN_API __attribute__((visibility("default")))
+#else
+#define ELMRNN_API
+#endif
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct elmrnn* elmrnn_t;
+
+/* The six architectures of S2.2. */
+typedef enum {
+    ELMRNN_ELMAN = 0,   /* Eq. 5: self recurrence over Q lags            */
+    ELMRNN_JORDAN = 1,  /* Eq. 6: output feedback, teacher forced (R7)   */
+    ELMRNN_NARMAX = 2,  /* Eq. 7: output (+ error, e == 0) feedback (R8) */
+    ELMRNN_FC = 3,      /* S2.2.4: all neurons, Q lags (prose, R9)       */
+    ELMRNN_LSTM = 4,    /* S2.2.5: dense U, gates (o, c, lambda, in)     */
+    ELMRNN_GRU = 5      /* S2.2.6: dense U, Cho form, gates (z, r, f)    */
+} elmrnn_arch;
+
+typedef enum {
+    ELMRNN_OK = 0,
+    ELMRNN_WARN_RIDGE = 1,            /* rank-deficient R: beta from the ridge fallback (R19) */
+    ELMRNN_ERR_ARG = -1,              /* null pointer, arch out of range, d/M/Q < 1, N < 0    */
+    ELMRNN_ERR_SHAPE = -2,            /* leading dimension smaller than the logical row       */
+    ELMRNN_ERR_UNDERDETERMINED = -3,  /* N_total < M                                          */
+    ELMRNN_ERR_NONFINITE = -4,        /* NaN/Inf met in H or Y during the solve               */
+    ELMRNN_ERR_UNSUPPORTED = -5,      /* size beyond the implemented range   */
+    ELMRNN_ERR_CUDA = -6,             /* CUDA error; text in elmrnn_last_error                */
+    ELMRNN_ERR_OOM = -7               /* device allocation failed                             */
+} elmrnn_status;
+
+/* Options (elmrnn_opts_default fills the defaults shown). */
+typedef struct {
+    int F, R;         /* NARMAX output / error lags; -1 -> Q ("max number of time
+                         dependencies", Table 1; reading R8)                 */
+    int act;          /* g for Elman/Jordan/NARMAX/FC: 0 sigmoid (default), 1 tanh (R3) */
+    int rec_scale;    /* 0: blocks multiplying the hidden state are scaled by
+                         1/sqrt(fan_in) (default, R1); 1: unit U[-1,1) everywhere     */
+    int weight_grid;  /* MMA blocks (FC A, LSTM/GRU U): 0 fp32 (default), 1 rounded
+                         to the fp16 grid, 2 rounded to the tf32 grid (RNA)            */
+    int fc_lags;      /* FC lags L; -1 -> Q (prose reading R9); 1 = first-order FC     */
+    int force_path;   /* H-builder choice: 0 auto, 1 FP32-FMA kernels, 2 tensor cores */
+} elmrnn_opts;
+
+/* Diagnostics of a solve (host struct). */
+typedef struct {
+    double rho;             /* || H beta - Y ||_2 = || R_aug [beta; -1] ||_2        */
+    double rmse;            /* rho / sqrt(n_total): training RMSE                   */
+    double rdiag_min_abs;   /* min_k |R_kk|, k < M                                  */
+    double rdiag_max_abs;   /* max_k |R_kk|, k < M                                  */
+    double ridge_lambda;    /* 0, or the ridge lambda used (R19)                    */
+    int rank_flag;          /* 0 full rank, 1 ridge fallback used                   */
+    int64_t n_total;        /* rows that entered the factorisation                  */
+} elmrnn_solve_info;
+
+ELMRNN_API void elmrnn_opts_default(elmrnn_opts* opts);
+
+/* Alg. 1 line 1: create a handle on the current CUDA device and draw
+ * the fixed random weights on the GPU with the counter-based generator of
+ * DESIGN.md "Weights" (R1, R2).  arch: elmrnn_arch; d = S input dimension
+ * (Table 1); M hidden neurons; Q window length / lags; seed: weight seed.
+ * Errors: ARG, UNSUPPORTED, OOM, CUDA.  *out is NULL on error. */
+ELMRNN_API elmrnn_status elmrnn_init(elmrnn_t* out, int arch, int d, int M, int Q, uint64_t seed);
+ELMRNN_API elmrnn_status elmrnn_init_ex(elmrnn_t* out, int arch, int d, int M, int Q, uint64_t seed,
+                             const elmrnn_opts* opts);
+
+/* Enqueue subsequent work on this cudaStream_t (NULL = legacy stream). */
+ELMRNN_API elmrnn_status elmrnn_set_stream(elmrnn_t h, void* cuda_stream);
+
+/* Alg. 1 line 2, Eqs. 5-10: H(Q) for N windows.
+ *   X   dev fp32 [N][ldx], window i at X + i*ldx laid out [Q][d] (time-major,
+ *       Table 1: x_j in R^{S x Q}); ldx >= Q*d.
+ *   Yfb dev fp32 [N][ldy] teacher signal, Yfb[i][tau-1] = y_i(tau) (R7), or NULL:
+ *       then y_i(tau) = X[i][tau][0] (univariate autoregressive window).
+ *       Used by Jordan/NARMAX only; ldy >= Q when given.
+ *   H   dev fp32 [N][ldh] output, ldh >= M.  Only H(Q) is written (R14), each
+ *       element exactly once.
+ * N == 0 is a no-op.  Errors: ARG, SHAPE, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_build_H(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb,
+                             int64_t ldy, int64_t N, float* H, int64_t ldh);
+
+/* S4.2: beta = argmin ||H beta - Y||_2 by fp64 Householder
+ * tall-skinny QR of [H | Y] (the reflectors are applied to Y as the augmented
+ * column, so z = Q^T Y comes out of the factorisation), sign normalisation,
+ * rank check with ridge fallback (R19), and back substitution R beta = z.
+ *   H dev fp32 [N][ldh], Y dev fp32 [N], beta dev fp64 [M] (output).
+ *   info host (optional): when non-NULL the call synchronises the stream and
+ *   fills it; non-finite input is then reported as ERR_NONFINITE and a ridge
+ *   solve as WARN_RIDGE.  With info == NULL the call is fully asynchronous and
+ *   returns OK once enqueued.
+ * Errors: ARG, SHAPE, UNDERDETERMINED (N < M), NONFINITE, OOM, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_solve_beta(elmrnn_t h, const float* H, int64_t ldh, const float* Y,
+                                int64_t N, double* beta, elmrnn_solve_info* info);
+
+/* Row-sharded solve, step 1 (one per rank / row block): factor the local
+ * [H | Y] (N rows) into its (M+1)x(M+1) upper-triangular R, written packed
+ * row-major (row k holds R[k][k..M]) to Rpk dev fp64 [elmrnn_packed_r_len(h)].
+ * N may be 0 (R = 0).  Asynchronous.  Errors: ARG, SHAPE, OOM, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_solve_local(elmrnn_t h, const float* H, int64_t ldh, const float* Y,
+                                 int64_t N, double* Rpk);
+
+/* Row-sharded solve, step 2: merge P packed R factors (dev fp64
+ * [P][elmrnn_packed_r_len(h)], e.g. the output of an NCCL all-gather) by
+ * Householder QR of their stack, then solve as elmrnn_solve_beta.  N_total is
+ * the total row count (for the RMSE).  beta dev fp64 [M]; info as above.
+ * Errors: ARG, UNDERDETERMINED, NONFINITE, OOM, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_solve_merge(elmrnn_t h, const double* Rpk_all, int P, int64_t N_total,
+                                 double* beta, elmrnn_solve_info* info);
+
+/* (M+1)(M+2)/2: length of one packed R in doubles. */
+ELMRNN_API int64_t elmrnn_packed_r_len(elmrnn_t h);
+
+/* Eq. 4: Yhat[i] = sum_j beta_j H(Q)[i][j] (no output bias, R16),
+ * building H(Q) internally with the same kernels as elmrnn_build_H.
+ * X, Yfb as in elmrnn_build_H; beta dev fp64 [M]; Yhat dev fp32 [N].
+ * Errors: ARG, SHAPE, OOM, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_predict(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb,
+                             int64_t ldy, int64_t N, const double* beta, float* Yhat);
+
+/* Parity hook: copy logical weight block block_id (DESIGN.md "Weights" block
+ * map, row-major logical layout) to host_dst (count floats, must equal the
+ * block's length).  Synchronous.  Errors: ARG, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_get_weights(elmrnn_t h, int block_id, float* host_dst, int64_t count);
+
+/* Length of weight block block_id, or -1 when out of range. */
+ELMRNN_API int64_t elmrnn_weight_block_len(elmrnn_t h, int block_id);
+
+/* Which H-builder the handle uses: 1 FP32-FMA kernels, 2 tcgen05 tensor cores. */
+ELMRNN_API int elmrnn_path(elmrnn_t h);
+
+/* Number of CUDA kernels this handle has launched so far (evidence counter). */
+ELMRNN_API int64_t elmrnn_launch_count(elmrnn_t h);
+
+/* Text of the last error on this handle (or of the last failed init when h is NULL). */
+ELMRNN_API const char* elmrnn_last_error(elmrnn_t h);
+
+/* Free weights and workspace.  NULL is a no-op. */
+ELMRNN_API void elmrnn_destroy(elmrnn_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ELMRNN_H */

@@ -1,0 +1,242 @@
+// api.cu -- the C ABI of include/elmrnn.h: validation, dispatch, workspace.
+// Every arithmetic step is a kernel of this library; there is no host or
+// library fallback.  Citations "P:n" = PAPER.md line n.
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "common.cuh"
+
+using namespace elm;
+
+static thread_local std::string g_init_error;
+
+static elmrnn_status fail(elmrnn* h, elmrnn_status st, const std::string& msg) {
+    if (h) h->err = msg; else g_init_error = msg;
+    return st;
+}
+
+static elmrnn_status cuda_fail(elmrnn* h, cudaError_t e, const char* where) {
+    std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+    return fail(h, e == cudaErrorMemoryAllocation ? ELMRNN_ERR_OOM : ELMRNN_ERR_CUDA, m);
+}
+
+extern "C" {
+
+void elmrnn_opts_default(elmrnn_opts* o) {
+    if (!o) return;
+    o->F = -1; o->R = -1; o->act = 0; o->rec_scale = 0; o->weight_grid = 0; o->fc_lags = -1; o->force_path = 0;
+}
+
+elmrnn_status elmrnn_init(elmrnn_t* out, int arch, int d, int M, int Q, uint64_t seed) {
+    return elmrnn_init_ex(out, arch, d, M, Q, seed, nullptr);
+}
+
+elmrnn_status elmrnn_init_ex(elmrnn_t* out, int arch, int d, int M, int Q, uint64_t seed, const elmrnn_opts* opts) {
+    if (!out) return fail(nullptr, ELMRNN_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    elmrnn_opts o;
+    elmrnn_opts_default(&o);
+    if (opts) o = *opts;
+    if (arch < ELMRNN_ELMAN || arch > ELMRNN_GRU) return fail(nullptr, ELMRNN_ERR_ARG, "arch out of range");
+    if (d < 1 || M < 1 || Q < 1) return fail(nullptr, ELMRNN_ERR_ARG, "d, M and Q must be >= 1");
+    if (o.F < 0) o.F = Q;
+    if (o.R < 0) o.R = Q;
+    if (o.fc_lags < 0) o.fc_lags = Q;
+    if (o.act < 0 || o.act > 1 || o.rec_scale < 0 || o.rec_scale > 1 || o.weight_grid < 0 || o.weight_grid > 2 ||
+        o.force_path < 0 || o.force_path > 2 || o.fc_lags < 1)
+        return fail(nullptr, ELMRNN_ERR_ARG, "invalid option value");
+    if (arch == ELMRNN_ELMAN && !elman_supported(Q))
+        return fail(nullptr, ELMRNN_ERR_UNSUPPORTED, "Elman supports Q <= 128");
+    if (M > 1023) return fail(nullptr, ELMRNN_ERR_UNSUPPORTED, "M <= 1023 (TSQR: one thread per column of [H|Y])");
+
+    elmrnn* h = new (std::nothrow) elmrnn();
+    if (!h) return fail(nullptr, ELMRNN_ERR_OOM, "host allocation failed");
+    h->arch = arch; h->S = d; h->M = M; h->Q = Q; h->F = o.F; h->R = o.R; h->act = o.act;
+    h->fc_lags = o.fc_lags; h->rec_scale = o.rec_scale; h->weight_grid = o.weight_grid;
+    h->force_path = o.force_path; h->seed = seed; h->G = gates_of(arch); h->stream = nullptr;
+    h->path = 1;
+    cudaError_t e;
+    if ((e = cudaGetDevice(&h->device))) { elmrnn_destroy(h); return cuda_fail(nullptr, e, "cudaGetDevice"); }
+    if ((e = cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device))) {
+        elmrnn_destroy(h);
+        return cuda_fail(nullptr, e, "cudaDeviceGetAttribute");
+    }
+    const int64_t GM = (int64_t)h->G * M;
+    switch (arch) {
+    case ELMRNN_ELMAN: case ELMRNN_JORDAN: h->rec_len = (int64_t)Q * M; break;
+    case ELMRNN_NARMAX: h->rec_len = (int64_t)(o.F > 0 ? o.F : 1) * M; break;
+    case ELMRNN_FC: h->rec_len = (int64_t)o.fc_lags * M * M; break;
+    default: h->rec_len = (int64_t)M * GM; break;
+    }
+    if ((e = cudaMalloc(&h->W, sizeof(float) * d * GM)) || (e = cudaMalloc(&h->b, sizeof(float) * GM)) ||
+        (e = cudaMalloc(&h->rec, sizeof(float) * h->rec_len))) {
+        elmrnn_destroy(h);
+        return cuda_fail(nullptr, e, "weight allocation");
+    }
+    if ((e = gen_weights(h))) { elmrnn_destroy(h); return cuda_fail(nullptr, e, "gen_weights"); }
+    // H-builder choice: tensor cores when the recurrence is a real dense
+    // contraction, else FP32 FMA.
+    if ((arch == ELMRNN_LSTM || arch == ELMRNN_GRU || arch == ELMRNN_FC) && o.force_path != 1 && tc_supported(h) &&
+        (o.force_path == 2 || M >= 128)) {
+        if ((e = tc_prepare(h))) { elmrnn_destroy(h); return cuda_fail(nullptr, e, "tc_prepare"); }
+        h->path = 2;
+    } else if (o.force_path == 2) {
+        elmrnn_destroy(h);
+        return fail(nullptr, ELMRNN_ERR_UNSUPPORTED, "tensor-core path not available for this shape");
+    }
+    if ((e = cudaStreamSynchronize(h->stream))) { elmrnn_destroy(h); return cuda_fail(nullptr, e, "init sync"); }
+    *out = h;
+    return ELMRNN_OK;
+}
+
+elmrnn_status elmrnn_set_stream(elmrnn_t h, void* s) {
+    if (!h) return ELMRNN_ERR_ARG;
+    h->stream = reinterpret_cast<cudaStream_t>(s);
+    return ELMRNN_OK;
+}
+
+static elmrnn_status build_impl(elmrnn* h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy, int64_t N,
+                                float* H, int64_t ldh) {
+    cudaError_t e;
+    switch (h->arch) {
+    case ELMRNN_ELMAN: e = launch_elman(h, X, ldx, N, H, ldh); break;
+    case ELMRNN_JORDAN: case ELMRNN_NARMAX: e = launch_teacher_forced(h, X, ldx, Yfb, ldy, N, H, ldh); break;
+    default:
+        e = h->path == 2 ? launch_dense_tc(h, X, ldx, N, H, ldh) : launch_dense_fma(h, X, ldx, N, H, ldh);
+        if (e == cudaErrorInvalidConfiguration)
+            return fail(h, ELMRNN_ERR_UNSUPPORTED, "recurrent state of one sample tile does not fit on chip");
+        break;
+    }
+    if (e) return cuda_fail(h, e, "build_H");
+    return ELMRNN_OK;
+}
+
+elmrnn_status elmrnn_build_H(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy, int64_t N,
+                             float* H, int64_t ldh) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (N < 0) return fail(h, ELMRNN_ERR_ARG, "N < 0");
+    if (N == 0) return ELMRNN_OK;
+    if (!X || !H) return fail(h, ELMRNN_ERR_ARG, "X or H is NULL");
+    if (ldx < (int64_t)h->Q * h->S) return fail(h, ELMRNN_ERR_SHAPE, "ldx < Q*d");
+    if (ldh < h->M) return fail(h, ELMRNN_ERR_SHAPE, "ldh < M");
+    if (Yfb && ldy < h->Q) return fail(h, ELMRNN_ERR_SHAPE, "ldy < Q");
+    if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(H)) & 3)
+        return fail(h, ELMRNN_ERR_SHAPE, "pointers must be 4-byte aligned");
+    return build_impl(h, X, ldx, Yfb, ldy, N, H, ldh);
+}
+
+static elmrnn_status finish_solve(elmrnn* h, elmrnn_solve_info* info) {
+    cudaError_t e;
+    if (!info) {
+        if ((e = cudaGetLastError())) return cuda_fail(h, e, "solve");
+        return ELMRNN_OK;
+    }
+    if ((e = cudaMemcpyAsync(h->shost, h->sdev, sizeof(SolveDev), cudaMemcpyDeviceToHost, h->stream)) ||
+        (e = cudaStreamSynchronize(h->stream)))
+        return cuda_fail(h, e, "solve");
+    const SolveDev& s = *h->shost;
+    info->rho = s.rho; info->rmse = s.rmse; info->rdiag_min_abs = s.dmin; info->rdiag_max_abs = s.dmax;
+    info->ridge_lambda = s.lambda; info->rank_flag = s.rank_flag; info->n_total = s.n_total;
+    if (s.nonfinite) return fail(h, ELMRNN_ERR_NONFINITE, "NaN or Inf in H or Y");
+    return s.rank_flag ? ELMRNN_WARN_RIDGE : ELMRNN_OK;
+}
+
+elmrnn_status elmrnn_solve_beta(elmrnn_t h, const float* H, int64_t ldh, const float* Y, int64_t N, double* beta,
+                                elmrnn_solve_info* info) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (!H || !Y || !beta) return fail(h, ELMRNN_ERR_ARG, "NULL pointer");
+    if (ldh < h->M) return fail(h, ELMRNN_ERR_SHAPE, "ldh < M");
+    if (N < h->M) return fail(h, ELMRNN_ERR_UNDERDETERMINED, "N < M");
+    cudaError_t e;
+    if ((e = tsqr_factor(h, H, ldh, Y, N))) return cuda_fail(h, e, "tsqr_factor");
+    if ((e = tsqr_solve(h, N, beta))) return cuda_fail(h, e, "tsqr_solve");
+    return finish_solve(h, info);
+}
+
+elmrnn_status elmrnn_solve_local(elmrnn_t h, const float* H, int64_t ldh, const float* Y, int64_t N, double* Rpk) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (!Rpk || N < 0 || (N > 0 && (!H || !Y))) return fail(h, ELMRNN_ERR_ARG, "bad argument");
+    if (ldh < h->M) return fail(h, ELMRNN_ERR_SHAPE, "ldh < M");
+    cudaError_t e;
+    if ((e = tsqr_factor(h, H, ldh, Y, N))) return cuda_fail(h, e, "tsqr_factor");
+    if ((e = tsqr_pack(h, Rpk))) return cuda_fail(h, e, "tsqr_pack");
+    return ELMRNN_OK;
+}
+
+elmrnn_status elmrnn_solve_merge(elmrnn_t h, const double* Rpk_all, int P, int64_t N_total, double* beta,
+                                 elmrnn_solve_info* info) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (!Rpk_all || !beta || P < 1) return fail(h, ELMRNN_ERR_ARG, "bad argument");
+    if (N_total < h->M) return fail(h, ELMRNN_ERR_UNDERDETERMINED, "N_total < M");
+    cudaError_t e;
+    if ((e = tsqr_merge_packed(h, Rpk_all, P))) return cuda_fail(h, e, "tsqr_merge");
+    if ((e = tsqr_solve(h, N_total, beta))) return cuda_fail(h, e, "tsqr_solve");
+    return finish_solve(h, info);
+}
+
+int64_t elmrnn_packed_r_len(elmrnn_t h) {
+    if (!h) return -1;
+    return (int64_t)(h->M + 1) * (h->M + 2) / 2;
+}
+
+elmrnn_status elmrnn_predict(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy, int64_t N,
+                             const double* beta, float* Yhat) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (N < 0) return fail(h, ELMRNN_ERR_ARG, "N < 0");
+    if (N == 0) return ELMRNN_OK;
+    if (!X || !beta || !Yhat) return fail(h, ELMRNN_ERR_ARG, "NULL pointer");
+    if (ldx < (int64_t)h->Q * h->S) return fail(h, ELMRNN_ERR_SHAPE, "ldx < Q*d");
+    if (Yfb && ldy < h->Q) return fail(h, ELMRNN_ERR_SHAPE, "ldy < Q");
+    cudaError_t e;
+    if (N > h->Hws_rows) {
+        if (h->Hws) cudaFree(h->Hws);
+        h->Hws = nullptr;
+        h->Hws_rows = 0;
+        if ((e = cudaMalloc(&h->Hws, sizeof(float) * N * h->M))) return cuda_fail(h, e, "predict workspace");
+        h->Hws_rows = N;
+    }
+    elmrnn_status st = build_impl(h, X, ldx, Yfb, ldy, N, h->Hws, h->M);
+    if (st != ELMRNN_OK) return st;
+    if ((e = launch_predict_gemv(h, h->Hws, h->M, N, beta, Yhat))) return cuda_fail(h, e, "predict");
+    return ELMRNN_OK;
+}
+
+int64_t elmrnn_weight_block_len(elmrnn_t h, int block_id) {
+    if (!h) return -1;
+    return logical_block_len(h, block_id);
+}
+
+elmrnn_status elmrnn_get_weights(elmrnn_t h, int block_id, float* host_dst, int64_t count) {
+    if (!h) return ELMRNN_ERR_ARG;
+    int64_t len = logical_block_len(h, block_id);
+    if (len < 0 || !host_dst || count != len) return fail(h, ELMRNN_ERR_ARG, "bad block id or count");
+    if (len == 0) return ELMRNN_OK;
+    float* tmp = nullptr;
+    cudaError_t e;
+    if ((e = cudaMalloc(&tmp, sizeof(float) * len))) return cuda_fail(h, e, "get_weights");
+    int64_t n = 0;
+    e = gen_logical_block(h, block_id, tmp, &n);
+    if (!e) e = cudaMemcpyAsync(host_dst, tmp, sizeof(float) * len, cudaMemcpyDeviceToHost, h->stream);
+    if (!e) e = cudaStreamSynchronize(h->stream);
+    cudaFree(tmp);
+    if (e) return cuda_fail(h, e, "get_weights");
+    return ELMRNN_OK;
+}
+
+int elmrnn_path(elmrnn_t h) { return h ? h->path : 0; }
+
+int64_t elmrnn_launch_count(elmrnn_t h) { return h ? h->launches : -1; }
+
+const char* elmrnn_last_error(elmrnn_t h) { return h ? h->err.c_str() : g_init_error.c_str(); }
+
+void elmrnn_destroy(elmrnn_t h) {
+    if (!h) return;
+    cudaFree(h->W); cudaFree(h->b); cudaFree(h->rec); cudaFree(h->tc_ops);
+    cudaFree(h->Rws); cudaFree(h->sdev); cudaFree(h->flag); cudaFree(h->Hws); cudaFree(h->scratch);
+    if (h->shost) cudaFreeHost(h->shost);
+    delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// common.cuh -- internal declarations of libelmrnn (not part of the ABI).
+// The public contract is include/elmrnn.h; citations "P:n" = PAPER.md line n.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+
+#include "elmrnn.h"
+
+namespace elm {
+
+constexpr int kArchElman = 0, kArchJordan = 1, kArchNarmax = 2, kArchFC = 3, kArchLSTM = 4, kArchGRU = 5;
+
+inline int gates_of(int arch) { return arch == kArchLSTM ? 4 : (arch == kArchGRU ? 3 : 1); }
+
+// Device-side solve diagnostics (copied to the host struct on request).
+struct SolveDev {
+    double rho, rmse, dmin, dmax, lambda;
+    int rank_flag;
+    int nonfinite;
+    long long n_total;
+};
+
+}  // namespace elm
+
+// The opaque handle.  Weights are stored in kernel-friendly packed layouts
+// (DESIGN.md "Data layout in HBM"); the logical blocks are regenerated on
+// demand by elmrnn_get_weights.
+struct elmrnn {
+    int arch, S, M, Q, F, R, act, fc_lags, rec_scale, weight_grid, force_path;
+    int G;                // gate blocks
+    uint64_t seed;
+    int device, sm_count;
+    cudaStream_t stream;
+    int path;             // 1 FMA, 2 tensor cores
+    // packed weights (device)
+    float* W;             // [S][G*M]
+    float* b;             // [G*M]
+    float* rec;           // Elman/Jordan alpha^T [Q][M]; NARMAX W'^T [F][M]; FC A [L][M][M];
+                          // LSTM/GRU U_cat [M][G*M] (U_cat[k][g*M+j] = U_g[k][j])
+    int64_t rec_len;
+    // tensor-core operands (device; only when path == 2)
+    void* tc_ops;
+    size_t tc_ops_bytes;
+    // solve workspace (device)
+    double* Rws;          // slabs of (M+1)^2 doubles
+    int64_t Rws_slabs;
+    elm::SolveDev* sdev;  // device diagnostics
+    int* flag;            // device non-finite flag
+    elm::SolveDev* shost; // pinned host mirror
+    float* Hws;           // predict scratch
+    int64_t Hws_rows;
+    float* scratch;       // builder scratch (FC history ring)
+    size_t scratch_bytes;
+    int64_t launches;
+    std::string err;
+};
+
+namespace elm {
+
+// ---- weights (weights.cu) -------------------------------------------------
+cudaError_t gen_weights(elmrnn* h);
+cudaError_t gen_logical_block(elmrnn* h, int block_id, float* dst_dev, int64_t* count);
+int64_t logical_block_len(const elmrnn* h, int block_id);
+int num_blocks(int arch);
+
+// ---- H builders --------------------------------------------------------------
+cudaError_t launch_elman(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
+cudaError_t launch_teacher_forced(elmrnn* h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy,
+                                  int64_t N, float* H, int64_t ldh);
+cudaError_t launch_dense_fma(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
+bool elman_supported(int Q);
+
+// ---- tensor-core builder (hbuild_dense_tc.cu) -----------------------------
+bool tc_supported(const elmrnn* h);
+cudaError_t tc_prepare(elmrnn* h);
+cudaError_t launch_dense_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
+
+// ---- TSQR (tsqr.cu) ------------------------------------------------------------
+// Fold [H | Y] rows into per-CTA R slabs and reduce them to slab 0 (full storage).
+cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t N);
+cudaError_t tsqr_pack(elmrnn* h, double* Rpk);
+cudaError_t tsqr_merge_packed(elmrnn* h, const double* Rpk_all, int P);
+cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta);
+cudaError_t ensure_solve_ws(elmrnn* h, int64_t slabs);
+int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N);
+cudaError_t launch_predict_gemv(elmrnn* h, const float* H, int64_t ldh, int64_t N, const double* beta, float* yhat);
+
+}  // namespace elm
+
+// ---- small device helpers ------------------------------------------------------
+#ifdef __CUDACC__
+namespace elm {
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// Activations (R3).  The H builders use the accurate forms: the beta of an
+// ill-conditioned [H|Y] (cond(H) ~ 1e6 on smooth series) amplifies every ulp
+// of H, so H is kept within ~1-2 ulp of the rounded fp64 value.
+//   sigma(a) = 1 / (1 + e^-a)  (expf: <= 2 ulp; IEEE division)
+//   tanh(a)  = tanhf(a)        (<= 2 ulp)
+__device__ __forceinline__ float sigmoidf_(float a) { return 1.0f / (1.0f + expf(-a)); }
+__device__ __forceinline__ float tanhf_(float a) { return tanhf(a); }
+__device__ __forceinline__ float act_g(float a, int act) { return act == 1 ? tanhf_(a) : sigmoidf_(a); }
+// fp64 forms for the latency-bound per-cell builders
+__device__ __forceinline__ double sigmoid64(double a) { return 1.0 / (1.0 + exp(-a)); }
+__device__ __forceinline__ double act_g64(double a, int act) { return act == 1 ? tanh(a) : sigmoid64(a); }
+// Fast MUFU forms (ex2.approx / rcp.approx, ~2 ulp each) for epilogues that
+// are MUFU bound; accuracy validated by the parity tests of the kernel using them.
+__device__ __forceinline__ float sigmoid_fast(float a) {
+    return rcp_approx(1.0f + ex2_approx(-1.4426950408889634f * a));
+}
+__device__ __forceinline__ float tanh_fast(float a) {
+    return 1.0f - 2.0f * rcp_approx(1.0f + ex2_approx(2.8853900817779268f * a));
+}
+}  // namespace elm
+#endif

@@ -1,0 +1,404 @@
+// tsqr.cu -- fp64 Householder tall-skinny QR of [H | Y], Q^T Y by the same
+// reflectors, and back substitution: S4.2 of the paper, "H = QR,
+// z = Q^T Y, R beta = z by back substitution".  The paper delegates this to a
+// Numba/NumPy library call; here it is three kernels:
+//
+//  k_tsqr_leaf   persistent CTAs, each owning a contiguous row block and an
+//                (M+1)x(M+1) R slab (full storage, L2 resident).  Row tiles of
+//                TR rows are folded in: R <- R-factor of [R; tile] by the
+//                structured Householder sweep (LAPACK tpqrt semantics).  The
+//                tile lives in registers: thread j owns column j of the tile
+//                (TR doubles) and column j of R, so R needs no inter-thread
+//                synchronisation; the reflector v (TR doubles) of column k is
+//                broadcast through shared memory, one barrier per column,
+//                with one-column look-ahead (the owner of k+1 builds its
+//                reflector right after its own update).
+//  k_tsqr_merge  one level of a binary tree: slab c absorbs slab c+stride by
+//                folding it in TR-row tiles, skipping the zero columns left of
+//                each tile's diagonal.
+//  k_tsqr_solve  one CTA: sign normalisation (R18), rank check + ridge
+//                fallback by folding sqrt(lambda) (I|0) rows (R19), back
+//                substitution, rho = ||R_aug [beta; -1]|| = ||H beta - Y||.
+//
+// All arithmetic is fp64 (reading R20: an fp32 streaming fold breaks the beta
+// tolerance); H and Y are read as fp32 and widened exactly.
+#include <cfloat>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace elm {
+
+template <int TR>
+struct TrBounds { static constexpr int threads = TR >= 32 ? 384 : 1024; };
+
+// Build the Householder reflector of column k from x0 = R[k][k] and the tile
+// column a[0..TR) (LAPACK dlarfg convention, sign(0) = +1).
+template <int TR>
+__device__ __forceinline__ void make_reflector(const double (&a)[TR], double x0, double* v, double* tau,
+                                               double* Rkk) {
+    double s2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < TR; ++i) s2 = fma(a[i], a[i], s2);
+    if (s2 == 0.0) {
+        *tau = 0.0;
+        return;
+    }
+    double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * sqrt(fma(x0, x0, s2));
+    *tau = (beta - x0) / beta;
+    double sc = 1.0 / (x0 - beta);
+#pragma unroll
+    for (int i = 0; i < TR; ++i) v[i] = a[i] * sc;
+    *Rkk = beta;
+}
+
+// Fold the register tile a (thread j = column j) into R (n x n, full storage),
+// columns k0..n-1.  vbuf: 2*TR doubles of shared memory, taus: 2 doubles.
+template <int TR>
+__device__ void fold_tile(double (&a)[TR], int n, int k0, double* __restrict__ R, double* vbuf, double* taus) {
+    const int j = threadIdx.x;
+    const bool own = j < n;
+    double rnext = (own && j >= k0) ? R[(size_t)k0 * n + j] : 0.0;
+    if (j == k0) make_reflector<TR>(a, rnext, vbuf + (k0 & 1) * TR, taus + (k0 & 1), R + (size_t)k0 * n + k0);
+    __syncthreads();
+    for (int k = k0; k < n; ++k) {
+        const double rkj = rnext;
+        if (own && j > k && k + 1 < n) rnext = R[(size_t)(k + 1) * n + j];
+        const double tau = taus[k & 1];
+        if (own && j > k && tau != 0.0) {
+            const double* v = vbuf + (k & 1) * TR;
+            double w = rkj;
+#pragma unroll
+            for (int i = 0; i < TR; ++i) w = fma(v[i], a[i], w);
+            const double tw = tau * w;
+            R[(size_t)k * n + j] = rkj - tw;
+#pragma unroll
+            for (int i = 0; i < TR; ++i) a[i] = fma(-tw, v[i], a[i]);
+        }
+        if (j == k + 1 && k + 1 < n)
+            make_reflector<TR>(a, rnext, vbuf + ((k + 1) & 1) * TR, taus + ((k + 1) & 1),
+                               R + (size_t)(k + 1) * n + (k + 1));
+        __syncthreads();
+    }
+}
+
+template <int TR>
+__global__ void __launch_bounds__(TrBounds<TR>::threads) k_tsqr_leaf(const float* __restrict__ H, int64_t ldh,
+                                                    const float* __restrict__ Y, int64_t N, int M,
+                                                    double* __restrict__ Rws, int64_t rows_per_cta,
+                                                    int* __restrict__ flag) {
+    __shared__ double vbuf[2 * TR];
+    __shared__ double taus[2];
+    const int n = M + 1, j = threadIdx.x;
+    double* R = Rws + (size_t)blockIdx.x * n * n;
+    if (j < n)
+        for (int k = 0; k < n; ++k) R[(size_t)k * n + j] = 0.0;   // column j is private to thread j
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+    const int64_t r1 = min(N, r0 + rows_per_cta);
+    bool bad = false;
+    for (int64_t base = r0; base < r1; base += TR) {
+        double a[TR];
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+            const int64_t row = base + i;
+            float v = 0.0f;
+            if (row < r1 && j < n) v = (j < M) ? __ldg(H + row * ldh + j) : __ldg(Y + row);
+            bad |= !isfinite(v);
+            a[i] = (double)v;
+        }
+        fold_tile<TR>(a, n, 0, R, vbuf, taus);
+    }
+    if (bad) atomicOr(flag, 1);
+}
+
+template <int TR>
+__global__ void __launch_bounds__(TrBounds<TR>::threads) k_tsqr_merge(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n) {
+    __shared__ double vbuf[2 * TR];
+    __shared__ double taus[2];
+    const int64_t c = (int64_t)blockIdx.x * 2 * stride, partner = c + stride;
+    if (partner >= slabs) return;
+    double* Ra = Rws + (size_t)c * n * n;
+    const double* Rb = Rws + (size_t)partner * n * n;
+    const int j = threadIdx.x;
+    for (int s = 0; s * TR < n; ++s) {
+        double a[TR];
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+            const int row = s * TR + i;
+            a[i] = (row < n && j < n && j >= row) ? Rb[(size_t)row * n + j] : 0.0;
+        }
+        fold_tile<TR>(a, n, s * TR, Ra, vbuf, taus);
+    }
+}
+
+// Unpack P packed R factors (row k holds R[k][k..n-1]) into full slabs.
+__global__ void k_unpack(const double* __restrict__ Rpk, int P, int n, double* __restrict__ Rws) {
+    const int64_t len = (int64_t)n * n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)P * len;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = e / len, rem = e - p * len;
+        int k = (int)(rem / n), j = (int)(rem - (int64_t)k * n);
+        double v = 0.0;
+        if (j >= k) v = Rpk[p * ((int64_t)n * (n + 1) / 2) + (int64_t)k * n - (int64_t)k * (k - 1) / 2 + (j - k)];
+        Rws[e] = v;
+    }
+}
+
+__global__ void k_pack(const double* __restrict__ R, int n, double* __restrict__ Rpk) {
+    const int64_t len = (int64_t)n * (n + 1) / 2;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
+        // row k: offset k*n - k(k-1)/2 ; find k by search (n <= 1024, cheap)
+        int lo = 0, hi = n - 1;
+        while (lo < hi) {
+            int mid = (lo + hi + 1) / 2;
+            if ((int64_t)mid * n - (int64_t)mid * (mid - 1) / 2 <= e) lo = mid; else hi = mid - 1;
+        }
+        int k = lo;
+        int j = k + (int)(e - ((int64_t)k * n - (int64_t)k * (k - 1) / 2));
+        Rpk[e] = R[(size_t)k * n + j];
+    }
+}
+
+__device__ double block_sum(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int i = 0; i < nw; ++i) s += red[i];
+    __syncthreads();
+    return s;
+}
+__device__ double block_min(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double s = INFINITY;
+    for (int i = 0; i < nw; ++i) s = fmin(s, red[i]);
+    __syncthreads();
+    return s;
+}
+__device__ double block_max(double v, double* red) { return -block_min(-v, red); }
+
+// Final solve on slab 0 (one CTA, blockDim >= n).  R0 is copied to Rorig
+// before a ridge refactorisation so rho is measured on the unregularised R.
+template <int TR>
+__global__ void __launch_bounds__(TrBounds<TR>::threads) k_tsqr_solve(double* __restrict__ R, double* __restrict__ Rorig, int M,
+                                                     long long n_total, const int* __restrict__ flag,
+                                                     double* __restrict__ beta, SolveDev* __restrict__ out) {
+    __shared__ double vbuf[2 * TR];
+    __shared__ double taus[2];
+    __shared__ double red[32];
+    __shared__ double bk;
+    extern __shared__ double zs[];   // [n] right-hand side / beta
+    const int n = M + 1, j = threadIdx.x;
+    const bool own = j < n;
+    // sign normalisation: flip row k when R_kk < 0 (thread j flips its column
+    // entries; the signs are read into shared memory first)
+    if (own) zs[j] = R[(size_t)j * n + j] < 0.0 ? -1.0 : 1.0;
+    __syncthreads();
+    if (own)
+        for (int k = 0; k <= j; ++k) R[(size_t)k * n + j] *= zs[k];
+    __syncthreads();
+    double d = (j < M) ? fabs(R[(size_t)j * n + j]) : INFINITY;
+    double dmin = block_min(d, red);
+    double dmax = block_max(j < M ? d : 0.0, red);
+    double f2 = 0.0;
+    if (j < M)
+        for (int k = 0; k <= j; ++k) f2 += R[(size_t)k * n + j] * R[(size_t)k * n + j];
+    double fro2 = block_sum(f2, red);
+    const bool ridge = !(dmin > DBL_EPSILON * (double)M * dmax);
+    double lambda = 0.0;
+    if (own)
+        for (int k = 0; k < n; ++k) Rorig[(size_t)k * n + j] = R[(size_t)k * n + j];
+    if (ridge) {
+        lambda = 1e-8 * fro2 / (double)M;
+        const double sl = sqrt(lambda);
+        for (int s = 0; s * TR < M; ++s) {
+            double a[TR];
+#pragma unroll
+            for (int i = 0; i < TR; ++i) a[i] = (s * TR + i < M && j == s * TR + i) ? sl : 0.0;
+            fold_tile<TR>(a, n, s * TR, R, vbuf, taus);
+        }
+        if (own) zs[j] = R[(size_t)j * n + j] < 0.0 ? -1.0 : 1.0;
+        __syncthreads();
+        if (own)
+            for (int k = 0; k <= j; ++k) R[(size_t)k * n + j] *= zs[k];
+        __syncthreads();
+    }
+    // back substitution: thread i holds z_i
+    if (j < M) zs[j] = R[(size_t)j * n + M];
+    __syncthreads();
+    for (int k = M - 1; k >= 0; --k) {
+        if (j == 0) bk = zs[k] / R[(size_t)k * n + k];
+        __syncthreads();
+        if (j < k) zs[j] -= R[(size_t)j * n + k] * bk;
+        if (j == k) zs[k] = bk;
+        __syncthreads();
+    }
+    if (j < M) beta[j] = zs[j];
+    // rho = || R_orig [beta; -1] ||
+    double s = 0.0;
+    if (own) {
+        for (int c = j; c < M; ++c) s += Rorig[(size_t)j * n + c] * zs[c];
+        s -= Rorig[(size_t)j * n + M];
+    }
+    double rho2 = block_sum(own ? s * s : 0.0, red);
+    if (j == 0) {
+        out->rho = sqrt(rho2);
+        out->rmse = sqrt(rho2) / sqrt((double)n_total);
+        out->dmin = dmin;
+        out->dmax = dmax;
+        out->lambda = lambda;
+        out->rank_flag = ridge ? 1 : 0;
+        out->nonfinite = *flag;
+        out->n_total = n_total;
+    }
+}
+
+// ---- host side ---------------------------------------------------------------------
+
+// TR = 32 keeps the tile in ~160 registers per thread (n <= 384 threads);
+// wider problems use TR = 16 under the 1024-thread register budget.
+static int pick_tr(int n) { return n <= 384 ? 32 : 16; }
+
+template <int TR>
+static int leaf_ctas_per_sm(int threads) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tsqr_leaf<TR>, threads, 0);
+    return per_sm < 1 ? 1 : per_sm;
+}
+
+int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
+    const int n = h->M + 1, TR = pick_tr(n), threads = (n + 31) / 32 * 32;
+    int per_sm = TR == 32 ? leaf_ctas_per_sm<32>(threads) : leaf_ctas_per_sm<16>(threads);
+    int64_t maxc = (int64_t)per_sm * h->sm_count;
+    int64_t byrows = (N + TR - 1) / TR;
+    int64_t g = byrows < maxc ? byrows : maxc;
+    return g < 1 ? 1 : g;
+}
+
+cudaError_t ensure_solve_ws(elmrnn* h, int64_t slabs) {
+    cudaError_t e;
+    const int n = h->M + 1;
+    if (slabs + 1 > h->Rws_slabs) {   // +1: Rorig copy for the final solve
+        if (h->Rws) cudaFree(h->Rws);
+        h->Rws = nullptr;
+        h->Rws_slabs = 0;
+        if ((e = cudaMalloc(&h->Rws, (size_t)(slabs + 1) * n * n * sizeof(double)))) return e;
+        h->Rws_slabs = slabs + 1;
+    }
+    if (!h->sdev) {
+        if ((e = cudaMalloc(&h->sdev, sizeof(SolveDev)))) return e;
+        if ((e = cudaMalloc(&h->flag, sizeof(int)))) return e;
+        if ((e = cudaMallocHost(&h->shost, sizeof(SolveDev)))) return e;
+    }
+    return cudaSuccess;
+}
+
+template <int TR>
+static cudaError_t tree_reduce(elmrnn* h, int64_t slabs) {
+    const int n = h->M + 1, threads = (n + 31) / 32 * 32;
+    for (int64_t stride = 1; stride < slabs; stride *= 2) {
+        int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
+        k_tsqr_merge<TR><<<(unsigned)pairs, threads, 0, h->stream>>>(h->Rws, slabs, stride, n);
+        h->launches++;
+    }
+    return cudaGetLastError();
+}
+
+static cudaError_t tree(elmrnn* h, int64_t slabs) {
+    switch (pick_tr(h->M + 1)) {
+    case 32: return tree_reduce<32>(h, slabs);
+    default: return tree_reduce<16>(h, slabs);
+    }
+}
+
+template <int TR>
+static cudaError_t leaf(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t N, int64_t slabs) {
+    const int n = h->M + 1, threads = (n + 31) / 32 * 32;
+    int64_t rows = (N + slabs - 1) / slabs;
+    rows = (rows + TR - 1) / TR * TR;
+    k_tsqr_leaf<TR><<<(unsigned)slabs, threads, 0, h->stream>>>(H, ldh, Y, N, h->M, h->Rws, rows, h->flag);
+    h->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t N) {
+    int64_t slabs = tsqr_leaf_slabs(h, N);
+    cudaError_t e;
+    if ((e = ensure_solve_ws(h, slabs))) return e;
+    if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream))) return e;
+    switch (pick_tr(h->M + 1)) {
+    case 32: e = leaf<32>(h, H, ldh, Y, N, slabs); break;
+    default: e = leaf<16>(h, H, ldh, Y, N, slabs); break;
+    }
+    if (e) return e;
+    return tree(h, slabs);
+}
+
+cudaError_t tsqr_pack(elmrnn* h, double* Rpk) {
+    const int n = h->M + 1;
+    int64_t len = (int64_t)n * (n + 1) / 2;
+    int blocks = (int)((len + 255) / 256);
+    if (blocks > 1024) blocks = 1024;
+    k_pack<<<blocks, 256, 0, h->stream>>>(h->Rws, n, Rpk);
+    h->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t tsqr_merge_packed(elmrnn* h, const double* Rpk_all, int P) {
+    const int n = h->M + 1;
+    cudaError_t e;
+    if ((e = ensure_solve_ws(h, P))) return e;
+    if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream))) return e;
+    int64_t total = (int64_t)P * n * n;
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 4096) blocks = 4096;
+    k_unpack<<<blocks, 256, 0, h->stream>>>(Rpk_all, P, n, h->Rws);
+    h->launches++;
+    if ((e = cudaGetLastError())) return e;
+    return tree(h, P);
+}
+
+template <int TR>
+static cudaError_t solve_t(elmrnn* h, int64_t n_total, double* beta) {
+    const int n = h->M + 1, threads = (n + 31) / 32 * 32;
+    double* Rorig = h->Rws + (size_t)(h->Rws_slabs - 1) * n * n;
+    k_tsqr_solve<TR><<<1, threads, n * sizeof(double), h->stream>>>(h->Rws, Rorig, h->M, (long long)n_total, h->flag,
+                                                                     beta, h->sdev);
+    h->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta) {
+    switch (pick_tr(h->M + 1)) {
+    case 32: return solve_t<32>(h, n_total, beta);
+    default: return solve_t<16>(h, n_total, beta);
+    }
+}
+
+// ---- predict: Eq. 4, yhat_i = sum_j beta_j H[i][j] ------------------------
+__global__ void k_predict_gemv(const float* __restrict__ H, int64_t ldh, int64_t N, int M,
+                               const double* __restrict__ beta, float* __restrict__ yhat) {
+    const int lane = threadIdx.x & 31;
+    int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (row >= N) return;
+    double s = 0.0;
+    for (int j = lane; j < M; j += 32) s = fma((double)H[row * ldh + j], beta[j], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) yhat[row] = (float)s;
+}
+
+cudaError_t launch_predict_gemv(elmrnn* h, const float* H, int64_t ldh, int64_t N, const double* beta, float* yhat) {
+    int64_t threads = N * 32;
+    int64_t blocks = (threads + 255) / 256;
+    k_predict_gemv<<<(unsigned)blocks, 256, 0, h->stream>>>(H, ldh, N, h->M, beta, yhat);
+    h->launches++;
+    return cudaGetLastError();
+}
+
+}  // namespace elm

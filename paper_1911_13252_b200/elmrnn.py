@@ -1,0 +1,257 @@
+"""Thin ctypes binding of libelmrnn.so (include/elmrnn.h), same names.
+
+Argument marshalling only: torch tensors -> device pointers + leading
+dimensions, the current torch CUDA stream -> the handle's stream.  Every
+arithmetic step runs in the library's CUDA kernels.  There is no fallback:
+if the shared library is missing or the device is not a CUDA device, calls
+raise.  (PAPER.md = arXiv 1911.13252; see the header for the citations.)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libelmrnn.so")
+
+ARCHS = {"elman": 0, "jordan": 1, "narmax": 2, "fc": 3, "lstm": 4, "gru": 5}
+STATUS = {0: "OK", 1: "WARN_RIDGE", -1: "ERR_ARG", -2: "ERR_SHAPE", -3: "ERR_UNDERDETERMINED",
+          -4: "ERR_NONFINITE", -5: "ERR_UNSUPPORTED", -6: "ERR_CUDA", -7: "ERR_OOM"}
+
+EXPORTED = ("elmrnn_opts_default", "elmrnn_init", "elmrnn_init_ex", "elmrnn_set_stream", "elmrnn_build_H",
+            "elmrnn_solve_beta", "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_packed_r_len",
+            "elmrnn_predict", "elmrnn_get_weights", "elmrnn_weight_block_len", "elmrnn_path",
+            "elmrnn_launch_count", "elmrnn_last_error", "elmrnn_destroy")
+
+
+class ElmrnnError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("F", ctypes.c_int), ("R", ctypes.c_int), ("act", ctypes.c_int), ("rec_scale", ctypes.c_int),
+                ("weight_grid", ctypes.c_int), ("fc_lags", ctypes.c_int), ("force_path", ctypes.c_int)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("rho", ctypes.c_double), ("rmse", ctypes.c_double), ("rdiag_min_abs", ctypes.c_double),
+                ("rdiag_max_abs", ctypes.c_double), ("ridge_lambda", ctypes.c_double), ("rank_flag", ctypes.c_int),
+                ("n_total", ctypes.c_int64)]
+
+
+@dataclass
+class SolveInfo:
+    rho: float
+    rmse: float
+    rdiag_min_abs: float
+    rdiag_max_abs: float
+    ridge_lambda: float
+    rank_flag: int
+    n_total: int
+    status: int
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libelmrnn.so (build it first with paper_1911_13252_b200.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_1911_13252_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, i32, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_uint64
+        L.elmrnn_opts_default.argtypes = [vp]
+        L.elmrnn_opts_default.restype = None
+        L.elmrnn_init.argtypes = [vp, i32, i32, i32, i32, u64]
+        L.elmrnn_init_ex.argtypes = [vp, i32, i32, i32, i32, u64, vp]
+        L.elmrnn_set_stream.argtypes = [vp, vp]
+        L.elmrnn_build_H.argtypes = [vp, vp, i64, vp, i64, i64, vp, i64]
+        L.elmrnn_solve_beta.argtypes = [vp, vp, i64, vp, i64, vp, vp]
+        L.elmrnn_solve_local.argtypes = [vp, vp, i64, vp, i64, vp]
+        L.elmrnn_solve_merge.argtypes = [vp, vp, i32, i64, vp, vp]
+        L.elmrnn_packed_r_len.argtypes = [vp]
+        L.elmrnn_packed_r_len.restype = i64
+        L.elmrnn_predict.argtypes = [vp, vp, i64, vp, i64, i64, vp, vp]
+        L.elmrnn_get_weights.argtypes = [vp, i32, vp, i64]
+        L.elmrnn_weight_block_len.argtypes = [vp, i32]
+        L.elmrnn_weight_block_len.restype = i64
+        L.elmrnn_path.argtypes = [vp]
+        L.elmrnn_launch_count.argtypes = [vp]
+        L.elmrnn_launch_count.restype = i64
+        L.elmrnn_last_error.argtypes = [vp]
+        L.elmrnn_last_error.restype = ctypes.c_char_p
+        L.elmrnn_destroy.argtypes = [vp]
+        L.elmrnn_destroy.restype = None
+        for f in ("elmrnn_init", "elmrnn_init_ex", "elmrnn_set_stream", "elmrnn_build_H", "elmrnn_solve_beta",
+                  "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_predict", "elmrnn_get_weights",
+                  "elmrnn_path"):
+            getattr(L, f).restype = i32
+        _lib = L
+    return _lib
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _dev_check(t: torch.Tensor, name: str, dtype: torch.dtype):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}")
+
+
+def _rows(t: torch.Tensor, name: str):
+    """(leading dimension, rows) of a 2-D view with unit inner stride."""
+    t2 = t.reshape(t.shape[0], -1) if t.dim() != 2 else t
+    if t2.dim() != 2 or t2.stride(1) != 1:
+        raise ValueError(f"{name} must have unit inner stride")
+    return t2.stride(0) if t2.shape[0] > 1 else t2.shape[1], t2.shape[0]
+
+
+class ELMRNN:
+    """Handle of one ELM-RNN (fixed random weights) on the current CUDA device.
+
+    ELMRNN(arch, d, M, Q, seed, F=-1, R=-1, act=0, rec_scale=0, weight_grid=0,
+    fc_lags=-1, force_path=0) -- elmrnn_init_ex."""
+
+    def __init__(self, arch, d: int, M: int, Q: int, seed: int = 1, **opts):
+        L = lib()
+        o = Opts()
+        L.elmrnn_opts_default(ctypes.byref(o))
+        for k, v in opts.items():
+            if not hasattr(o, k):
+                raise TypeError(f"unknown option {k}")
+            setattr(o, k, int(v))
+        self.arch = arch if isinstance(arch, str) else [k for k, v in ARCHS.items() if v == arch][0]
+        self.d, self.M, self.Q = d, M, Q
+        self.opts = {f: getattr(o, f) for f, _ in Opts._fields_}
+        h = ctypes.c_void_p()
+        st = L.elmrnn_init_ex(ctypes.byref(h), ARCHS[self.arch], d, M, Q, ctypes.c_uint64(seed & (2**64 - 1)),
+                              ctypes.byref(o))
+        if st != 0:
+            raise ElmrnnError(st, L.elmrnn_last_error(None).decode())
+        self._h = h
+
+    # -- plumbing
+    def _check(self, st: int) -> int:
+        if st < 0:
+            raise ElmrnnError(st, lib().elmrnn_last_error(self._h).decode())
+        return st
+
+    def _stream(self):
+        lib().elmrnn_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().elmrnn_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    @property
+    def path(self) -> int:
+        return lib().elmrnn_path(self._h)
+
+    @property
+    def launch_count(self) -> int:
+        return lib().elmrnn_launch_count(self._h)
+
+    @property
+    def packed_r_len(self) -> int:
+        return lib().elmrnn_packed_r_len(self._h)
+
+    # -- API
+    def build_H(self, X: torch.Tensor, Yfb: torch.Tensor | None = None, H: torch.Tensor | None = None):
+        """elmrnn_build_H: X [N][Q][d] (or [N][ldx]) fp32 CUDA -> H [N][M] fp32."""
+        _dev_check(X, "X", torch.float32)
+        N = X.shape[0]
+        ldx, _ = _rows(X, "X") if N else (self.Q * self.d, 0)
+        ldy = 0
+        if Yfb is not None:
+            _dev_check(Yfb, "Yfb", torch.float32)
+            ldy, _ = _rows(Yfb, "Yfb")
+        if H is None:
+            H = torch.empty((N, self.M), dtype=torch.float32, device=X.device)
+        _dev_check(H, "H", torch.float32)
+        ldh, _ = _rows(H, "H") if N else (self.M, 0)
+        self._stream()
+        self._check(lib().elmrnn_build_H(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, N, _ptr(H), ldh))
+        return H
+
+    def solve_beta(self, H: torch.Tensor, Y: torch.Tensor, beta: torch.Tensor | None = None, info: bool = True):
+        """elmrnn_solve_beta -> (beta fp64 [M], SolveInfo or None)."""
+        _dev_check(H, "H", torch.float32)
+        _dev_check(Y, "Y", torch.float32)
+        N = H.shape[0]
+        ldh, _ = _rows(H, "H")
+        if beta is None:
+            beta = torch.empty(self.M, dtype=torch.float64, device=H.device)
+        self._stream()
+        inf = _Info()
+        st = self._check(lib().elmrnn_solve_beta(self._h, _ptr(H), ldh, _ptr(Y), N, _ptr(beta),
+                                                 ctypes.byref(inf) if info else None))
+        return beta, (self._info(inf, st) if info else None)
+
+    def solve_local(self, H: torch.Tensor, Y: torch.Tensor, Rpk: torch.Tensor | None = None):
+        """elmrnn_solve_local -> packed R fp64 [(M+1)(M+2)/2]."""
+        _dev_check(H, "H", torch.float32)
+        _dev_check(Y, "Y", torch.float32)
+        N = H.shape[0]
+        ldh = _rows(H, "H")[0] if N else self.M
+        if Rpk is None:
+            Rpk = torch.empty(self.packed_r_len, dtype=torch.float64, device=H.device)
+        self._stream()
+        self._check(lib().elmrnn_solve_local(self._h, _ptr(H), ldh, _ptr(Y), N, _ptr(Rpk)))
+        return Rpk
+
+    def solve_merge(self, Rpk_all: torch.Tensor, P: int, N_total: int, beta: torch.Tensor | None = None,
+                    info: bool = True):
+        """elmrnn_solve_merge on P stacked packed R factors."""
+        _dev_check(Rpk_all, "Rpk_all", torch.float64)
+        if beta is None:
+            beta = torch.empty(self.M, dtype=torch.float64, device=Rpk_all.device)
+        self._stream()
+        inf = _Info()
+        st = self._check(lib().elmrnn_solve_merge(self._h, _ptr(Rpk_all), P, N_total, _ptr(beta),
+                                                  ctypes.byref(inf) if info else None))
+        return beta, (self._info(inf, st) if info else None)
+
+    def predict(self, X: torch.Tensor, beta: torch.Tensor, Yfb: torch.Tensor | None = None):
+        """elmrnn_predict -> Yhat fp32 [N]."""
+        _dev_check(X, "X", torch.float32)
+        _dev_check(beta, "beta", torch.float64)
+        N = X.shape[0]
+        ldx = _rows(X, "X")[0] if N else self.Q * self.d
+        ldy = _rows(Yfb, "Yfb")[0] if Yfb is not None else 0
+        out = torch.empty(N, dtype=torch.float32, device=X.device)
+        self._stream()
+        self._check(lib().elmrnn_predict(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, N, _ptr(beta), _ptr(out)))
+        return out
+
+    def get_weights(self, block_id: int):
+        """elmrnn_get_weights: logical weight block as a flat float32 CPU tensor."""
+        n = lib().elmrnn_weight_block_len(self._h, block_id)
+        if n < 0:
+            raise ValueError("block id out of range")
+        out = torch.empty(n, dtype=torch.float32)
+        self._stream()
+        self._check(lib().elmrnn_get_weights(self._h, block_id, out.data_ptr(), n))
+        return out
+
+    def train(self, X, Y, Yfb=None):
+        """Alg. 1 lines 2-3: H(Q) then beta."""
+        H = self.build_H(X, Yfb)
+        beta, info = self.solve_beta(H, Y)
+        return H, beta, info
+
+    @staticmethod
+    def _info(i: _Info, st: int) -> SolveInfo:
+        return SolveInfo(i.rho, i.rmse, i.rdiag_min_abs, i.rdiag_max_abs, i.ridge_lambda, i.rank_flag, i.n_total, st)
