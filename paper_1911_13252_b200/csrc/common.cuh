@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "elmrnn.h"
 
@@ -42,6 +43,8 @@ struct elmrnn {
     // tensor-core operands (device; only when path == 2)
     void* tc_ops;
     size_t tc_ops_bytes;
+    float tc_inv_scale;       // 2^-sigma of the scaled fp16 U images
+    std::vector<float> tc_wb; // host copy of W | b (kernel parameter block)
     // solve workspace (device)
     double* Rws;          // slabs of (M+1)^2 doubles
     int64_t Rws_slabs;

@@ -52,21 +52,33 @@ __device__ __forceinline__ void load_rows(const float* src, float (&v)[RT]) {
 
 // acc[rr][g] += sum_k A[k][row0+rr] * B[k][g*ldgate + j]  over k in [0, K)
 // A row k is at a_of(k) (a [T]-vector); B row k at b_of(k).
-template <int RT, int GG, class AOf, class BOf>
+// A_STAGE: the A rows live in global memory (FC history ring in L2) and are
+// staged through shared memory slice by slice together with B.
+template <int RT, int GG, bool A_STAGE = false, class AOf, class BOf>
 __device__ __forceinline__ void tile_contract(float (&acc)[RT][GG], int K, int c0, int M, AOf a_of, BOf b_of,
-                                              float* us, int rbase) {
+                                              float* us, int rbase, float* as = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31;
+    constexpr int T = 8 * RT;
     for (int k0 = 0; k0 < K; k0 += kKC) {
         for (int e = tid; e < kKC * GG * kNJ; e += blockDim.x) {
             int kk = e / (GG * kNJ), rem = e - kk * (GG * kNJ), g = rem / kNJ, jj = rem - g * kNJ;
             int k = k0 + kk, j = c0 + jj;
             us[e] = (k < K && j < M) ? __ldg(b_of(k) + g * M + j) : 0.0f;
         }
+        if constexpr (A_STAGE) {
+            for (int e = tid; e < kKC * T; e += blockDim.x) {
+                int kk = e / T, rr = e - kk * T;
+                as[e] = (k0 + kk < K) ? a_of(k0 + kk)[rr] : 0.0f;
+            }
+        }
         __syncthreads();
         int kmax = min(kKC, K - k0);
         for (int kk = 0; kk < kmax; ++kk) {
             float hv[RT];
-            load_rows<RT>(a_of(k0 + kk) + rbase, hv);
+            if constexpr (A_STAGE)
+                load_rows<RT>(as + kk * T + rbase, hv);
+            else
+                load_rows<RT>(a_of(k0 + kk) + rbase, hv);
             float u[GG];
 #pragma unroll
             for (int g = 0; g < GG; ++g) u[g] = us[(kk * GG + g) * kNJ + lane];
@@ -91,7 +103,8 @@ __global__ void __launch_bounds__(256) k_dense_fma(DenseParams p) {
 
     float* xs = sm;                                           // [T][S]
     float* us = xs + ((T * S + 3) & ~3);                      // [KC][GG][NJ]
-    float* cur = us + kKC * 4 * kNJ;
+    float* as = us + kKC * 4 * kNJ;                           // [KC][T] staged A (FC, global ring)
+    float* cur = as + kKC * T;
     float* ring;
     if (p.ring_global) {
         ring = p.ring_global + (size_t)blockIdx.x * nslots * MT;
@@ -137,11 +150,13 @@ __global__ void __launch_bounds__(256) k_dense_fma(DenseParams p) {
                 }
                 if (ARCH == kArchFC) {
                     const int nl = min(t - 1, p.L);
-                    tile_contract<RT, GG>(
-                        acc, nl * M, c0, M,
-                        [&](int k) { int lag = k / M + 1, m = k - (lag - 1) * M;
-                                     return ring + (size_t)((t - lag) % nslots) * MT + (size_t)m * T; },
-                        [&](int k) { return p.U + (size_t)k * M; }, us, rbase);
+                    auto aof = [&](int k) { int lag = k / M + 1, m = k - (lag - 1) * M;
+                                            return ring + (size_t)((t - lag) % nslots) * MT + (size_t)m * T; };
+                    auto bof = [&](int k) { return p.U + (size_t)k * M; };
+                    if (p.ring_global)
+                        tile_contract<RT, GG, true>(acc, nl * M, c0, M, aof, bof, us, rbase, as);
+                    else
+                        tile_contract<RT, GG>(acc, nl * M, c0, M, aof, bof, us, rbase);
                 } else {
                     tile_contract<RT, GG>(
                         acc, M, c0, M, [&](int k) { return hprev + (size_t)k * T; },
@@ -209,7 +224,7 @@ __global__ void __launch_bounds__(256) k_dense_fma(DenseParams p) {
 // Shared-memory floats the kernel needs for a given tile height.
 static size_t dense_smem_floats(int arch, int T, int S, int M, int L, bool ring_in_smem) {
     size_t MT = (size_t)M * T;
-    size_t f = ((size_t)T * S + 3) / 4 * 4 + (size_t)kKC * 4 * kNJ;
+    size_t f = ((size_t)T * S + 3) / 4 * 4 + (size_t)kKC * 4 * kNJ + (size_t)kKC * T;
     int nslots = arch == kArchFC ? L + 1 : 2;
     if (ring_in_smem) f += nslots * MT;
     if (arch == kArchLSTM) f += MT;
