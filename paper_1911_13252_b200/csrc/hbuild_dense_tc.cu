@@ -16,10 +16,10 @@
 //   smem: A = h(t-1) hi/lo, K-major SW128 (128 KB at M = 256)
 //         B ring: 3 stages x (hi + lo) 128 x 64 fp16 U slices (32 KB each)
 //   TMEM: 2 x 128 accumulator columns (double buffered) + M columns of h(t)
-//   warps: 0 = bulk-copy producer (U stages from L2), 1 = MMA issuer (one
-//          thread), 2 = TMEM allocator, 3 idle, 4..11 = epilogue (2 per TMEM
-//          lane quadrant; a thread owns one row and 16 neurons per chunk and
-//          keeps c(t) for its 128 neurons in registers).
+//   warps: 0 = bulk-copy producer (one thread) + TMEM allocator, 1 = MMA
+//          issuer (one thread), 2..17 = epilogue (4 per TMEM lane quadrant;
+//          a thread owns one row and 8 neurons per chunk and keeps c(t) for
+//          its M/4 neurons in registers).
 //   per step: NCH = M/32 chunks of 32 neurons x 4 gates = 128 accumulator
 //   columns; chunk n+1's MMAs overlap chunk n's epilogue.  After the last
 //   chunk the epilogue converts h(t) (TMEM) to fp16 hi/lo into A and
@@ -30,6 +30,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -42,8 +45,9 @@ constexpr int kTcRows = 128;
 constexpr int kTcStages = 3;
 constexpr int kTcSliceBytes = 128 * 64 * 2;      // one 128 x 64 fp16 SW128 tile
 constexpr int kTcStageBytes = 2 * kTcSliceBytes;  // hi + lo
-constexpr int kTcEpiWarps = 8;
-constexpr int kTcThreads = (4 + kTcEpiWarps) * 32;
+constexpr int kTcEpiWarps = 16;                 // 4 per TMEM lane quadrant, 8 neurons per chunk each
+constexpr int kTcCtlWarps = 2;                  // 0: bulk-copy producer + TMEM alloc, 1: MMA issuer
+constexpr int kTcThreads = (kTcCtlWarps + kTcEpiWarps) * 32;
 constexpr int kTcWbMax = 7168;                    // floats of W|b in the parameter block
 
 struct TcParams {
@@ -54,18 +58,22 @@ struct TcParams {
     const uint8_t* Uimg;   // [NCH][KS][hi|lo][16 KB] pre-swizzled images
     int S, Q;
     int64_t ntiles;
-    float inv_scale;       // 2^-sigma
-    float wb[kTcWbMax];    // W [S][4M] then b [4M]
+    float k_sig, k_tanh;   // -log2(e) 2^-sigma, 2 log2(e) 2^-sigma
+    unsigned long long* trace;   // optional event trace of CTA 0 (ELMRNN_TRACE), else null
+    int trace_cap;
+    float wb[kTcWbMax];    // per neuron j, gate g: [b, W_0..W_{S-1}] x 2^sigma
 };
 
 template <int M>
 struct TcCfg {
     static constexpr int NCH = M / 32;
     static constexpr int KS = M / 64;
-    static constexpr int A_BYTES = kTcRows * M * 2;   // one of hi / lo
-    static constexpr int SMEM = 1024 + 2 * A_BYTES + kTcStages * kTcStageBytes + 256;
+    static constexpr int ITEMS = NCH * 8;                  // staged words per epilogue thread
+    static constexpr int STG_BYTES = kTcEpiWarps * ITEMS * 32 * 4;
+    static constexpr int SMEM = 1024 + kTcStages * kTcStageBytes + STG_BYTES + 256;
     static constexpr int TMEM_COLS = 512;
-    static constexpr int H_COL = 256;                 // first h(t) staging column
+    static constexpr int A_HI = 256;                       // TMEM columns of A = h(t-1): hi parts
+    static constexpr int A_LO = 256 + M / 2;               //   lo parts (2 fp16 per 32-bit column)
 };
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
@@ -78,55 +86,46 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-            taddr),
-        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-        "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-        "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
-        "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
-        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
-        "r"(__float_as_uint(v[15]))
-        : "memory");
-}
+__device__ __forceinline__ float clamp30(float x) { return fminf(fmaxf(x, -30.0f), 30.0f); }
 
-// Write 16 consecutive h values (K indices k0..k0+15, k0 % 16 == 0) of row r
-// into the A operand as fp16 hi and lo parts (K-major SW128, 64-wide slices).
-__device__ __forceinline__ void store_h16(uint8_t* A_hi, uint8_t* A_lo, int r, int k0, const float (&h)[16]) {
-    uint32_t hi[8], lo[8];
+// Split 8 fp32 h values into fp16 hi = fp16(h) and lo = fp16(h - hi), packed
+// two per 32-bit word (even K index in the low half) as the TMEM A operand wants.
+__device__ __forceinline__ void split_h8(const float (&h)[8], uint32_t (&hi)[4], uint32_t (&lo)[4]) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        __half a0 = __float2half_rn(h[2 * i]), a1 = __float2half_rn(h[2 * i + 1]);
-        __half b0 = __float2half_rn(h[2 * i] - __half2float(a0));
-        __half b1 = __float2half_rn(h[2 * i + 1] - __half2float(a1));
-        hi[i] = (uint32_t)__half_as_ushort(a0) | ((uint32_t)__half_as_ushort(a1) << 16);
-        lo[i] = (uint32_t)__half_as_ushort(b0) | ((uint32_t)__half_as_ushort(b1) << 16);
+    for (int i = 0; i < 4; ++i) {
+        const __half2 a = __floats2half2_rn(h[2 * i], h[2 * i + 1]);   // packed F2FP
+        const float2 af = __half22float2(a);
+        const __half2 b = __floats2half2_rn(h[2 * i] - af.x, h[2 * i + 1] - af.y);
+        hi[i] = *reinterpret_cast<const uint32_t*>(&a);
+        lo[i] = *reinterpret_cast<const uint32_t*>(&b);
     }
-    const int s = k0 >> 6, kin = k0 & 63;
-    const uint32_t o0 = s * kTcSliceBytes + ptx::sw128_offset(r, kin);
-    const uint32_t o1 = s * kTcSliceBytes + ptx::sw128_offset(r, kin + 8);
-    *reinterpret_cast<uint4*>(A_hi + o0) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    *reinterpret_cast<uint4*>(A_hi + o1) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
-    *reinterpret_cast<uint4*>(A_lo + o0) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-    *reinterpret_cast<uint4*>(A_lo + o1) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
 }
 
-template <int M>
+// Event trace (tracing aux subsystem): CTA 0 records (kind, step, chunk, clock)
+// for its first trace_cap events when the launcher passes a buffer.
+__device__ __forceinline__ void trace_ev(const TcParams& p, uint32_t* cnt, int kind, int step, int chunk) {
+    if (p.trace == nullptr || blockIdx.x != 0) return;
+    const uint32_t i = atomicAdd(cnt, 1u);
+    if ((int)i < p.trace_cap)
+        p.trace[i] = ((unsigned long long)kind << 56) | ((unsigned long long)(step & 0xFFFF) << 40) |
+                     ((unsigned long long)(chunk & 0xFF) << 32) | (unsigned long long)(clock64() & 0xFFFFFFFFull);
+}
+
+template <int M, int SS>
 __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant__ TcParams p) {
     using C = TcCfg<M>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* A_hi = smem;
-    uint8_t* A_lo = A_hi + C::A_BYTES;
-    uint8_t* stages = A_lo + C::A_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kTcStages * kTcStageBytes);
+    uint8_t* stages = smem;                                                     // U ring
+    uint32_t* stg = reinterpret_cast<uint32_t*>(stages + kTcStages * kTcStageBytes);  // h(t) hi|lo staging
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + C::STG_BYTES);
     uint64_t* full = bars;                       // [kTcStages]
     uint64_t* empty = bars + kTcStages;          // [kTcStages]
     uint64_t* acc_full = bars + 2 * kTcStages;   // [2]
     uint64_t* acc_empty = acc_full + 2;          // [2]
     uint64_t* a_ready = acc_empty + 2;           // [1]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_ready + 1);
+    uint32_t* trace_cnt = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -139,9 +138,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
             ptx::mbar_init(acc_empty + i, kTcEpiWarps);
         }
         ptx::mbar_init(a_ready, kTcEpiWarps);
+        *trace_cnt = 0;
         ptx::fence_mbar_init();
     }
-    if (warp == 2) {
+    if (warp == 0) {
         ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
         ptx::tmem_relinquish();
     }
@@ -169,15 +169,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
         // ---------------- MMA issuer
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_f16(128, 128);
-            const uint32_t a_hi = ptx::smem_u32(A_hi), a_lo = ptx::smem_u32(A_lo);
+            const uint32_t a_hi = tmem + C::A_HI, a_lo = tmem + C::A_LO;   // A operand in TMEM
             const uint32_t b0 = ptx::smem_u32(stages);
             uint32_t st = 0, ph = 0, ach = 0, aph = 0;
             for (int64_t s = 0; s < steps_total; ++s) {
                 ptx::mbar_wait(a_ready, (uint32_t)(s & 1));   // h(t-1) hi/lo is in A
+                trace_ev(p, trace_cnt, 1, (int)s, 0);
                 ptx::tc_fence_after();
                 for (int n = 0; n < C::NCH; ++n) {
                     ptx::mbar_wait(acc_empty + ach, aph ^ 1);
                     ptx::tc_fence_after();
+                    trace_ev(p, trace_cnt, 2, (int)s, n);
                     const uint32_t d = tmem + ach * 128;
                     for (int ks = 0; ks < C::KS; ++ks) {
                         ptx::mbar_wait(full + st, ph);
@@ -185,40 +187,43 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                         const uint32_t bh = b0 + st * kTcStageBytes, bl = bh + kTcSliceBytes;
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
-                            const uint64_t dah = ptx::desc_sw128_kmajor(a_hi + ks * kTcSliceBytes + kk * 32);
-                            const uint64_t dal = ptx::desc_sw128_kmajor(a_lo + ks * kTcSliceBytes + kk * 32);
+                            const uint32_t tah = a_hi + ks * 32 + kk * 8, tal = a_lo + ks * 32 + kk * 8;
                             const uint64_t dbh = ptx::desc_sw128_kmajor(bh + kk * 32);
                             const uint64_t dbl = ptx::desc_sw128_kmajor(bl + kk * 32);
-                            ptx::mma_f16_ss(d, dah, dbh, idesc, (ks | kk) != 0);
-                            ptx::mma_f16_ss(d, dah, dbl, idesc, 1);
-                            ptx::mma_f16_ss(d, dal, dbh, idesc, 1);
+                            ptx::mma_f16_ts(d, tah, dbh, idesc, (ks | kk) != 0);
+                            ptx::mma_f16_ts(d, tah, dbl, idesc, 1);
+                            ptx::mma_f16_ts(d, tal, dbh, idesc, 1);
                         }
                         ptx::mma_commit(empty + st);                      // frees the U stage
                         if (++st == kTcStages) { st = 0; ph ^= 1; }
                     }
                     ptx::mma_commit(acc_full + ach);                      // chunk accumulator ready
+                    trace_ev(p, trace_cnt, 3, (int)s, n);
                     if (++ach == 2) { ach = 0; aph ^= 1; }
                 }
             }
         }
-    } else if (warp >= 4) {
+    } else {
         // ---------------- epilogue: gates, c/h update, A write-back, H(Q) store
-        const int e = warp - 4, q = e & 3, u = e >> 2;
+        // Pre-activations stay in the 2^sigma-scaled domain: W, b were scaled on
+        // the host, and 2^-sigma is folded into the exp2 argument constants.
+        // epilogue warp w: TMEM lane quadrant w % 4 (hardware rule), neuron group u
+        const int e = warp - kTcCtlWarps, q = warp & 3, u = e >> 2;
         const int r = 32 * q + lane;                 // tile row = TMEM lane
         const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
-        const int S = p.S, GM = 4 * M;
-        const float* Wp = p.wb;
-        const float* bp = p.wb + S * GM;
-        float c[C::NCH * 16];
+        const float kS = p.k_sig, kT = p.k_tanh;     // -log2e 2^-sigma, 2 log2e 2^-sigma
+        float c[C::NCH * 8];                         // c(t) of neurons n*32 + 8u + 0..7
         uint32_t ach = 0, aph = 0;
-        // h(0) = 0 for the first tile
-        {
-            float z[16];
+        uint32_t* my_stg = stg + (size_t)e * C::ITEMS * 32 + lane;   // [item][lane]
+        {   // h(0) = 0 for the first tile
+            const uint32_t z[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-            for (int i = 0; i < 16; ++i) z[i] = 0.0f;
-#pragma unroll
-            for (int n = 0; n < C::NCH; ++n) store_h16(A_hi, A_lo, r, n * 32 + 16 * u, z);
-            ptx::fence_proxy_async_smem();
+            for (int n = 0; n < C::NCH; ++n) {
+                ptx::tmem_st4(lane_base + C::A_HI + n * 16 + 4 * u, z);
+                ptx::tmem_st4(lane_base + C::A_LO + n * 16 + 4 * u, z);
+            }
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(a_ready);
         }
@@ -227,84 +232,117 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
             const bool valid = row < p.N;
             const float* xrow = p.X + (valid ? row : 0) * p.ldx;
 #pragma unroll
-            for (int i = 0; i < C::NCH * 16; ++i) c[i] = 0.0f;
+            for (int i = 0; i < C::NCH * 8; ++i) c[i] = 0.0f;
             for (int t = 1; t <= p.Q; ++t) {
-                float xs[8];
+                float xs[SS];
 #pragma unroll
-                for (int s = 0; s < 8; ++s) xs[s] = (s < S && valid) ? __ldg(xrow + (int64_t)(t - 1) * S + s) : 0.0f;
+                for (int s = 0; s < SS; ++s)
+                    xs[s] = (valid && s < p.S) ? __ldg(xrow + (int64_t)(t - 1) * p.S + s) : 0.0f;
 #pragma unroll
                 for (int n = 0; n < C::NCH; ++n) {
                     ptx::mbar_wait(acc_full + ach, aph);
                     ptx::tc_fence_after();
-                    float hv[16];
+                    if (e == 0 && lane == 0) trace_ev(p, trace_cnt, 4, t, n);
+                    float a[2][16];   // 2 groups x 4 neurons x (o, c, lambda, in), scaled domain
+                    tmem_ld16(lane_base + ach * 128 + (8 * u) * 4, a[0]);
+                    tmem_ld16(lane_base + ach * 128 + (8 * u + 4) * 4, a[1]);
+                    ptx::tmem_wait_ld();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(acc_empty + ach);   // accumulator drained
+                    float hv[8];
+                    // MUFU budget: 5 ex2 + 1.25 rcp per element.  The four gate
+                    // denominators of a neuron share one reciprocal (1/a = bcd/(abcd)),
+                    // as do the tanh(c) denominators of 4 neurons; exp2 arguments are
+                    // clamped to +-30 so the products stay finite (sigma(20.8) = 1 - 9e-10).
 #pragma unroll
-                    for (int g4 = 0; g4 < 4; ++g4) {
-                        float a[16];   // 4 neurons x (o, c, lambda, in)
-                        tmem_ld16(lane_base + ach * 128 + (16 * u + 4 * g4) * 4, a);
-                        ptx::tmem_wait_ld();
-                        if (g4 == 3) {   // accumulator buffer fully read: release it
-                            ptx::tc_fence_before();
-                            __syncwarp();
-                            if (lane == 0) ptx::mbar_arrive(acc_empty + ach);
-                        }
+                    for (int g4 = 0; g4 < 2; ++g4) {
+                        float so[4], dc[4];
 #pragma unroll
                         for (int nb = 0; nb < 4; ++nb) {
-                            const int jl = 16 * u + 4 * g4 + nb;   // neuron within chunk
-                            const int j = n * 32 + jl;
+                            const int j = n * 32 + 8 * u + 4 * g4 + nb;
+                            const float* w = p.wb + j * (4 * (SS + 1));   // [gate][b, W_0..W_{S-1}]
                             float pre[4];
 #pragma unroll
                             for (int g = 0; g < 4; ++g) {
-                                float v = fmaf(a[nb * 4 + g], p.inv_scale, bp[g * M + j]);
+                                float v = a[g4][nb * 4 + g] + w[g * (SS + 1)];
 #pragma unroll
-                                for (int s = 0; s < 8; ++s)
-                                    if (s < S) v = fmaf(xs[s], Wp[s * GM + g * M + j], v);
+                                for (int s = 0; s < SS; ++s) v = fmaf(xs[s], w[g * (SS + 1) + 1 + s], v);
                                 pre[g] = v;
                             }
-                            const int ci = n * 16 + 4 * g4 + nb;
-                            const float cn = sigmoidf_(pre[2]) * c[ci] + sigmoidf_(pre[3]) * tanhf_(pre[1]);
+                            const float d0 = 1.0f + ex2_approx(clamp30(kS * pre[0]));   // o
+                            const float d1 = 1.0f + ex2_approx(clamp30(kT * pre[1]));   // c~ (tanh)
+                            const float d2 = 1.0f + ex2_approx(clamp30(kS * pre[2]));   // lambda
+                            const float d3 = 1.0f + ex2_approx(clamp30(kS * pre[3]));   // in
+                            const float p01 = d0 * d1, p23 = d2 * d3;
+                            const float rr = rcp_approx(p01 * p23);
+                            const float r01 = rr * p23, r23 = rr * p01;
+                            so[nb] = d1 * r01;
+                            const float tc = fmaf(-2.0f, d0 * r01, 1.0f);
+                            const float sl = d3 * r23, si = d2 * r23;
+                            const int ci = n * 8 + 4 * g4 + nb;
+                            const float cn = fmaf(sl, c[ci], si * tc);
                             c[ci] = cn;
-                            hv[4 * g4 + nb] = sigmoidf_(pre[0]) * tanhf_(cn);
+                            dc[nb] = 1.0f + ex2_approx(clamp30(2.8853900817779268f * cn));
+                        }
+                        const float p01 = dc[0] * dc[1], p23 = dc[2] * dc[3];
+                        const float rr = rcp_approx(p01 * p23);
+                        const float r01 = rr * p23, r23 = rr * p01;
+                        hv[4 * g4 + 0] = so[0] * fmaf(-2.0f, dc[1] * r01, 1.0f);
+                        hv[4 * g4 + 1] = so[1] * fmaf(-2.0f, dc[0] * r01, 1.0f);
+                        hv[4 * g4 + 2] = so[2] * fmaf(-2.0f, dc[3] * r23, 1.0f);
+                        hv[4 * g4 + 3] = so[3] * fmaf(-2.0f, dc[2] * r23, 1.0f);
+                    }
+                    // stage h(t) of these 8 neurons as fp16 hi|lo pairs (the A operand
+                    // format); at the last step also store the fp32 H(Q) row segment
+                    {
+                        uint32_t hi[4], lo[4];
+                        split_h8(hv, hi, lo);
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) {
+                            my_stg[(n * 8 + w) * 32] = hi[w];
+                            my_stg[(n * 8 + 4 + w) * 32] = lo[w];
                         }
                     }
-                    tmem_st16(lane_base + C::H_COL + n * 32 + 16 * u, hv);
+                    if (t == p.Q && valid) {
+                        float* d1 = p.H + row * p.ldh + n * 32 + 8 * u;
+                        if ((p.ldh & 3) == 0) {
+                            float4* dst = reinterpret_cast<float4*>(d1);
+                            dst[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+                            dst[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) d1[i] = hv[i];
+                        }
+                    }
+                    if (e == 0 && lane == 0) trace_ev(p, trace_cnt, 5, t, n);
                     if (++ach == 2) { ach = 0; aph ^= 1; }
                 }
-                // all MMAs of step t are complete (the last chunk's commit covers them):
-                // publish h(t) as the next A operand, or store H(Q) and reset A for the next tile
-                ptx::tmem_wait_st();
+                // all MMAs of step t are complete (the last chunk's commit covers
+                // them): move h(t) into the TMEM A operand, or zero it for the next tile
+                const bool last = (t == p.Q);
 #pragma unroll
                 for (int n = 0; n < C::NCH; ++n) {
-                    float hv[16];
-                    tmem_ld16(lane_base + C::H_COL + n * 32 + 16 * u, hv);
-                    ptx::tmem_wait_ld();
-                    if (t == p.Q) {
-                        if (valid) {
-                            float4* dst = reinterpret_cast<float4*>(p.H + row * p.ldh + n * 32 + 16 * u);
-                            if ((p.ldh & 3) == 0) {
+                    uint32_t hi[4], lo[4];
 #pragma unroll
-                                for (int i = 0; i < 4; ++i)
-                                    dst[i] = make_float4(hv[4 * i], hv[4 * i + 1], hv[4 * i + 2], hv[4 * i + 3]);
-                            } else {
-                                float* d1 = p.H + row * p.ldh + n * 32 + 16 * u;
-#pragma unroll
-                                for (int i = 0; i < 16; ++i) d1[i] = hv[i];
-                            }
-                        }
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) hv[i] = 0.0f;   // h(0) of the next tile
+                    for (int w = 0; w < 4; ++w) {
+                        hi[w] = last ? 0u : my_stg[(n * 8 + w) * 32];
+                        lo[w] = last ? 0u : my_stg[(n * 8 + 4 + w) * 32];
                     }
-                    store_h16(A_hi, A_lo, r, n * 32 + 16 * u, hv);
+                    ptx::tmem_st4(lane_base + C::A_HI + n * 16 + 4 * u, hi);
+                    ptx::tmem_st4(lane_base + C::A_LO + n * 16 + 4 * u, lo);
                 }
-                ptx::fence_proxy_async_smem();
+                ptx::tmem_wait_st();
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(a_ready);
+                if (e == 0 && lane == 0) trace_ev(p, trace_cnt, 6, t, 0);
             }
         }
     }
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 2) {
+    if (warp == 0) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, C::TMEM_COLS);
     }
@@ -331,7 +369,7 @@ __global__ void k_pack_u(const float* __restrict__ U, int M, float scale, uint8_
     }
 }
 
-template <int M>
+template <int M, int SS>
 cudaError_t launch_lstm_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh) {
     using C = TcCfg<M>;
     static TcParams p;   // host staging of the (large) parameter block
@@ -339,23 +377,52 @@ cudaError_t launch_lstm_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, fl
     p.Uimg = static_cast<const uint8_t*>(h->tc_ops);
     p.S = h->S; p.Q = h->Q;
     p.ntiles = (N + kTcRows - 1) / kTcRows;
-    p.inv_scale = h->tc_inv_scale;
+    p.k_sig = -1.4426950408889634f * h->tc_inv_scale;
+    p.k_tanh = 2.8853900817779268f * h->tc_inv_scale;
     std::copy(h->tc_wb.begin(), h->tc_wb.end(), p.wb);   // W | b captured at init
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_lstm_tc<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(k_lstm_tc<M, SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM))) return e;
     int grid = (int)std::min<int64_t>(p.ntiles, h->sm_count);
-    k_lstm_tc<M><<<grid, kTcThreads, C::SMEM, h->stream>>>(p);
+    const char* tpath = std::getenv("ELMRNN_TRACE");
+    unsigned long long* tbuf = nullptr;
+    p.trace = nullptr;
+    p.trace_cap = 0;
+    if (tpath && *tpath) {
+        p.trace_cap = 1 << 16;
+        if ((e = cudaMalloc(&tbuf, sizeof(unsigned long long) * p.trace_cap))) return e;
+        cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * p.trace_cap, h->stream);
+        p.trace = tbuf;
+    }
+    k_lstm_tc<M, SS><<<grid, kTcThreads, C::SMEM, h->stream>>>(p);
     h->launches++;
-    return cudaGetLastError();
+    if ((e = cudaGetLastError())) return e;
+    if (tbuf) {   // debug path: synchronous dump of CTA 0's event trace
+        std::vector<unsigned long long> hbuf(p.trace_cap);
+        cudaMemcpyAsync(hbuf.data(), tbuf, sizeof(unsigned long long) * p.trace_cap, cudaMemcpyDeviceToHost,
+                        h->stream);
+        cudaStreamSynchronize(h->stream);
+        cudaFree(tbuf);
+        if (FILE* f = std::fopen(tpath, "w")) {
+            std::fprintf(f, "kind,step,chunk,clock\n");
+            for (auto v : hbuf)
+                if (v) std::fprintf(f, "%llu,%llu,%llu,%llu\n", v >> 56, (v >> 40) & 0xFFFF, (v >> 32) & 0xFF,
+                                    v & 0xFFFFFFFFull);
+            std::fclose(f);
+        }
+    }
+    return cudaSuccess;
 }
 
 }  // namespace
 
+// the kernel is specialised on S in {1, 2, 4}; S = 3 rounds up with zero W
+static int tc_padded_s(int S) { return S <= 1 ? 1 : (S <= 2 ? 2 : 4); }
+
 bool tc_supported(const elmrnn* h) {
     if (h->arch != kArchLSTM) return false;
     if (h->M != 128 && h->M != 256) return false;
-    if (h->S > 8) return false;
-    return (h->S + 1) * 4 * h->M <= kTcWbMax;
+    if (h->S > 4) return false;
+    return (tc_padded_s(h->S) + 1) * 4 * h->M <= kTcWbMax;
 }
 
 cudaError_t tc_prepare(elmrnn* h) {
@@ -368,15 +435,20 @@ cudaError_t tc_prepare(elmrnn* h) {
     int sigma = h->rec_scale == 1 ? 0 : (int)std::floor(std::log2(std::sqrt((double)M)));
     float scale = std::ldexp(1.0f, sigma);
     h->tc_inv_scale = std::ldexp(1.0f, -sigma);
-    // W | b for the x(t) W + b epilogue term travel in the kernel parameter block
-    const int GM = 4 * M;
-    h->tc_wb.assign((size_t)(h->S + 1) * GM, 0.0f);
-    if ((e = cudaMemcpyAsync(h->tc_wb.data(), h->W, sizeof(float) * h->S * GM, cudaMemcpyDeviceToHost, h->stream)))
-        return e;
-    if ((e = cudaMemcpyAsync(h->tc_wb.data() + (size_t)h->S * GM, h->b, sizeof(float) * GM, cudaMemcpyDeviceToHost,
-                             h->stream)))
-        return e;
+    // W | b for the x(t) W + b epilogue term travel in the kernel parameter
+    // block, scaled by 2^sigma (exact) and laid out [neuron][gate][b, W_0..W_{S-1}]
+    const int GM = 4 * M, S = h->S, SP = tc_padded_s(S);
+    std::vector<float> W((size_t)S * GM), b(GM);
+    if ((e = cudaMemcpyAsync(W.data(), h->W, sizeof(float) * S * GM, cudaMemcpyDeviceToHost, h->stream))) return e;
+    if ((e = cudaMemcpyAsync(b.data(), h->b, sizeof(float) * GM, cudaMemcpyDeviceToHost, h->stream))) return e;
     if ((e = cudaStreamSynchronize(h->stream))) return e;
+    h->tc_wb.assign((size_t)M * 4 * (SP + 1), 0.0f);
+    for (int j = 0; j < M; ++j)
+        for (int g = 0; g < 4; ++g) {
+            float* d = h->tc_wb.data() + ((size_t)j * 4 + g) * (SP + 1);
+            d[0] = b[g * M + j] * scale;
+            for (int s2 = 0; s2 < S; ++s2) d[1 + s2] = W[(size_t)s2 * GM + g * M + j] * scale;
+        }
     int64_t total = (int64_t)(M / 32) * (M / 64) * 128 * 64;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
     k_pack_u<<<blocks, 256, 0, h->stream>>>(h->rec, M, scale, static_cast<uint8_t*>(h->tc_ops));
@@ -384,9 +456,19 @@ cudaError_t tc_prepare(elmrnn* h) {
     return cudaGetLastError();
 }
 
+template <int M>
+static cudaError_t launch_m(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh) {
+    switch (tc_padded_s(h->S)) {
+    case 1: return launch_lstm_tc<M, 1>(h, X, ldx, N, H, ldh);
+    case 2: return launch_lstm_tc<M, 2>(h, X, ldx, N, H, ldh);
+    case 4: return launch_lstm_tc<M, 4>(h, X, ldx, N, H, ldh);
+    }
+    return cudaErrorNotSupported;
+}
+
 cudaError_t launch_dense_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh) {
-    if (h->M == 256) return launch_lstm_tc<256>(h, X, ldx, N, H, ldh);
-    if (h->M == 128) return launch_lstm_tc<128>(h, X, ldx, N, H, ldh);
+    if (h->M == 256) return launch_m<256>(h, X, ldx, N, H, ldh);
+    if (h->M == 128) return launch_m<128>(h, X, ldx, N, H, ldh);
     return cudaErrorNotSupported;
 }
 

@@ -5,17 +5,18 @@
 //
 //  k_tsqr_leaf   persistent CTAs, each owning a contiguous row block and an
 //                (M+1)x(M+1) R slab (full storage, L2 resident).  Row tiles of
-//                TR rows are folded in: R <- R-factor of [R; tile] by the
+//                P*TR rows are folded in: R <- R-factor of [R; tile] by the
 //                structured Householder sweep (LAPACK tpqrt semantics).  The
-//                tile lives in registers: thread j owns column j of the tile
-//                (TR doubles) and column j of R, so R needs no inter-thread
-//                synchronisation; the reflector v (TR doubles) of column k is
-//                broadcast through shared memory, one barrier per column,
-//                with one-column look-ahead (the owner of k+1 builds its
-//                reflector right after its own update).
+//                tile lives in registers: the P threads of column j (adjacent
+//                lanes) hold TR rows each of tile column j, and they own column
+//                j of R, so R needs no inter-thread synchronisation; partial
+//                dot products of a column pair combine with one shuffle.  The
+//                reflector v of column k is broadcast through shared memory,
+//                one barrier per column, with one-column look-ahead (the owner
+//                of k+1 builds its reflector right after its own update).
 //  k_tsqr_merge  one level of a binary tree: slab c absorbs slab c+stride by
-//                folding it in TR-row tiles, skipping the zero columns left of
-//                each tile's diagonal.
+//                folding it in (P*TR)-row tiles, skipping the zero columns
+//                left of each tile's diagonal.
 //  k_tsqr_solve  one CTA: sign normalisation (R18), rank check + ridge
 //                fallback by folding sqrt(lambda) (I|0) rows (R19), back
 //                substitution, rho = ||R_aug [beta; -1]|| = ||H beta - Y||.
@@ -24,110 +25,148 @@
 // tolerance); H and Y are read as fp32 and widened exactly.
 #include <cfloat>
 #include <cmath>
+#include <type_traits>
 
 #include "common.cuh"
 
 namespace elm {
 
-template <int TR>
-struct TrBounds { static constexpr int threads = TR >= 32 ? 384 : 1024; };
+// TR rows per thread, P threads per column (1 or 2): tile = P*TR rows.
+template <int TR, int P>
+struct Fold {
+    static constexpr int ROWS = TR * P;
+    // register budget (16K registers per SM sub-partition): 2*TR registers of
+    // tile per thread plus ~40; 576 threads -> 96 registers, 1024 -> 64
+    static constexpr int MAX_THREADS = (P == 2 && TR == 24) ? 576 : 1024;
+};
 
-// Build the Householder reflector of column k from x0 = R[k][k] and the tile
-// column a[0..TR) (LAPACK dlarfg convention, sign(0) = +1).
-template <int TR>
-__device__ __forceinline__ void make_reflector(const double (&a)[TR], double x0, double* v, double* tau,
-                                               double* Rkk) {
-    double s2 = 0.0;
+// Reflector of column k from x0 = R[k][k] and the tile column (this thread's
+// TR rows; the partner lane holds the rest), LAPACK dlarfg convention,
+// sign(0) = +1.  Both threads of the column compute it; half 0 publishes
+// tau and R[k][k].
+template <int TR, int P>
+__device__ __forceinline__ void make_reflector(const double (&a)[TR], double x0, double* v, double* tau, double* Rkk,
+                                               int half, unsigned mask) {
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
 #pragma unroll
-    for (int i = 0; i < TR; ++i) s2 = fma(a[i], a[i], s2);
+    for (int i = 0; i < TR; i += 4) {
+        p0 = fma(a[i], a[i], p0);
+        p1 = fma(a[i + 1], a[i + 1], p1);
+        p2 = fma(a[i + 2], a[i + 2], p2);
+        p3 = fma(a[i + 3], a[i + 3], p3);
+    }
+    double s2 = (p0 + p1) + (p2 + p3);
+    if (P == 2) s2 += __shfl_xor_sync(mask, s2, 1);
     if (s2 == 0.0) {
-        *tau = 0.0;
+        if (half == 0) *tau = 0.0;
         return;
     }
-    double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * sqrt(fma(x0, x0, s2));
-    *tau = (beta - x0) / beta;
-    double sc = 1.0 / (x0 - beta);
+    const double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * sqrt(fma(x0, x0, s2));
+    const double sc = 1.0 / (x0 - beta);
 #pragma unroll
-    for (int i = 0; i < TR; ++i) v[i] = a[i] * sc;
-    *Rkk = beta;
+    for (int i = 0; i < TR; ++i) v[half * TR + i] = a[i] * sc;
+    if (half == 0) {
+        *tau = (beta - x0) / beta;
+        *Rkk = beta;
+    }
 }
 
-// Fold the register tile a (thread j = column j) into R (n x n, full storage),
-// columns k0..n-1.  vbuf: 2*TR doubles of shared memory, taus: 2 doubles.
-template <int TR>
+// Fold the register tile (thread (j, half) holds rows half*TR.. of column j)
+// into R (n x n, full storage), columns k0..n-1.  vbuf: 2*ROWS doubles of
+// shared memory, taus: 2 doubles.
+template <int TR, int P>
 __device__ void fold_tile(double (&a)[TR], int n, int k0, double* __restrict__ R, double* vbuf, double* taus) {
-    const int j = threadIdx.x;
+    constexpr int ROWS = TR * P;
+    const int j = threadIdx.x / P, half = threadIdx.x % P;
     const bool own = j < n;
     double rnext = (own && j >= k0) ? R[(size_t)k0 * n + j] : 0.0;
-    if (j == k0) make_reflector<TR>(a, rnext, vbuf + (k0 & 1) * TR, taus + (k0 & 1), R + (size_t)k0 * n + k0);
+    {
+        const unsigned m = __ballot_sync(0xffffffffu, j == k0);
+        if (j == k0)
+            make_reflector<TR, P>(a, rnext, vbuf + (k0 & 1) * ROWS, taus + (k0 & 1), R + (size_t)k0 * n + k0, half,
+                                  m);
+    }
     __syncthreads();
     for (int k = k0; k < n; ++k) {
         const double rkj = rnext;
         if (own && j > k && k + 1 < n) rnext = R[(size_t)(k + 1) * n + j];
         const double tau = taus[k & 1];
-        if (own && j > k && tau != 0.0) {
-            const double* v = vbuf + (k & 1) * TR;
-            double w = rkj;
+        const bool upd = own && j > k && tau != 0.0;
+        const unsigned mu = __ballot_sync(0xffffffffu, upd);
+        if (upd) {
+            const double* v = vbuf + (k & 1) * ROWS + half * TR;
+            double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
 #pragma unroll
-            for (int i = 0; i < TR; ++i) w = fma(v[i], a[i], w);
-            const double tw = tau * w;
-            R[(size_t)k * n + j] = rkj - tw;
+            for (int i = 0; i < TR; i += 4) {
+                w0 = fma(v[i], a[i], w0);
+                w1 = fma(v[i + 1], a[i + 1], w1);
+                w2 = fma(v[i + 2], a[i + 2], w2);
+                w3 = fma(v[i + 3], a[i + 3], w3);
+            }
+            double d = (w0 + w1) + (w2 + w3);
+            if (P == 2) d += __shfl_xor_sync(mu, d, 1);
+            const double tw = tau * (rkj + d);
+            if (half == 0) R[(size_t)k * n + j] = rkj - tw;
 #pragma unroll
             for (int i = 0; i < TR; ++i) a[i] = fma(-tw, v[i], a[i]);
         }
-        if (j == k + 1 && k + 1 < n)
-            make_reflector<TR>(a, rnext, vbuf + ((k + 1) & 1) * TR, taus + ((k + 1) & 1),
-                               R + (size_t)(k + 1) * n + (k + 1));
+        const bool nxt = j == k + 1 && k + 1 < n;
+        const unsigned mr = __ballot_sync(0xffffffffu, nxt);
+        if (nxt)
+            make_reflector<TR, P>(a, rnext, vbuf + ((k + 1) & 1) * ROWS, taus + ((k + 1) & 1),
+                                  R + (size_t)(k + 1) * n + (k + 1), half, mr);
         __syncthreads();
     }
 }
 
-template <int TR>
-__global__ void __launch_bounds__(TrBounds<TR>::threads) k_tsqr_leaf(const float* __restrict__ H, int64_t ldh,
-                                                    const float* __restrict__ Y, int64_t N, int M,
-                                                    double* __restrict__ Rws, int64_t rows_per_cta,
-                                                    int* __restrict__ flag) {
-    __shared__ double vbuf[2 * TR];
+template <int TR, int P>
+__global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
+    k_tsqr_leaf(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t N, int M,
+                double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag) {
+    constexpr int ROWS = TR * P;
+    __shared__ double vbuf[2 * ROWS];
     __shared__ double taus[2];
-    const int n = M + 1, j = threadIdx.x;
+    const int n = M + 1, j = threadIdx.x / P, half = threadIdx.x % P;
     double* R = Rws + (size_t)blockIdx.x * n * n;
     if (j < n)
-        for (int k = 0; k < n; ++k) R[(size_t)k * n + j] = 0.0;   // column j is private to thread j
+        for (int k = half; k < n; k += P) R[(size_t)k * n + j] = 0.0;   // column j is private to its threads
     const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
     const int64_t r1 = min(N, r0 + rows_per_cta);
     bool bad = false;
-    for (int64_t base = r0; base < r1; base += TR) {
+    for (int64_t base = r0; base < r1; base += ROWS) {
         double a[TR];
 #pragma unroll
         for (int i = 0; i < TR; ++i) {
-            const int64_t row = base + i;
+            const int64_t row = base + half * TR + i;
             float v = 0.0f;
             if (row < r1 && j < n) v = (j < M) ? __ldg(H + row * ldh + j) : __ldg(Y + row);
             bad |= !isfinite(v);
             a[i] = (double)v;
         }
-        fold_tile<TR>(a, n, 0, R, vbuf, taus);
+        fold_tile<TR, P>(a, n, 0, R, vbuf, taus);
     }
     if (bad) atomicOr(flag, 1);
 }
 
-template <int TR>
-__global__ void __launch_bounds__(TrBounds<TR>::threads) k_tsqr_merge(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n) {
-    __shared__ double vbuf[2 * TR];
+template <int TR, int P>
+__global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
+    k_tsqr_merge(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n) {
+    constexpr int ROWS = TR * P;
+    __shared__ double vbuf[2 * ROWS];
     __shared__ double taus[2];
     const int64_t c = (int64_t)blockIdx.x * 2 * stride, partner = c + stride;
     if (partner >= slabs) return;
     double* Ra = Rws + (size_t)c * n * n;
     const double* Rb = Rws + (size_t)partner * n * n;
-    const int j = threadIdx.x;
-    for (int s = 0; s * TR < n; ++s) {
+    const int j = threadIdx.x / P, half = threadIdx.x % P;
+    for (int s = 0; s * ROWS < n; ++s) {
         double a[TR];
 #pragma unroll
         for (int i = 0; i < TR; ++i) {
-            const int row = s * TR + i;
+            const int row = s * ROWS + half * TR + i;
             a[i] = (row < n && j < n && j >= row) ? Rb[(size_t)row * n + j] : 0.0;
         }
-        fold_tile<TR>(a, n, s * TR, Ra, vbuf, taus);
+        fold_tile<TR, P>(a, n, s * ROWS, Ra, vbuf, taus);
     }
 }
 
@@ -147,7 +186,7 @@ __global__ void k_unpack(const double* __restrict__ Rpk, int P, int n, double* _
 __global__ void k_pack(const double* __restrict__ R, int n, double* __restrict__ Rpk) {
     const int64_t len = (int64_t)n * (n + 1) / 2;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
-        // row k: offset k*n - k(k-1)/2 ; find k by search (n <= 1024, cheap)
+        // row k starts at k*n - k(k-1)/2; find k by bisection (n <= 1024)
         int lo = 0, hi = n - 1;
         while (lo < hi) {
             int mid = (lo + hi + 1) / 2;
@@ -183,33 +222,34 @@ __device__ double block_min(double v, double* red) {
 }
 __device__ double block_max(double v, double* red) { return -block_min(-v, red); }
 
-// Final solve on slab 0 (one CTA, blockDim >= n).  R0 is copied to Rorig
+// Final solve on slab 0 (one CTA of P*n threads).  R0 is copied to Rorig
 // before a ridge refactorisation so rho is measured on the unregularised R.
-template <int TR>
-__global__ void __launch_bounds__(TrBounds<TR>::threads) k_tsqr_solve(double* __restrict__ R, double* __restrict__ Rorig, int M,
-                                                     long long n_total, const int* __restrict__ flag,
-                                                     double* __restrict__ beta, SolveDev* __restrict__ out) {
-    __shared__ double vbuf[2 * TR];
+template <int TR, int P>
+__global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
+    k_tsqr_solve(double* __restrict__ R, double* __restrict__ Rorig, int M, long long n_total,
+                 const int* __restrict__ flag, double* __restrict__ beta, SolveDev* __restrict__ out) {
+    constexpr int ROWS = TR * P;
+    __shared__ double vbuf[2 * ROWS];
     __shared__ double taus[2];
     __shared__ double red[32];
     __shared__ double bk;
-    extern __shared__ double zs[];   // [n] right-hand side / beta
-    const int n = M + 1, j = threadIdx.x;
-    const bool own = j < n;
-    // sign normalisation: flip row k when R_kk < 0 (thread j flips its column
-    // entries; the signs are read into shared memory first)
+    extern __shared__ double zs[];   // [n] signs / right-hand side / beta
+    const int n = M + 1, j = threadIdx.x / P, half = threadIdx.x % P;
+    const bool own = j < n && half == 0;
+    // sign normalisation: flip row k when R_kk < 0 (signs read into smem first)
     if (own) zs[j] = R[(size_t)j * n + j] < 0.0 ? -1.0 : 1.0;
     __syncthreads();
     if (own)
         for (int k = 0; k <= j; ++k) R[(size_t)k * n + j] *= zs[k];
     __syncthreads();
-    double d = (j < M) ? fabs(R[(size_t)j * n + j]) : INFINITY;
-    double dmin = block_min(d, red);
-    double dmax = block_max(j < M ? d : 0.0, red);
+    const bool diag = own && j < M;
+    double d = diag ? fabs(R[(size_t)j * n + j]) : INFINITY;
+    const double dmin = block_min(d, red);
+    const double dmax = block_max(diag ? d : 0.0, red);
     double f2 = 0.0;
-    if (j < M)
+    if (diag)
         for (int k = 0; k <= j; ++k) f2 += R[(size_t)k * n + j] * R[(size_t)k * n + j];
-    double fro2 = block_sum(f2, red);
+    const double fro2 = block_sum(f2, red);
     const bool ridge = !(dmin > DBL_EPSILON * (double)M * dmax);
     double lambda = 0.0;
     if (own)
@@ -217,11 +257,14 @@ __global__ void __launch_bounds__(TrBounds<TR>::threads) k_tsqr_solve(double* __
     if (ridge) {
         lambda = 1e-8 * fro2 / (double)M;
         const double sl = sqrt(lambda);
-        for (int s = 0; s * TR < M; ++s) {
+        for (int s = 0; s * ROWS < M; ++s) {
             double a[TR];
 #pragma unroll
-            for (int i = 0; i < TR; ++i) a[i] = (s * TR + i < M && j == s * TR + i) ? sl : 0.0;
-            fold_tile<TR>(a, n, s * TR, R, vbuf, taus);
+            for (int i = 0; i < TR; ++i) {
+                const int row = s * ROWS + half * TR + i;
+                a[i] = (row < M && j == row) ? sl : 0.0;
+            }
+            fold_tile<TR, P>(a, n, s * ROWS, R, vbuf, taus);
         }
         if (own) zs[j] = R[(size_t)j * n + j] < 0.0 ? -1.0 : 1.0;
         __syncthreads();
@@ -229,25 +272,25 @@ __global__ void __launch_bounds__(TrBounds<TR>::threads) k_tsqr_solve(double* __
             for (int k = 0; k <= j; ++k) R[(size_t)k * n + j] *= zs[k];
         __syncthreads();
     }
-    // back substitution: thread i holds z_i
-    if (j < M) zs[j] = R[(size_t)j * n + M];
+    // back substitution: thread (i, 0) holds z_i
+    if (diag) zs[j] = R[(size_t)j * n + M];
     __syncthreads();
     for (int k = M - 1; k >= 0; --k) {
-        if (j == 0) bk = zs[k] / R[(size_t)k * n + k];
+        if (threadIdx.x == 0) bk = zs[k] / R[(size_t)k * n + k];
         __syncthreads();
-        if (j < k) zs[j] -= R[(size_t)j * n + k] * bk;
-        if (j == k) zs[k] = bk;
+        if (own && j < k) zs[j] -= R[(size_t)j * n + k] * bk;
+        if (own && j == k) zs[k] = bk;
         __syncthreads();
     }
-    if (j < M) beta[j] = zs[j];
+    if (diag) beta[j] = zs[j];
     // rho = || R_orig [beta; -1] ||
     double s = 0.0;
     if (own) {
         for (int c = j; c < M; ++c) s += Rorig[(size_t)j * n + c] * zs[c];
         s -= Rorig[(size_t)j * n + M];
     }
-    double rho2 = block_sum(own ? s * s : 0.0, red);
-    if (j == 0) {
+    const double rho2 = block_sum(own ? s * s : 0.0, red);
+    if (threadIdx.x == 0) {
         out->rho = sqrt(rho2);
         out->rmse = sqrt(rho2) / sqrt((double)n_total);
         out->dmin = dmin;
@@ -261,22 +304,35 @@ __global__ void __launch_bounds__(TrBounds<TR>::threads) k_tsqr_solve(double* __
 
 // ---- host side ---------------------------------------------------------------------
 
-// TR = 32 keeps the tile in ~160 registers per thread (n <= 384 threads);
-// wider problems use TR = 16 under the 1024-thread register budget.
-static int pick_tr(int n) { return n <= 384 ? 32 : 16; }
+// Variants: n <= 288: 2 threads x 24 rows per column (48-row tiles, <= 576
+// threads); n <= 512: 2 x 12 (24-row tiles, <= 1024 threads); else 1 x 12.
+enum class Var { P2T24, P2T12, P1T12 };
+static Var pick_var(int n) { return n <= 288 ? Var::P2T24 : (n <= 512 ? Var::P2T12 : Var::P1T12); }
+static int var_rows(Var v) { return v == Var::P2T24 ? 48 : (v == Var::P2T12 ? 24 : 12); }
+static int var_p(Var v) { return v == Var::P1T12 ? 1 : 2; }
+static int var_threads(Var v, int n) { return (var_p(v) * n + 31) / 32 * 32; }
 
-template <int TR>
-static int leaf_ctas_per_sm(int threads) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tsqr_leaf<TR>, threads, 0);
-    return per_sm < 1 ? 1 : per_sm;
+template <class F>
+static auto dispatch(Var v, F&& f) {
+    switch (v) {
+    case Var::P2T24: return f(std::integral_constant<int, 24>{}, std::integral_constant<int, 2>{});
+    case Var::P2T12: return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 2>{});
+    default: return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 1>{});
+    }
 }
 
 int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
-    const int n = h->M + 1, TR = pick_tr(n), threads = (n + 31) / 32 * 32;
-    int per_sm = TR == 32 ? leaf_ctas_per_sm<32>(threads) : leaf_ctas_per_sm<16>(threads);
+    const int n = h->M + 1;
+    const Var v = pick_var(n);
+    const int threads = var_threads(v, n);
+    int per_sm = dispatch(v, [&](auto tr, auto p) {
+        int ps = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_tsqr_leaf<decltype(tr)::value, decltype(p)::value>,
+                                                      threads, 0);
+        return ps < 1 ? 1 : ps;
+    });
     int64_t maxc = (int64_t)per_sm * h->sm_count;
-    int64_t byrows = (N + TR - 1) / TR;
+    int64_t byrows = (N + var_rows(v) - 1) / var_rows(v);
     int64_t g = byrows < maxc ? byrows : maxc;
     return g < 1 ? 1 : g;
 }
@@ -299,43 +355,38 @@ cudaError_t ensure_solve_ws(elmrnn* h, int64_t slabs) {
     return cudaSuccess;
 }
 
-template <int TR>
-static cudaError_t tree_reduce(elmrnn* h, int64_t slabs) {
-    const int n = h->M + 1, threads = (n + 31) / 32 * 32;
-    for (int64_t stride = 1; stride < slabs; stride *= 2) {
-        int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
-        k_tsqr_merge<TR><<<(unsigned)pairs, threads, 0, h->stream>>>(h->Rws, slabs, stride, n);
-        h->launches++;
-    }
-    return cudaGetLastError();
-}
-
 static cudaError_t tree(elmrnn* h, int64_t slabs) {
-    switch (pick_tr(h->M + 1)) {
-    case 32: return tree_reduce<32>(h, slabs);
-    default: return tree_reduce<16>(h, slabs);
-    }
-}
-
-template <int TR>
-static cudaError_t leaf(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t N, int64_t slabs) {
-    const int n = h->M + 1, threads = (n + 31) / 32 * 32;
-    int64_t rows = (N + slabs - 1) / slabs;
-    rows = (rows + TR - 1) / TR * TR;
-    k_tsqr_leaf<TR><<<(unsigned)slabs, threads, 0, h->stream>>>(H, ldh, Y, N, h->M, h->Rws, rows, h->flag);
-    h->launches++;
-    return cudaGetLastError();
+    const int n = h->M + 1;
+    const Var v = pick_var(n);
+    const int threads = var_threads(v, n);
+    return dispatch(v, [&](auto tr, auto p) {
+        for (int64_t stride = 1; stride < slabs; stride *= 2) {
+            int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
+            k_tsqr_merge<decltype(tr)::value, decltype(p)::value>
+                <<<(unsigned)pairs, threads, 0, h->stream>>>(h->Rws, slabs, stride, n);
+            h->launches++;
+        }
+        return cudaGetLastError();
+    });
 }
 
 cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t N) {
-    int64_t slabs = tsqr_leaf_slabs(h, N);
+    const int n = h->M + 1;
+    const Var v = pick_var(n);
+    const int64_t slabs = tsqr_leaf_slabs(h, N);
     cudaError_t e;
     if ((e = ensure_solve_ws(h, slabs))) return e;
     if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream))) return e;
-    switch (pick_tr(h->M + 1)) {
-    case 32: e = leaf<32>(h, H, ldh, Y, N, slabs); break;
-    default: e = leaf<16>(h, H, ldh, Y, N, slabs); break;
-    }
+    const int rows_tile = var_rows(v);
+    int64_t rows = (N + slabs - 1) / slabs;
+    rows = (rows + rows_tile - 1) / rows_tile * rows_tile;
+    const int threads = var_threads(v, n);
+    e = dispatch(v, [&](auto tr, auto p) {
+        k_tsqr_leaf<decltype(tr)::value, decltype(p)::value>
+            <<<(unsigned)slabs, threads, 0, h->stream>>>(H, ldh, Y, N, h->M, h->Rws, rows, h->flag);
+        h->launches++;
+        return cudaGetLastError();
+    });
     if (e) return e;
     return tree(h, slabs);
 }
@@ -364,21 +415,17 @@ cudaError_t tsqr_merge_packed(elmrnn* h, const double* Rpk_all, int P) {
     return tree(h, P);
 }
 
-template <int TR>
-static cudaError_t solve_t(elmrnn* h, int64_t n_total, double* beta) {
-    const int n = h->M + 1, threads = (n + 31) / 32 * 32;
-    double* Rorig = h->Rws + (size_t)(h->Rws_slabs - 1) * n * n;
-    k_tsqr_solve<TR><<<1, threads, n * sizeof(double), h->stream>>>(h->Rws, Rorig, h->M, (long long)n_total, h->flag,
-                                                                     beta, h->sdev);
-    h->launches++;
-    return cudaGetLastError();
-}
-
 cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta) {
-    switch (pick_tr(h->M + 1)) {
-    case 32: return solve_t<32>(h, n_total, beta);
-    default: return solve_t<16>(h, n_total, beta);
-    }
+    const int n = h->M + 1;
+    const Var v = pick_var(n);
+    const int threads = var_threads(v, n);
+    double* Rorig = h->Rws + (size_t)(h->Rws_slabs - 1) * n * n;
+    return dispatch(v, [&](auto tr, auto p) {
+        k_tsqr_solve<decltype(tr)::value, decltype(p)::value><<<1, threads, n * sizeof(double), h->stream>>>(
+            h->Rws, Rorig, h->M, (long long)n_total, h->flag, beta, h->sdev);
+        h->launches++;
+        return cudaGetLastError();
+    });
 }
 
 // ---- predict: Eq. 4, yhat_i = sum_j beta_j H[i][j] ------------------------

@@ -107,6 +107,24 @@ def test_H_parity(arch, N, S, M, Q, o, yfb):
     assert err <= H_TOL, f"max |dH| = {err:.3e}"
 
 
+# tcgen05 LSTM builder (3-pass fp16 hi/lo split): ragged tiles, Q = 1, S padded 3 -> 4
+TC_CASES = [(256, 333, 50, 1), (256, 129, 1, 1), (128, 1000, 10, 3), (128, 257, 30, 4), (256, 2100, 20, 2),
+            (128, 64, 7, 1)]
+
+
+@pytest.mark.parametrize("M,N,Q,S", TC_CASES)
+def test_tc_lstm_parity(M, N, Q, S):
+    X, Y, _ = inputs(N, Q, S, seed=M + Q)
+    e, Hg = gpu_H("lstm", S, M, Q, 4, X, force_path=2)
+    assert e.path == 2
+    net = orc.Net("lstm", S=S, M=M, Q=Q)
+    Ho = orc.build_H(net, orc.gen_weights(net, 4), X, threads=8)
+    err = np.abs(Hg - Ho).max()
+    assert err <= H_TOL, f"max |dH| = {err:.3e}"
+    _, Hf = gpu_H("lstm", S, M, Q, 4, X, force_path=1)
+    assert np.abs(Hf - Ho).max() <= H_TOL
+
+
 def test_H_written_once_and_ld_respected():
     N, M, Q = 100, 20, 10
     X, _, _ = inputs(N, Q, 1)
