@@ -16,10 +16,10 @@
 //   smem: A = h(t-1) hi/lo, K-major SW128 (128 KB at M = 256)
 //         B ring: 3 stages x (hi + lo) 128 x 64 fp16 U slices (32 KB each)
 //   TMEM: 2 x 128 accumulator columns (double buffered) + M columns of h(t)
-//   warps: 0 = bulk-copy producer (one thread) + TMEM allocator, 1 = MMA
-//          issuer (one thread), 2..17 = epilogue (4 per TMEM lane quadrant;
-//          a thread owns one row and 8 neurons per chunk and keeps c(t) for
-//          its M/4 neurons in registers).
+//   warps: 0..15 = epilogue (4 per TMEM lane quadrant; a thread owns one row
+//          and 8 neurons per chunk and keeps c(t) for its M/4 neurons in
+//          registers), 16 = bulk-copy producer (one thread) + TMEM allocator,
+//          17 = MMA issuer (one thread; the highest warp id has issue priority).
 //   per step: NCH = M/32 chunks of 32 neurons x 4 gates = 128 accumulator
 //   columns; chunk n+1's MMAs overlap chunk n's epilogue.  After the last
 //   chunk the epilogue converts h(t) (TMEM) to fp16 hi/lo into A and
@@ -46,7 +46,8 @@ constexpr int kTcStages = 3;
 constexpr int kTcSliceBytes = 128 * 64 * 2;      // one 128 x 64 fp16 SW128 tile
 constexpr int kTcStageBytes = 2 * kTcSliceBytes;  // hi + lo
 constexpr int kTcEpiWarps = 16;                 // 4 per TMEM lane quadrant, 8 neurons per chunk each
-constexpr int kTcCtlWarps = 2;                  // 0: bulk-copy producer + TMEM alloc, 1: MMA issuer
+constexpr int kTcCtlWarps = 2;                  // 16: bulk-copy producer + TMEM alloc, 17: MMA issuer
+constexpr int kTcProdWarp = kTcEpiWarps, kTcMmaWarp = kTcEpiWarps + 1;
 constexpr int kTcThreads = (kTcCtlWarps + kTcEpiWarps) * 32;
 constexpr int kTcWbMax = 7168;                    // floats of W|b in the parameter block
 
@@ -123,8 +124,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
     uint64_t* empty = bars + kTcStages;          // [kTcStages]
     uint64_t* acc_full = bars + 2 * kTcStages;   // [2]
     uint64_t* acc_empty = acc_full + 2;          // [2]
-    uint64_t* a_ready = acc_empty + 2;           // [1]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_ready + 1);
+    uint64_t* a_ready = acc_empty + 2;           // [KS]: K-slice ks of A = h(t-1) is in TMEM
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_ready + C::KS);
     uint32_t* trace_cnt = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -137,11 +138,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
             ptx::mbar_init(acc_full + i, 1);
             ptx::mbar_init(acc_empty + i, kTcEpiWarps);
         }
-        ptx::mbar_init(a_ready, kTcEpiWarps);
+        for (int i = 0; i < C::KS; ++i) ptx::mbar_init(a_ready + i, kTcEpiWarps);
         *trace_cnt = 0;
         ptx::fence_mbar_init();
     }
-    if (warp == 0) {
+    if (warp == kTcProdWarp) {
         ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
         ptx::tmem_relinquish();
     }
@@ -151,56 +152,66 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
     const uint32_t tmem = *tmem_slot;
     const int64_t steps_total = ((p.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x) * p.Q;
 
-    if (warp == 0) {
-        // ---------------- producer: stream U slices (chunk, K-slice) from L2
-        if (lane == 0) {
-            uint32_t st = 0, ph = 0;
-            for (int64_t s = 0; s < steps_total; ++s) {
-                for (int c = 0; c < C::NCH * C::KS; ++c) {
-                    ptx::mbar_wait(empty + st, ph ^ 1);
+    if (warp == kTcProdWarp) {
+        // ---------------- producer: stream U slices (chunk, K-slice) from L2.
+        // The whole warp runs the loop (warp-uniform state lives in uniform
+        // registers); one elected lane issues.
+        uint32_t st = 0, ph = 0;
+        for (int64_t s = 0; s < steps_total; ++s) {
+            for (int c = 0; c < C::NCH * C::KS; ++c) {
+                ptx::mbar_wait(empty + st, ph ^ 1);
+                if (ptx::elect_one()) {
                     ptx::mbar_arrive_expect_tx(full + st, kTcStageBytes);
                     ptx::bulk_g2s(stages + st * kTcStageBytes, p.Uimg + (size_t)c * kTcStageBytes, kTcStageBytes,
                                   full + st);
-                    if (++st == kTcStages) { st = 0; ph ^= 1; }
                 }
+                __syncwarp();
+                if (++st == kTcStages) { st = 0; ph ^= 1; }
             }
         }
-    } else if (warp == 1) {
-        // ---------------- MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_f16(128, 128);
-            const uint32_t a_hi = tmem + C::A_HI, a_lo = tmem + C::A_LO;   // A operand in TMEM
-            const uint32_t b0 = ptx::smem_u32(stages);
-            uint32_t st = 0, ph = 0, ach = 0, aph = 0;
-            for (int64_t s = 0; s < steps_total; ++s) {
-                ptx::mbar_wait(a_ready, (uint32_t)(s & 1));   // h(t-1) hi/lo is in A
-                trace_ev(p, trace_cnt, 1, (int)s, 0);
+    } else if (warp == kTcMmaWarp) {
+        // ---------------- MMA issuer (highest warp id = highest issue priority
+        // on its SM sub-partition).  Warp-uniform loop, one elected lane issues
+        // the 12 MMAs of a K-slice; descriptors and TMEM addresses advance by
+        // plain adds (the SW128 start field is in 16-byte units).
+        constexpr uint32_t idesc = ptx::idesc_f16(128, 128);
+        const uint32_t a_hi = tmem + C::A_HI, a_lo = tmem + C::A_LO;   // A operand in TMEM
+        const uint64_t dbase = ptx::desc_sw128_kmajor(ptx::smem_u32(stages));
+        uint32_t st = 0, ph = 0, ach = 0, aph = 0;
+        for (int64_t s = 0; s < steps_total; ++s) {
+            if (lane == 0) trace_ev(p, trace_cnt, 1, (int)s, 0);
+            for (int n = 0; n < C::NCH; ++n) {
+                ptx::mbar_wait(acc_empty + ach, aph ^ 1);
                 ptx::tc_fence_after();
-                for (int n = 0; n < C::NCH; ++n) {
-                    ptx::mbar_wait(acc_empty + ach, aph ^ 1);
-                    ptx::tc_fence_after();
-                    trace_ev(p, trace_cnt, 2, (int)s, n);
-                    const uint32_t d = tmem + ach * 128;
-                    for (int ks = 0; ks < C::KS; ++ks) {
-                        ptx::mbar_wait(full + st, ph);
+                const uint32_t d = tmem + ach * 128;
+                for (int ks = 0; ks < C::KS; ++ks) {
+                    if (n == 0) {   // first chunk of a step: K-slice ks of h(t-1) must be in TMEM
+                        ptx::mbar_wait(a_ready + ks, (uint32_t)(s & 1));
                         ptx::tc_fence_after();
-                        const uint32_t bh = b0 + st * kTcStageBytes, bl = bh + kTcSliceBytes;
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            const uint32_t tah = a_hi + ks * 32 + kk * 8, tal = a_lo + ks * 32 + kk * 8;
-                            const uint64_t dbh = ptx::desc_sw128_kmajor(bh + kk * 32);
-                            const uint64_t dbl = ptx::desc_sw128_kmajor(bl + kk * 32);
-                            ptx::mma_f16_ts(d, tah, dbh, idesc, (ks | kk) != 0);
-                            ptx::mma_f16_ts(d, tah, dbl, idesc, 1);
-                            ptx::mma_f16_ts(d, tal, dbh, idesc, 1);
-                        }
-                        ptx::mma_commit(empty + st);                      // frees the U stage
-                        if (++st == kTcStages) { st = 0; ph ^= 1; }
                     }
-                    ptx::mma_commit(acc_full + ach);                      // chunk accumulator ready
-                    trace_ev(p, trace_cnt, 3, (int)s, n);
-                    if (++ach == 2) { ach = 0; aph ^= 1; }
+                    ptx::mbar_wait(full + st, ph);
+                    ptx::tc_fence_after();
+                    const uint64_t dbh = dbase + (uint64_t)((st * kTcStageBytes) >> 4);
+                    const uint64_t dbl = dbh + (uint64_t)(kTcSliceBytes >> 4);
+                    const uint32_t tah = a_hi + ks * 32, tal = a_lo + ks * 32;
+                    if (ptx::elect_one()) {
+                        ptx::mma_f16_ts(d, tah, dbh, idesc, ks != 0);
+                        ptx::mma_f16_ts(d, tah, dbl, idesc, 1);
+                        ptx::mma_f16_ts(d, tal, dbh, idesc, 1);
+#pragma unroll
+                        for (int kk = 1; kk < 4; ++kk) {
+                            ptx::mma_f16_ts(d, tah + kk * 8, dbh + 2 * kk, idesc, 1);
+                            ptx::mma_f16_ts(d, tah + kk * 8, dbl + 2 * kk, idesc, 1);
+                            ptx::mma_f16_ts(d, tal + kk * 8, dbh + 2 * kk, idesc, 1);
+                        }
+                        ptx::mma_commit(empty + st);                  // frees the U stage
+                        if (ks == C::KS - 1) ptx::mma_commit(acc_full + ach);   // chunk accumulator ready
+                    }
+                    __syncwarp();
+                    if (++st == kTcStages) { st = 0; ph ^= 1; }
                 }
+                if (lane == 0) trace_ev(p, trace_cnt, 3, (int)s, n);
+                if (++ach == 2) { ach = 0; aph ^= 1; }
             }
         }
     } else {
@@ -208,7 +219,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
         // Pre-activations stay in the 2^sigma-scaled domain: W, b were scaled on
         // the host, and 2^-sigma is folded into the exp2 argument constants.
         // epilogue warp w: TMEM lane quadrant w % 4 (hardware rule), neuron group u
-        const int e = warp - kTcCtlWarps, q = warp & 3, u = e >> 2;
+        const int e = warp, q = warp & 3, u = e >> 2;
         const int r = 32 * q + lane;                 // tile row = TMEM lane
         const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
         const float kS = p.k_sig, kT = p.k_tanh;     // -log2e 2^-sigma, 2 log2e 2^-sigma
@@ -225,8 +236,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(a_ready);
+            if (lane == 0)
+                for (int ks = 0; ks < C::KS; ++ks) ptx::mbar_arrive(a_ready + ks);
         }
+        // Publish K-slices [k0, k1) of h(t) (staged fp16 hi|lo words) into the
+        // TMEM A operand -- or zeros, h(0) of the next tile, after the last step.
+        auto publish = [&](int k0, int k1, bool zero) {
+#pragma unroll
+            for (int n = 0; n < C::NCH; ++n) {
+                if (n < 2 * k0 || n >= 2 * k1) continue;
+                uint32_t hi[4], lo[4];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    hi[w] = zero ? 0u : my_stg[(n * 8 + w) * 32];
+                    lo[w] = zero ? 0u : my_stg[(n * 8 + 4 + w) * 32];
+                }
+                ptx::tmem_st4(lane_base + C::A_HI + n * 16 + 4 * u, hi);
+                ptx::tmem_st4(lane_base + C::A_LO + n * 16 + 4 * u, lo);
+            }
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0)
+                for (int ks = k0; ks < k1; ++ks) ptx::mbar_arrive(a_ready + ks);
+        };
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             const int64_t row = tile * kTcRows + r;
             const bool valid = row < p.N;
@@ -250,6 +283,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(acc_empty + ach);   // accumulator drained
+                    // The last chunk's accumulator implies every MMA of step t is done:
+                    // release K-slices 0..KS-2 of h(t) now, so step t+1's first MMAs
+                    // overlap this chunk's epilogue (its own slice follows below).
+                    if (n == C::NCH - 1) publish(0, C::KS - 1, t == p.Q);
                     float hv[8];
                     // MUFU budget: 5 ex2 + 1.25 rcp per element.  The four gate
                     // denominators of a neuron share one reciprocal (1/a = bcd/(abcd)),
@@ -318,31 +355,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                     if (e == 0 && lane == 0) trace_ev(p, trace_cnt, 5, t, n);
                     if (++ach == 2) { ach = 0; aph ^= 1; }
                 }
-                // all MMAs of step t are complete (the last chunk's commit covers
-                // them): move h(t) into the TMEM A operand, or zero it for the next tile
-                const bool last = (t == p.Q);
-#pragma unroll
-                for (int n = 0; n < C::NCH; ++n) {
-                    uint32_t hi[4], lo[4];
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        hi[w] = last ? 0u : my_stg[(n * 8 + w) * 32];
-                        lo[w] = last ? 0u : my_stg[(n * 8 + 4 + w) * 32];
-                    }
-                    ptx::tmem_st4(lane_base + C::A_HI + n * 16 + 4 * u, hi);
-                    ptx::tmem_st4(lane_base + C::A_LO + n * 16 + 4 * u, lo);
-                }
-                ptx::tmem_wait_st();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(a_ready);
+                publish(C::KS - 1, C::KS, t == p.Q);
                 if (e == 0 && lane == 0) trace_ev(p, trace_cnt, 6, t, 0);
             }
         }
     }
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 0) {
+    if (warp == kTcProdWarp) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, C::TMEM_COLS);
     }

@@ -40,12 +40,38 @@ struct Fold {
     static constexpr int MAX_THREADS = (P == 2 && TR == 24) ? 576 : 1024;
 };
 
-// Reflector of column k from x0 = R[k][k] and the tile column (this thread's
-// TR rows; the partner lane holds the rest), LAPACK dlarfg convention,
-// sign(0) = +1.  Both threads of the column compute it; half 0 publishes
-// tau and R[k][k].
+// Fast fp64 reciprocal / square root: hardware approximation + Newton steps
+// (the reflector is on the per-column critical path; IEEE div/sqrt sequences
+// cost hundreds of cycles of dependent latency).  Outside a safe exponent
+// range the IEEE forms are used.
+__device__ __forceinline__ double rcp_fast(double d) {
+    const double ad = fabs(d);
+    if (!(ad > 1e-250 && ad < 1e250)) return 1.0 / d;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+__device__ __forceinline__ double sqrt_fast(double t) {
+    if (!(t > 1e-250 && t < 1e250)) return sqrt(t);
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(t));
+    y = y * fma(-0.5 * t * y, y, 1.5);
+    double s = t * y;
+    return fma(0.5 * y, fma(-s, s, t), s);
+}
+
+// Reflector of column k from x0 = R[k][k] and the tile column a (this thread's
+// TR rows; the partner lane holds the rest), in the unnormalised form
+//   H = I + g u u^T,  u = [x0 - beta; a],  g = 1 / (beta (x0 - beta)),
+//   beta = -sign(x0) ||(x0, a)||,  sign(0) = +1,
+// which equals LAPACK's I - tau v v^T (v = u / u0, tau = (beta - x0)/beta)
+// with one reciprocal and no scaling of u.  ||a|| = 0 gives H = I (g = 0).
+// Both threads of the column compute it; half 0 publishes (g, u0) and R[k][k].
 template <int TR, int P>
-__device__ __forceinline__ void make_reflector(const double (&a)[TR], double x0, double* v, double* tau, double* Rkk,
+__device__ __forceinline__ void make_reflector(const double (&a)[TR], double x0, double* v, double* coef, double* Rkk,
                                                int half, unsigned mask) {
     double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
 #pragma unroll
@@ -58,74 +84,230 @@ __device__ __forceinline__ void make_reflector(const double (&a)[TR], double x0,
     double s2 = (p0 + p1) + (p2 + p3);
     if (P == 2) s2 += __shfl_xor_sync(mask, s2, 1);
     if (s2 == 0.0) {
-        if (half == 0) *tau = 0.0;
+        if (half == 0) coef[0] = 0.0;
         return;
     }
-    const double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * sqrt(fma(x0, x0, s2));
-    const double sc = 1.0 / (x0 - beta);
+    const double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * sqrt_fast(fma(x0, x0, s2));
+    const double u0 = x0 - beta;
 #pragma unroll
-    for (int i = 0; i < TR; ++i) v[half * TR + i] = a[i] * sc;
+    for (int i = 0; i < TR; ++i) v[half * TR + i] = a[i];
     if (half == 0) {
-        *tau = (beta - x0) / beta;
+        coef[0] = rcp_fast(beta * u0);
+        coef[1] = u0;
         *Rkk = beta;
     }
 }
 
 // Fold the register tile (thread (j, half) holds rows half*TR.. of column j)
 // into R (n x n, full storage), columns k0..n-1.  vbuf: 2*ROWS doubles of
-// shared memory, taus: 2 doubles.
+// shared memory (u tails), coefs: 2 x (g, u0).
 template <int TR, int P>
-__device__ void fold_tile(double (&a)[TR], int n, int k0, double* __restrict__ R, double* vbuf, double* taus) {
+__device__ void fold_tile(double (&a)[TR], int n, int k0, double* __restrict__ R, double* vbuf, double* coefs) {
     constexpr int ROWS = TR * P;
     const int j = threadIdx.x / P, half = threadIdx.x % P;
     const bool own = j < n;
-    double rnext = (own && j >= k0) ? R[(size_t)k0 * n + j] : 0.0;
+    // R[k][j] for the next three rows are prefetched into registers: the
+    // reflector of column k+1 needs R[k+1][k+1] right after its own update,
+    // so its L2 latency must be hidden two columns ahead.
+    const double* Rj = R + j;
+    auto ld = [&](int row) -> double { return (own && row < n && j >= row) ? Rj[(size_t)row * n] : 0.0; };
+    double rq0 = ld(k0), rq1 = ld(k0 + 1), rq2 = ld(k0 + 2);
     {
         const unsigned m = __ballot_sync(0xffffffffu, j == k0);
         if (j == k0)
-            make_reflector<TR, P>(a, rnext, vbuf + (k0 & 1) * ROWS, taus + (k0 & 1), R + (size_t)k0 * n + k0, half,
-                                  m);
+            make_reflector<TR, P>(a, rq0, vbuf + (k0 & 1) * ROWS, coefs + 2 * (k0 & 1), R + (size_t)k0 * n + k0,
+                                  half, m);
     }
     __syncthreads();
     for (int k = k0; k < n; ++k) {
-        const double rkj = rnext;
-        if (own && j > k && k + 1 < n) rnext = R[(size_t)(k + 1) * n + j];
-        const double tau = taus[k & 1];
-        const bool upd = own && j > k && tau != 0.0;
+        const double rkj = rq0;
+        rq0 = rq1;
+        rq1 = rq2;
+        rq2 = ld(k + 3);
+        const double g = coefs[2 * (k & 1)], u0 = coefs[2 * (k & 1) + 1];
+        const bool upd = own && j > k && g != 0.0;
         const unsigned mu = __ballot_sync(0xffffffffu, upd);
         if (upd) {
-            const double* v = vbuf + (k & 1) * ROWS + half * TR;
-            double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+            const double2* v = reinterpret_cast<const double2*>(vbuf + (k & 1) * ROWS + half * TR);
+            double w0 = (half == 0) ? u0 * rkj : 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
 #pragma unroll
             for (int i = 0; i < TR; i += 4) {
-                w0 = fma(v[i], a[i], w0);
-                w1 = fma(v[i + 1], a[i + 1], w1);
-                w2 = fma(v[i + 2], a[i + 2], w2);
-                w3 = fma(v[i + 3], a[i + 3], w3);
+                const double2 va = v[i / 2], vb = v[i / 2 + 1];
+                w0 = fma(va.x, a[i], w0);
+                w1 = fma(va.y, a[i + 1], w1);
+                w2 = fma(vb.x, a[i + 2], w2);
+                w3 = fma(vb.y, a[i + 3], w3);
             }
-            double d = (w0 + w1) + (w2 + w3);
-            if (P == 2) d += __shfl_xor_sync(mu, d, 1);
-            const double tw = tau * (rkj + d);
-            if (half == 0) R[(size_t)k * n + j] = rkj - tw;
+            double w = (w0 + w1) + (w2 + w3);
+            if (P == 2) w += __shfl_xor_sync(mu, w, 1);
+            const double f = g * w;                      // x_j += f u
+            if (half == 0) R[(size_t)k * n + j] = fma(f, u0, rkj);
 #pragma unroll
-            for (int i = 0; i < TR; ++i) a[i] = fma(-tw, v[i], a[i]);
+            for (int i = 0; i < TR; i += 2) {
+                const double2 vv = v[i / 2];
+                a[i] = fma(f, vv.x, a[i]);
+                a[i + 1] = fma(f, vv.y, a[i + 1]);
+            }
         }
         const bool nxt = j == k + 1 && k + 1 < n;
         const unsigned mr = __ballot_sync(0xffffffffu, nxt);
         if (nxt)
-            make_reflector<TR, P>(a, rnext, vbuf + ((k + 1) & 1) * ROWS, taus + ((k + 1) & 1),
+            make_reflector<TR, P>(a, rq0, vbuf + ((k + 1) & 1) * ROWS, coefs + 2 * ((k + 1) & 1),
                                   R + (size_t)(k + 1) * n + (k + 1), half, mr);
         __syncthreads();
     }
 }
 
-template <int TR, int P>
+// ---- blocked fold (panels of kNB columns) -------------------------------------------
+// Same reflectors as fold_tile, applied panel by panel: the warp owning the
+// kNB panel columns factors the panel warp-synchronously (shuffles and
+// __syncwarp, no block barriers), publishing the reflector tails Y and
+// (g, u0) in shared memory; then every trailing column applies the kNB
+// reflectors back to back.  The R rows of the panel live in shared memory
+// for the duration of the panel.  Four block barriers per panel instead of
+// one per column.  Requires P = 2 and k0 % kNB == 0.
+constexpr int kNB = 16;
+
+template <int TR>
+__device__ void fold_tile_blk(double (&a)[TR], int n, int k0, double* __restrict__ R, double* Rp, double* Yb,
+                              double* cf) {
+    constexpr int ROWS = 2 * TR;
+    const int tid = threadIdx.x, j = tid >> 1, half = tid & 1, warp = tid >> 5;
+    const bool own = j < n;
+    for (int pk = k0; pk < n; pk += kNB) {
+        const int pe = min(pk + kNB, n), np = pe - pk;
+        for (int idx = tid; idx < np * n; idx += blockDim.x) {
+            const int r = idx / n, c = idx - r * n;
+            Rp[idx] = (c >= pk + r) ? R[(size_t)(pk + r) * n + c] : 0.0;
+        }
+        __syncthreads();
+        if (warp == (pk >> 4)) {
+            // ---- panel factorisation (columns pk..pe-1 live in this warp)
+            for (int kk = pk; kk < pe; ++kk) {
+                const int r = kk - pk;
+                double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+                if (j == kk) {
+#pragma unroll
+                    for (int i = 0; i < TR; i += 4) {
+                        p0 = fma(a[i], a[i], p0);
+                        p1 = fma(a[i + 1], a[i + 1], p1);
+                        p2 = fma(a[i + 2], a[i + 2], p2);
+                        p3 = fma(a[i + 3], a[i + 3], p3);
+                    }
+                }
+                double s2 = (p0 + p1) + (p2 + p3);
+                s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+                if (j == kk) {
+                    double g = 0.0, u0 = 0.0;
+                    if (s2 != 0.0) {
+                        const double x0 = Rp[r * n + kk];
+                        const double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * sqrt_fast(fma(x0, x0, s2));
+                        u0 = x0 - beta;
+                        g = rcp_fast(beta * u0);
+                        if (half == 0) Rp[r * n + kk] = beta;
+                    }
+#pragma unroll
+                    for (int i = 0; i < TR; ++i) Yb[r * ROWS + half * TR + i] = a[i];
+                    if (half == 0) {
+                        cf[2 * r] = g;
+                        cf[2 * r + 1] = u0;
+                    }
+                }
+                __syncwarp();
+                const double g = cf[2 * r], u0 = cf[2 * r + 1];
+                const bool upd = j > kk && j < pe && g != 0.0;
+                double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+                if (upd) {
+                    const double2* y = reinterpret_cast<const double2*>(Yb + r * ROWS + half * TR);
+                    if (half == 0) w0 = u0 * Rp[r * n + j];
+#pragma unroll
+                    for (int i = 0; i < TR; i += 4) {
+                        const double2 ya = y[i / 2], yb = y[i / 2 + 1];
+                        w0 = fma(ya.x, a[i], w0);
+                        w1 = fma(ya.y, a[i + 1], w1);
+                        w2 = fma(yb.x, a[i + 2], w2);
+                        w3 = fma(yb.y, a[i + 3], w3);
+                    }
+                }
+                double w = (w0 + w1) + (w2 + w3);
+                w += __shfl_xor_sync(0xffffffffu, w, 1);
+                if (upd) {
+                    const double f = g * w;
+                    const double2* y = reinterpret_cast<const double2*>(Yb + r * ROWS + half * TR);
+                    if (half == 0) Rp[r * n + j] = fma(f, u0, Rp[r * n + j]);
+#pragma unroll
+                    for (int i = 0; i < TR; i += 2) {
+                        const double2 yy = y[i / 2];
+                        a[i] = fma(f, yy.x, a[i]);
+                        a[i + 1] = fma(f, yy.y, a[i + 1]);
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        // ---- trailing update: columns j >= pe apply the panel's reflectors in order
+        if (warp >= (pe >> 4) || (pe & 15)) {
+            const bool act = own && j >= pe;
+            for (int r = 0; r < np; ++r) {
+                const double g = cf[2 * r], u0 = cf[2 * r + 1];
+                if (g == 0.0) continue;
+                double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+                const double2* y = reinterpret_cast<const double2*>(Yb + r * ROWS + half * TR);
+                if (act) {
+                    if (half == 0) w0 = u0 * Rp[r * n + j];
+#pragma unroll
+                    for (int i = 0; i < TR; i += 4) {
+                        const double2 ya = y[i / 2], yb = y[i / 2 + 1];
+                        w0 = fma(ya.x, a[i], w0);
+                        w1 = fma(ya.y, a[i + 1], w1);
+                        w2 = fma(yb.x, a[i + 2], w2);
+                        w3 = fma(yb.y, a[i + 3], w3);
+                    }
+                }
+                double w = (w0 + w1) + (w2 + w3);
+                w += __shfl_xor_sync(0xffffffffu, w, 1);
+                if (act) {
+                    const double f = g * w;
+                    if (half == 0) Rp[r * n + j] = fma(f, u0, Rp[r * n + j]);
+#pragma unroll
+                    for (int i = 0; i < TR; i += 2) {
+                        const double2 yy = y[i / 2];
+                        a[i] = fma(f, yy.x, a[i]);
+                        a[i + 1] = fma(f, yy.y, a[i + 1]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        for (int idx = tid; idx < np * n; idx += blockDim.x) {
+            const int r = idx / n, c = idx - r * n;
+            if (c >= pk + r) R[(size_t)(pk + r) * n + c] = Rp[idx];
+        }
+        __syncthreads();
+    }
+}
+
+// fold dispatcher: BLK selects the panel-blocked sweep (P = 2 only)
+template <int TR, int P, bool BLK>
+__device__ __forceinline__ void fold(double (&a)[TR], int n, int k0, double* R, double* vbuf, double* coefs,
+                                     double* dsm) {
+    if constexpr (BLK) {
+        fold_tile_blk<TR>(a, n, k0, R, dsm, dsm + kNB * n, dsm + kNB * n + kNB * 2 * TR);
+    } else {
+        fold_tile<TR, P>(a, n, k0, R, vbuf, coefs);
+    }
+}
+__host__ __device__ constexpr size_t blk_smem_doubles(int n, int TR) { return (size_t)kNB * n + kNB * 2 * TR + 2 * kNB; }
+
+template <int TR, int P, bool BLK>
 __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
     k_tsqr_leaf(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t N, int M,
                 double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag) {
     constexpr int ROWS = TR * P;
-    __shared__ double vbuf[2 * ROWS];
-    __shared__ double taus[2];
+    __shared__ __align__(16) double vbuf[2 * ROWS];
+    __shared__ double coefs[4];
+    extern __shared__ __align__(16) double dsm[];
     const int n = M + 1, j = threadIdx.x / P, half = threadIdx.x % P;
     double* R = Rws + (size_t)blockIdx.x * n * n;
     if (j < n)
@@ -143,17 +325,18 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
             bad |= !isfinite(v);
             a[i] = (double)v;
         }
-        fold_tile<TR, P>(a, n, 0, R, vbuf, taus);
+        fold<TR, P, BLK>(a, n, 0, R, vbuf, coefs, dsm);
     }
     if (bad) atomicOr(flag, 1);
 }
 
-template <int TR, int P>
+template <int TR, int P, bool BLK>
 __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
     k_tsqr_merge(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n) {
     constexpr int ROWS = TR * P;
-    __shared__ double vbuf[2 * ROWS];
-    __shared__ double taus[2];
+    __shared__ __align__(16) double vbuf[2 * ROWS];
+    __shared__ double coefs[4];
+    extern __shared__ __align__(16) double dsm[];
     const int64_t c = (int64_t)blockIdx.x * 2 * stride, partner = c + stride;
     if (partner >= slabs) return;
     double* Ra = Rws + (size_t)c * n * n;
@@ -166,7 +349,7 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
             const int row = s * ROWS + half * TR + i;
             a[i] = (row < n && j < n && j >= row) ? Rb[(size_t)row * n + j] : 0.0;
         }
-        fold_tile<TR, P>(a, n, s * ROWS, Ra, vbuf, taus);
+        fold<TR, P, BLK>(a, n, s * ROWS, Ra, vbuf, coefs, dsm);
     }
 }
 
@@ -224,16 +407,16 @@ __device__ double block_max(double v, double* red) { return -block_min(-v, red);
 
 // Final solve on slab 0 (one CTA of P*n threads).  R0 is copied to Rorig
 // before a ridge refactorisation so rho is measured on the unregularised R.
-template <int TR, int P>
+template <int TR, int P, bool BLK>
 __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
     k_tsqr_solve(double* __restrict__ R, double* __restrict__ Rorig, int M, long long n_total,
                  const int* __restrict__ flag, double* __restrict__ beta, SolveDev* __restrict__ out) {
     constexpr int ROWS = TR * P;
-    __shared__ double vbuf[2 * ROWS];
-    __shared__ double taus[2];
+    __shared__ __align__(16) double vbuf[2 * ROWS];
+    __shared__ double coefs[4];
     __shared__ double red[32];
     __shared__ double bk;
-    extern __shared__ double zs[];   // [n] signs / right-hand side / beta
+    extern __shared__ __align__(16) double zs[];   // [n] signs / rhs / beta, then the blocked-fold buffers
     const int n = M + 1, j = threadIdx.x / P, half = threadIdx.x % P;
     const bool own = j < n && half == 0;
     // sign normalisation: flip row k when R_kk < 0 (signs read into smem first)
@@ -264,7 +447,7 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
                 const int row = s * ROWS + half * TR + i;
                 a[i] = (row < M && j == row) ? sl : 0.0;
             }
-            fold_tile<TR, P>(a, n, s * ROWS, R, vbuf, taus);
+            fold<TR, P, BLK>(a, n, s * ROWS, R, vbuf, coefs, zs + ((n + 1) & ~1));
         }
         if (own) zs[j] = R[(size_t)j * n + j] < 0.0 ? -1.0 : 1.0;
         __syncthreads();
@@ -306,18 +489,22 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
 
 // Variants: n <= 288: 2 threads x 24 rows per column (48-row tiles, <= 576
 // threads); n <= 512: 2 x 12 (24-row tiles, <= 1024 threads); else 1 x 12.
-enum class Var { P2T24, P2T12, P1T12 };
-static Var pick_var(int n) { return n <= 288 ? Var::P2T24 : (n <= 512 ? Var::P2T12 : Var::P1T12); }
-static int var_rows(Var v) { return v == Var::P2T24 ? 48 : (v == Var::P2T12 ? 24 : 12); }
+enum class Var { B2T24, P2T12, P1T12 };
+static Var pick_var(int n) { return n <= 288 ? Var::B2T24 : (n <= 512 ? Var::P2T12 : Var::P1T12); }
+static int var_rows(Var v) { return v == Var::B2T24 ? 48 : (v == Var::P2T12 ? 24 : 12); }
 static int var_p(Var v) { return v == Var::P1T12 ? 1 : 2; }
+static bool var_blk(Var v) { return v == Var::B2T24; }
+static size_t var_smem(Var v, int n) { return var_blk(v) ? blk_smem_doubles(n, 24) * sizeof(double) : 0; }
 static int var_threads(Var v, int n) { return (var_p(v) * n + 31) / 32 * 32; }
 
 template <class F>
 static auto dispatch(Var v, F&& f) {
     switch (v) {
-    case Var::P2T24: return f(std::integral_constant<int, 24>{}, std::integral_constant<int, 2>{});
-    case Var::P2T12: return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 2>{});
-    default: return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 1>{});
+    case Var::B2T24:
+        return f(std::integral_constant<int, 24>{}, std::integral_constant<int, 2>{}, std::true_type{});
+    case Var::P2T12:
+        return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 2>{}, std::false_type{});
+    default: return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 1>{}, std::false_type{});
     }
 }
 
@@ -325,10 +512,10 @@ int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
     const int n = h->M + 1;
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
-    int per_sm = dispatch(v, [&](auto tr, auto p) {
+    int per_sm = dispatch(v, [&](auto tr, auto p, auto b) {
         int ps = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_tsqr_leaf<decltype(tr)::value, decltype(p)::value>,
-                                                      threads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &ps, k_tsqr_leaf<decltype(tr)::value, decltype(p)::value, decltype(b)::value>, threads, var_smem(v, n));
         return ps < 1 ? 1 : ps;
     });
     int64_t maxc = (int64_t)per_sm * h->sm_count;
@@ -359,11 +546,11 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
     const int n = h->M + 1;
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
-    return dispatch(v, [&](auto tr, auto p) {
+    return dispatch(v, [&](auto tr, auto p, auto b) {
         for (int64_t stride = 1; stride < slabs; stride *= 2) {
             int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
-            k_tsqr_merge<decltype(tr)::value, decltype(p)::value>
-                <<<(unsigned)pairs, threads, 0, h->stream>>>(h->Rws, slabs, stride, n);
+            k_tsqr_merge<decltype(tr)::value, decltype(p)::value, decltype(b)::value>
+                <<<(unsigned)pairs, threads, var_smem(v, n), h->stream>>>(h->Rws, slabs, stride, n);
             h->launches++;
         }
         return cudaGetLastError();
@@ -381,9 +568,9 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
     int64_t rows = (N + slabs - 1) / slabs;
     rows = (rows + rows_tile - 1) / rows_tile * rows_tile;
     const int threads = var_threads(v, n);
-    e = dispatch(v, [&](auto tr, auto p) {
-        k_tsqr_leaf<decltype(tr)::value, decltype(p)::value>
-            <<<(unsigned)slabs, threads, 0, h->stream>>>(H, ldh, Y, N, h->M, h->Rws, rows, h->flag);
+    e = dispatch(v, [&](auto tr, auto p, auto b) {
+        k_tsqr_leaf<decltype(tr)::value, decltype(p)::value, decltype(b)::value>
+            <<<(unsigned)slabs, threads, var_smem(v, n), h->stream>>>(H, ldh, Y, N, h->M, h->Rws, rows, h->flag);
         h->launches++;
         return cudaGetLastError();
     });
@@ -420,8 +607,9 @@ cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta) {
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
     double* Rorig = h->Rws + (size_t)(h->Rws_slabs - 1) * n * n;
-    return dispatch(v, [&](auto tr, auto p) {
-        k_tsqr_solve<decltype(tr)::value, decltype(p)::value><<<1, threads, n * sizeof(double), h->stream>>>(
+    const size_t smem = ((n + 1) & ~1) * sizeof(double) + var_smem(v, n);
+    return dispatch(v, [&](auto tr, auto p, auto b) {
+        k_tsqr_solve<decltype(tr)::value, decltype(p)::value, decltype(b)::value><<<1, threads, smem, h->stream>>>(
             h->Rws, Rorig, h->M, (long long)n_total, h->flag, beta, h->sdev);
         h->launches++;
         return cudaGetLastError();
