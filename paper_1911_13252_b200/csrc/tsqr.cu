@@ -25,6 +25,7 @@
 // tolerance); H and Y are read as fp32 and widened exactly.
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -45,6 +46,9 @@ struct Fold {
 // cost hundreds of cycles of dependent latency).  Outside a safe exponent
 // range the IEEE forms are used.
 __device__ __forceinline__ double rcp_fast(double d) {
+#ifdef ELM_TSQR_IEEE
+    return 1.0 / d;
+#endif
     const double ad = fabs(d);
     if (!(ad > 1e-250 && ad < 1e250)) return 1.0 / d;
     double r;
@@ -55,6 +59,9 @@ __device__ __forceinline__ double rcp_fast(double d) {
     return fma(r, e, r);
 }
 __device__ __forceinline__ double sqrt_fast(double t) {
+#ifdef ELM_TSQR_IEEE
+    return sqrt(t);
+#endif
     if (!(t > 1e-250 && t < 1e250)) return sqrt(t);
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(t));
@@ -89,6 +96,14 @@ __device__ __forceinline__ void make_reflector(const double (&a)[TR], double x0,
     }
     const double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * sqrt_fast(fma(x0, x0, s2));
     const double u0 = x0 - beta;
+    // A reflector of a column whose norm is at rounding-noise-of-noise level
+    // (trailing rows of rank-deficient partial R factors) would overflow
+    // 1/(beta u0); such a column is treated as already reduced (H = I), as
+    // LAPACK's dlarfg guards with safmin.
+    if (!(fabs(beta * u0) > 1e-280)) {
+        if (half == 0) coef[0] = 0.0;
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < TR; ++i) v[half * TR + i] = a[i];
     if (half == 0) {
@@ -202,9 +217,11 @@ __device__ void fold_tile_blk(double (&a)[TR], int n, int k0, double* __restrict
                     if (s2 != 0.0) {
                         const double x0 = Rp[r * n + kk];
                         const double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * sqrt_fast(fma(x0, x0, s2));
-                        u0 = x0 - beta;
-                        g = rcp_fast(beta * u0);
-                        if (half == 0) Rp[r * n + kk] = beta;
+                        if (fabs(beta * (x0 - beta)) > 1e-280) {   // see make_reflector
+                            u0 = x0 - beta;
+                            g = rcp_fast(beta * u0);
+                            if (half == 0) Rp[r * n + kk] = beta;
+                        }
                     }
 #pragma unroll
                     for (int i = 0; i < TR; ++i) Yb[r * ROWS + half * TR + i] = a[i];
@@ -489,9 +506,19 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
 
 // Variants: n <= 288: 2 threads x 24 rows per column (48-row tiles, <= 576
 // threads); n <= 512: 2 x 12 (24-row tiles, <= 1024 threads); else 1 x 12.
-enum class Var { B2T24, P2T12, P1T12 };
-static Var pick_var(int n) { return n <= 288 ? Var::B2T24 : (n <= 512 ? Var::P2T12 : Var::P1T12); }
-static int var_rows(Var v) { return v == Var::B2T24 ? 48 : (v == Var::P2T12 ? 24 : 12); }
+enum class Var { B2T24, P2T24, P2T12, P1T12 };
+static Var pick_var(int n) {
+    // ELMRNN_TSQR_VAR=0/1/2 forces a variant (testing aid; must fit the thread limit)
+    if (const char* e = std::getenv("ELMRNN_TSQR_VAR")) {
+        const int v = std::atoi(e);
+        if (v == 0 && n <= 288) return Var::B2T24;
+        if (v == 1 && n <= 512) return Var::P2T12;
+        if (v == 2) return Var::P1T12;
+        if (v == 3 && n <= 288) return Var::P2T24;
+    }
+    return n <= 288 ? Var::B2T24 : (n <= 512 ? Var::P2T12 : Var::P1T12);
+}
+static int var_rows(Var v) { return (v == Var::B2T24 || v == Var::P2T24) ? 48 : (v == Var::P2T12 ? 24 : 12); }
 static int var_p(Var v) { return v == Var::P1T12 ? 1 : 2; }
 static bool var_blk(Var v) { return v == Var::B2T24; }
 static size_t var_smem(Var v, int n) { return var_blk(v) ? blk_smem_doubles(n, 24) * sizeof(double) : 0; }
@@ -502,6 +529,8 @@ static auto dispatch(Var v, F&& f) {
     switch (v) {
     case Var::B2T24:
         return f(std::integral_constant<int, 24>{}, std::integral_constant<int, 2>{}, std::true_type{});
+    case Var::P2T24:
+        return f(std::integral_constant<int, 24>{}, std::integral_constant<int, 2>{}, std::false_type{});
     case Var::P2T12:
         return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 2>{}, std::false_type{});
     default: return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 1>{}, std::false_type{});
@@ -519,7 +548,9 @@ int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
         return ps < 1 ? 1 : ps;
     });
     int64_t maxc = (int64_t)per_sm * h->sm_count;
-    int64_t byrows = (N + var_rows(v) - 1) / var_rows(v);
+    // at least n rows per leaf: a leaf R with fewer rows is rank deficient
+    // and its noise rows only cost merges (and risk underflow cascades)
+    int64_t byrows = N / n;
     int64_t g = byrows < maxc ? byrows : maxc;
     return g < 1 ? 1 : g;
 }
@@ -546,8 +577,10 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
     const int n = h->M + 1;
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
+    const char* lv = std::getenv("ELMRNN_TSQR_LEVELS");   // testing aid: stop the tree early
+    const int64_t max_stride = lv ? ((int64_t)1 << std::atoi(lv)) : slabs;
     return dispatch(v, [&](auto tr, auto p, auto b) {
-        for (int64_t stride = 1; stride < slabs; stride *= 2) {
+        for (int64_t stride = 1; stride < slabs && stride < max_stride; stride *= 2) {
             int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
             k_tsqr_merge<decltype(tr)::value, decltype(p)::value, decltype(b)::value>
                 <<<(unsigned)pairs, threads, var_smem(v, n), h->stream>>>(h->Rws, slabs, stride, n);

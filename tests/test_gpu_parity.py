@@ -108,20 +108,21 @@ def test_H_parity(arch, N, S, M, Q, o, yfb):
 
 
 # tcgen05 LSTM builder (3-pass fp16 hi/lo split): ragged tiles, Q = 1, S padded 3 -> 4
-TC_CASES = [(256, 333, 50, 1), (256, 129, 1, 1), (128, 1000, 10, 3), (128, 257, 30, 4), (256, 2100, 20, 2),
-            (128, 64, 7, 1)]
+TC_CASES = [("lstm", 256, 333, 50, 1), ("lstm", 256, 129, 1, 1), ("lstm", 128, 1000, 10, 3),
+            ("lstm", 128, 257, 30, 4), ("lstm", 256, 2100, 20, 2), ("lstm", 128, 64, 7, 1),
+            ("gru", 128, 333, 30, 4), ("gru", 128, 129, 1, 1), ("gru", 128, 1000, 10, 2), ("gru", 128, 300, 50, 3)]
 
 
-@pytest.mark.parametrize("M,N,Q,S", TC_CASES)
-def test_tc_lstm_parity(M, N, Q, S):
+@pytest.mark.parametrize("arch,M,N,Q,S", TC_CASES)
+def test_tc_parity(arch, M, N, Q, S):
     X, Y, _ = inputs(N, Q, S, seed=M + Q)
-    e, Hg = gpu_H("lstm", S, M, Q, 4, X, force_path=2)
+    e, Hg = gpu_H(arch, S, M, Q, 4, X, force_path=2)
     assert e.path == 2
-    net = orc.Net("lstm", S=S, M=M, Q=Q)
+    net = orc.Net(arch, S=S, M=M, Q=Q)
     Ho = orc.build_H(net, orc.gen_weights(net, 4), X, threads=8)
     err = np.abs(Hg - Ho).max()
     assert err <= H_TOL, f"max |dH| = {err:.3e}"
-    _, Hf = gpu_H("lstm", S, M, Q, 4, X, force_path=1)
+    _, Hf = gpu_H(arch, S, M, Q, 4, X, force_path=1)
     assert np.abs(Hf - Ho).max() <= H_TOL
 
 

@@ -1,2 +1,4 @@
-timeout 300 python tools/qr_check.py 2>&1 | tail -6
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -k "solve or virtual or ridge or predict or full_config" 2>&1 | grep -E "^E  |passed|failed" | head -30
+TAG=fixed timeout 300 python tools/qr_debug2.py
+timeout 600 python tools/qr_variants.py 2>&1 | tail -12
+timeout 300 python tools/tc_check.py 2>&1 | tail -12
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -4
