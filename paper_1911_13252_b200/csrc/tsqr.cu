@@ -25,7 +25,9 @@
 // tolerance); H and Y are read as fp32 and widened exactly.
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 #include <type_traits>
 
 #include "common.cuh"
@@ -113,14 +115,30 @@ __device__ __forceinline__ void make_reflector(const double (&a)[TR], double x0,
     }
 }
 
+// Column owned by this thread (adjacent lanes share a column when P = 2).
+// A reversed mapping (look-ahead column in the highest warp) was measured
+// slower (2200 vs 2055 cycles per column), so columns map in order.
+template <int P, bool BLK>
+__device__ __forceinline__ int col_of(int n) {
+    return (int)(threadIdx.x / P);
+}
+
+// Optional event trace of CTA 0 (testing aid, ELMRNN_TRACE_QR): per column,
+// clock at loop top (thread 0), after the update of thread k+1, after its
+// reflector, and after the barrier.
+__device__ unsigned long long* g_qr_trace = nullptr;
+__device__ __forceinline__ void qr_ev(int slot, int k) {
+    if (g_qr_trace && blockIdx.x == 0 && k < 4096) g_qr_trace[k * 4 + slot] = clock64();
+}
+
 // Fold the register tile (thread (j, half) holds rows half*TR.. of column j)
 // into R (n x n, full storage), columns k0..n-1.  vbuf: 2*ROWS doubles of
 // shared memory (u tails), coefs: 2 x (g, u0).
 template <int TR, int P>
 __device__ void fold_tile(double (&a)[TR], int n, int k0, double* __restrict__ R, double* vbuf, double* coefs) {
     constexpr int ROWS = TR * P;
-    const int j = threadIdx.x / P, half = threadIdx.x % P;
-    const bool own = j < n;
+    const int j = col_of<P, false>(n), half = threadIdx.x % P;
+    const bool own = j >= 0 && j < n;
     // R[k][j] for the next three rows are prefetched into registers: the
     // reflector of column k+1 needs R[k+1][k+1] right after its own update,
     // so its L2 latency must be hidden two columns ahead.
@@ -135,6 +153,7 @@ __device__ void fold_tile(double (&a)[TR], int n, int k0, double* __restrict__ R
     }
     __syncthreads();
     for (int k = k0; k < n; ++k) {
+        if (threadIdx.x == 0) qr_ev(0, k);
         const double rkj = rq0;
         rq0 = rq1;
         rq1 = rq2;
@@ -165,11 +184,14 @@ __device__ void fold_tile(double (&a)[TR], int n, int k0, double* __restrict__ R
             }
         }
         const bool nxt = j == k + 1 && k + 1 < n;
+        if (nxt && half == 0) qr_ev(1, k);
         const unsigned mr = __ballot_sync(0xffffffffu, nxt);
         if (nxt)
             make_reflector<TR, P>(a, rq0, vbuf + ((k + 1) & 1) * ROWS, coefs + 2 * ((k + 1) & 1),
                                   R + (size_t)(k + 1) * n + (k + 1), half, mr);
+        if (nxt && half == 0) qr_ev(2, k);
         __syncthreads();
+        if (threadIdx.x == 0) qr_ev(3, k);
     }
 }
 
@@ -325,9 +347,9 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
     __shared__ __align__(16) double vbuf[2 * ROWS];
     __shared__ double coefs[4];
     extern __shared__ __align__(16) double dsm[];
-    const int n = M + 1, j = threadIdx.x / P, half = threadIdx.x % P;
+    const int n = M + 1, j = col_of<P, BLK>(n), half = threadIdx.x % P;
     double* R = Rws + (size_t)blockIdx.x * n * n;
-    if (j < n)
+    if (j >= 0 && j < n)
         for (int k = half; k < n; k += P) R[(size_t)k * n + j] = 0.0;   // column j is private to its threads
     const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
     const int64_t r1 = min(N, r0 + rows_per_cta);
@@ -338,7 +360,7 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
         for (int i = 0; i < TR; ++i) {
             const int64_t row = base + half * TR + i;
             float v = 0.0f;
-            if (row < r1 && j < n) v = (j < M) ? __ldg(H + row * ldh + j) : __ldg(Y + row);
+            if (row < r1 && j >= 0 && j < n) v = (j < M) ? __ldg(H + row * ldh + j) : __ldg(Y + row);
             bad |= !isfinite(v);
             a[i] = (double)v;
         }
@@ -358,13 +380,13 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
     if (partner >= slabs) return;
     double* Ra = Rws + (size_t)c * n * n;
     const double* Rb = Rws + (size_t)partner * n * n;
-    const int j = threadIdx.x / P, half = threadIdx.x % P;
+    const int j = col_of<P, BLK>(n), half = threadIdx.x % P;
     for (int s = 0; s * ROWS < n; ++s) {
         double a[TR];
 #pragma unroll
         for (int i = 0; i < TR; ++i) {
             const int row = s * ROWS + half * TR + i;
-            a[i] = (row < n && j < n && j >= row) ? Rb[(size_t)row * n + j] : 0.0;
+            a[i] = (row < n && j >= 0 && j < n && j >= row) ? Rb[(size_t)row * n + j] : 0.0;
         }
         fold<TR, P, BLK>(a, n, s * ROWS, Ra, vbuf, coefs, dsm);
     }
@@ -434,8 +456,8 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
     __shared__ double red[32];
     __shared__ double bk;
     extern __shared__ __align__(16) double zs[];   // [n] signs / rhs / beta, then the blocked-fold buffers
-    const int n = M + 1, j = threadIdx.x / P, half = threadIdx.x % P;
-    const bool own = j < n && half == 0;
+    const int n = M + 1, j = col_of<P, BLK>(n), half = threadIdx.x % P;
+    const bool own = j >= 0 && j < n && half == 0;
     // sign normalisation: flip row k when R_kk < 0 (signs read into smem first)
     if (own) zs[j] = R[(size_t)j * n + j] < 0.0 ? -1.0 : 1.0;
     __syncthreads();
@@ -516,7 +538,7 @@ static Var pick_var(int n) {
         if (v == 2) return Var::P1T12;
         if (v == 3 && n <= 288) return Var::P2T24;
     }
-    return n <= 288 ? Var::B2T24 : (n <= 512 ? Var::P2T12 : Var::P1T12);
+    return n <= 288 ? Var::P2T24 : (n <= 512 ? Var::P2T12 : Var::P1T12);
 }
 static int var_rows(Var v) { return (v == Var::B2T24 || v == Var::P2T24) ? 48 : (v == Var::P2T12 ? 24 : 12); }
 static int var_p(Var v) { return v == Var::P1T12 ? 1 : 2; }
@@ -590,7 +612,31 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
     });
 }
 
+static unsigned long long* qr_trace_setup() {
+    if (!std::getenv("ELMRNN_TRACE_QR")) return nullptr;
+    unsigned long long* buf = nullptr;
+    cudaMalloc(&buf, sizeof(unsigned long long) * 4 * 4096);
+    cudaMemset(buf, 0, sizeof(unsigned long long) * 4 * 4096);
+    cudaMemcpyToSymbol(g_qr_trace, &buf, sizeof(buf));
+    return buf;
+}
+static void qr_trace_dump(unsigned long long* buf) {
+    if (!buf) return;
+    std::vector<unsigned long long> hb(4 * 4096);
+    cudaDeviceSynchronize();
+    cudaMemcpy(hb.data(), buf, sizeof(unsigned long long) * hb.size(), cudaMemcpyDeviceToHost);
+    unsigned long long* null = nullptr;
+    cudaMemcpyToSymbol(g_qr_trace, &null, sizeof(null));
+    cudaFree(buf);
+    if (FILE* f = std::fopen(std::getenv("ELMRNN_TRACE_QR"), "w")) {
+        for (int k = 0; k < 4096; ++k)
+            if (hb[4 * k]) std::fprintf(f, "%d,%llu,%llu,%llu,%llu\n", k, hb[4 * k], hb[4 * k + 1], hb[4 * k + 2], hb[4 * k + 3]);
+        std::fclose(f);
+    }
+}
+
 cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t N) {
+    struct TraceGuard { unsigned long long* b = qr_trace_setup(); ~TraceGuard() { qr_trace_dump(b); } } tg;
     const int n = h->M + 1;
     const Var v = pick_var(n);
     const int64_t slabs = tsqr_leaf_slabs(h, N);

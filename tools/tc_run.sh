@@ -1,4 +1,4 @@
-TAG=fixed timeout 300 python tools/qr_debug2.py
-timeout 600 python tools/qr_variants.py 2>&1 | tail -12
-timeout 300 python tools/tc_check.py 2>&1 | tail -12
-timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -4
+TAG=rev timeout 300 python tools/qr_debug2.py
+ELMRNN_TSQR_VAR=3 ELMRNN_TRACE_QR=gpurun_out/qrtrace2.csv timeout 120 python tools/prof_qr.py 256 100000
+timeout 300 python tools/qt.py
+timeout 300 python tools/qr_check.py 2>&1 | tail -6
