@@ -96,9 +96,9 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
     uint64_t* empty = bars + kGStages;
     uint64_t* acc_full = bars + 2 * kGStages;
     uint64_t* acc_empty = acc_full + 2;
-    uint64_t* a_ready = acc_empty + 2;   // [KS]
-    uint64_t* rh_ready = a_ready + kGKS;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rh_ready + 1);
+    uint64_t* a_ready = acc_empty + 2;   // [KS]: K-slice ks of h(t-1) is in TMEM
+    uint64_t* rh_ready = a_ready + kGKS; // [KS]: K-slice ks of r o h(t-1) is in TMEM
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rh_ready + kGKS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
             ptx::mbar_init(acc_empty + i, kGEpiWarps);
         }
         for (int i = 0; i < kGKS; ++i) ptx::mbar_init(a_ready + i, kGEpiWarps);
-        ptx::mbar_init(rh_ready, kGEpiWarps);
+        for (int i = 0; i < kGKS; ++i) ptx::mbar_init(rh_ready + i, kGEpiWarps);
         ptx::fence_mbar_init();
     }
     if (warp == kGProdWarp) {
@@ -153,8 +153,8 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                         ptx::mbar_wait(a_ready + ks, (uint32_t)(s & 1));
                         ptx::tc_fence_after();
                     }
-                    if (q == 2 && ks == 0) {   // r o h(t-1) is in TMEM
-                        ptx::mbar_wait(rh_ready, (uint32_t)(s & 1));
+                    if (q == 2) {   // K-slice ks of r o h(t-1) is in TMEM
+                        ptx::mbar_wait(rh_ready + ks, (uint32_t)(s & 1));
                         ptx::tc_fence_after();
                     }
                     ptx::mbar_wait(full + st, ph);
@@ -191,27 +191,25 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
         float h[32];                                            // h of neurons 16u+i, 64+16u+i
         uint32_t ach = 0, aph = 0;
         // write h (or zero) of this thread's neurons into A_h hi/lo and publish both K-slices
-        auto publish_h = [&](bool zero) {
+        // K-slice `half` of this thread's h (or zeros) into A_h, then release it
+        auto publish_h = [&](int half, bool zero) {
+            float v[16];
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                float v[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = zero ? 0.0f : h[half * 16 + i];
-                uint32_t hi[8], lo[8];
-                split16(v, hi, lo);
-                const uint32_t col = (64 * half + 16 * u) / 2;   // two fp16 per column
-                tmem_st8u(lb + kAH + col, hi);
-                tmem_st8u(lb + kAH + 64 + col, lo);
-            }
+            for (int i = 0; i < 16; ++i) v[i] = zero ? 0.0f : h[half * 16 + i];
+            uint32_t hi[8], lo[8];
+            split16(v, hi, lo);
+            const uint32_t col = (64 * half + 16 * u) / 2;   // two fp16 per column
+            tmem_st8u(lb + kAH + col, hi);
+            tmem_st8u(lb + kAH + 64 + col, lo);
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0)
-                for (int ks = 0; ks < kGKS; ++ks) ptx::mbar_arrive(a_ready + ks);
+            if (lane == 0) ptx::mbar_arrive(a_ready + half);
         };
 #pragma unroll
         for (int i = 0; i < 32; ++i) h[i] = 0.0f;
-        publish_h(true);
+        publish_h(0, true);
+        publish_h(1, true);
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             const int64_t row = tile * kGRows + r;
             const bool valid = row < p.N;
@@ -259,11 +257,11 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                     const uint32_t col = (64 * c + 16 * u) / 2;
                     tmem_st8u(lb + kARH + col, hi);
                     tmem_st8u(lb + kARH + 64 + col, lo);
+                    ptx::tmem_wait_st();   // K-slice c of r o h is complete: phase 2 may start on it
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(rh_ready + c);
                 }
-                ptx::tmem_wait_st();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(rh_ready);
                 // ---- phase 2: n = tanh(.), h <- (1 - z) h + z n
                 ptx::mbar_wait(acc_full + ach, aph);
                 ptx::tc_fence_after();
@@ -276,7 +274,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                 if (lane == 0) ptx::mbar_arrive(acc_empty + ach);
                 if (++ach == 2) { ach = 0; aph ^= 1; }
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {
+                for (int c = 0; c < 2; ++c) {   // c = K-slice of the next step's A
 #pragma unroll
                     for (int i = 0; i < 16; i += 2) {
                         float dn[2];
@@ -297,10 +295,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                         h0 = fmaf(z0, n0 - h0, h0);   // (1 - z) h + z n
                         h1 = fmaf(z1, n1 - h1, h1);
                     }
-                }
-                if (t == p.Q && valid) {
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
+                    if (t == p.Q && valid) {
                         float* d1 = p.H + row * p.ldh + 64 * c + 16 * u;
                         if ((p.ldh & 3) == 0) {
                             float4* dst = reinterpret_cast<float4*>(d1);
@@ -313,8 +308,8 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                             for (int i = 0; i < 16; ++i) d1[i] = h[c * 16 + i];
                         }
                     }
+                    publish_h(c, t == p.Q);   // next step's A slice c (or h(0) = 0 of the next tile)
                 }
-                publish_h(t == p.Q);   // next step's A (or h(0) = 0 of the next tile)
             }
         }
     }

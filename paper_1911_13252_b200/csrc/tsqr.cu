@@ -40,7 +40,7 @@ struct Fold {
     static constexpr int ROWS = TR * P;
     // register budget (16K registers per SM sub-partition): 2*TR registers of
     // tile per thread plus ~40; 576 threads -> 96 registers, 1024 -> 64
-    static constexpr int MAX_THREADS = (P == 2 && TR == 24) ? 576 : 1024;
+    static constexpr int MAX_THREADS = (P == 2 && (TR == 24 || TR == 16)) ? 576 : 1024;
 };
 
 // Fast fp64 reciprocal / square root: hardware approximation + Newton steps
@@ -195,6 +195,83 @@ __device__ void fold_tile(double (&a)[TR], int n, int k0, double* __restrict__ R
     }
 }
 
+// ---- lagged fold: critical path isolated from the trailing updates --------------------
+// Round k: phase A -- the owner of column k alone applies the pending reflector
+// k-1 to its column and builds reflector k (the FP64 pipe is otherwise idle,
+// so this latency chain runs uncontended); barrier; phase B -- every column
+// j > k applies reflector k-1; barrier.  In the look-ahead fold_tile the
+// critical chain shares the FP64 pipe with all trailing updates and was
+// measured ~3.5x slower than its uncontended length (profiles/).
+template <int TR, int P>
+__device__ __forceinline__ void apply_reflector(double (&a)[TR], double& rkj, const double* vbase, double g, double u0,
+                                                int half, unsigned mask) {
+    const double2* v = reinterpret_cast<const double2*>(vbase + half * TR);
+    double w0 = (half == 0) ? u0 * rkj : 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < TR; i += 4) {
+        const double2 va = v[i / 2], vb = v[i / 2 + 1];
+        w0 = fma(va.x, a[i], w0);
+        w1 = fma(va.y, a[i + 1], w1);
+        w2 = fma(vb.x, a[i + 2], w2);
+        w3 = fma(vb.y, a[i + 3], w3);
+    }
+    double w = (w0 + w1) + (w2 + w3);
+    if (P == 2) w += __shfl_xor_sync(mask, w, 1);
+    const double f = g * w;
+    rkj = fma(f, u0, rkj);
+#pragma unroll
+    for (int i = 0; i < TR; i += 2) {
+        const double2 vv = v[i / 2];
+        a[i] = fma(f, vv.x, a[i]);
+        a[i + 1] = fma(f, vv.y, a[i + 1]);
+    }
+}
+
+template <int TR, int P>
+__device__ void fold_tile_lag(double (&a)[TR], int n, int k0, double* __restrict__ R, double* vbuf, double* coefs) {
+    constexpr int ROWS = TR * P;
+    const int j = threadIdx.x / P, half = threadIdx.x % P;
+    const bool own = j < n;
+    const double* Rj = R + j;
+    auto ld = [&](int row) -> double { return (own && row < n && j >= row) ? Rj[(size_t)row * n] : 0.0; };
+    // the R entry of the pending row (k-1) for this column, prefetched
+    double rcur = ld(k0), rnext = ld(k0 + 1);
+    {
+        const unsigned m = __ballot_sync(0xffffffffu, j == k0);
+        if (j == k0)
+            make_reflector<TR, P>(a, rcur, vbuf + (k0 & 1) * ROWS, coefs + 2 * (k0 & 1), R + (size_t)k0 * n + k0,
+                                  half, m);
+    }
+    __syncthreads();
+    for (int k = k0 + 1; k <= n; ++k) {
+        // rcur = R[k-1][j] (row of the pending reflector), rnext = R[k][j]
+        const double* vb = vbuf + ((k - 1) & 1) * ROWS;
+        const double g = coefs[2 * ((k - 1) & 1)], u0 = coefs[2 * ((k - 1) & 1) + 1];
+        // ---- phase A: column k alone
+        const bool crit = (j == k) && k < n;
+        const unsigned mc = __ballot_sync(0xffffffffu, crit);
+        if (crit) {
+            if (g != 0.0) {
+                apply_reflector<TR, P>(a, rcur, vb, g, u0, half, mc);
+                if (half == 0) R[(size_t)(k - 1) * n + j] = rcur;
+            }
+            make_reflector<TR, P>(a, rnext, vbuf + (k & 1) * ROWS, coefs + 2 * (k & 1), R + (size_t)k * n + k, half,
+                                  mc);
+        }
+        __syncthreads();
+        // ---- phase B: columns j > k apply reflector k-1
+        const bool upd = own && j > k && g != 0.0;
+        const unsigned mu = __ballot_sync(0xffffffffu, upd);
+        if (upd) {
+            apply_reflector<TR, P>(a, rcur, vb, g, u0, half, mu);
+            if (half == 0) R[(size_t)(k - 1) * n + j] = rcur;
+        }
+        rcur = rnext;
+        rnext = ld(k + 1);
+        __syncthreads();
+    }
+}
+
 // ---- blocked fold (panels of kNB columns) -------------------------------------------
 // Same reflectors as fold_tile, applied panel by panel: the warp owning the
 // kNB panel columns factors the panel warp-synchronously (shuffles and
@@ -331,7 +408,9 @@ __device__ void fold_tile_blk(double (&a)[TR], int n, int k0, double* __restrict
 template <int TR, int P, bool BLK>
 __device__ __forceinline__ void fold(double (&a)[TR], int n, int k0, double* R, double* vbuf, double* coefs,
                                      double* dsm) {
-    if constexpr (BLK) {
+    if constexpr (!BLK && TR == 16) {   // TR = 16 selects the lagged fold (variant L2T16)
+        fold_tile_lag<TR, P>(a, n, k0, R, vbuf, coefs);
+    } else if constexpr (BLK) {
         fold_tile_blk<TR>(a, n, k0, R, dsm, dsm + kNB * n, dsm + kNB * n + kNB * 2 * TR);
     } else {
         fold_tile<TR, P>(a, n, k0, R, vbuf, coefs);
@@ -528,7 +607,7 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
 
 // Variants: n <= 288: 2 threads x 24 rows per column (48-row tiles, <= 576
 // threads); n <= 512: 2 x 12 (24-row tiles, <= 1024 threads); else 1 x 12.
-enum class Var { B2T24, P2T24, P2T12, P1T12 };
+enum class Var { B2T24, P2T24, P2T12, P1T12, L2T16 };
 static Var pick_var(int n) {
     // ELMRNN_TSQR_VAR=0/1/2 forces a variant (testing aid; must fit the thread limit)
     if (const char* e = std::getenv("ELMRNN_TSQR_VAR")) {
@@ -537,10 +616,13 @@ static Var pick_var(int n) {
         if (v == 1 && n <= 512) return Var::P2T12;
         if (v == 2) return Var::P1T12;
         if (v == 3 && n <= 288) return Var::P2T24;
+        if (v == 4 && n <= 288) return Var::L2T16;
     }
     return n <= 288 ? Var::P2T24 : (n <= 512 ? Var::P2T12 : Var::P1T12);
 }
-static int var_rows(Var v) { return (v == Var::B2T24 || v == Var::P2T24) ? 48 : (v == Var::P2T12 ? 24 : 12); }
+static int var_rows(Var v) {
+    return (v == Var::B2T24 || v == Var::P2T24) ? 48 : (v == Var::L2T16 ? 32 : (v == Var::P2T12 ? 24 : 12));
+}
 static int var_p(Var v) { return v == Var::P1T12 ? 1 : 2; }
 static bool var_blk(Var v) { return v == Var::B2T24; }
 static size_t var_smem(Var v, int n) { return var_blk(v) ? blk_smem_doubles(n, 24) * sizeof(double) : 0; }
@@ -555,6 +637,8 @@ static auto dispatch(Var v, F&& f) {
         return f(std::integral_constant<int, 24>{}, std::integral_constant<int, 2>{}, std::false_type{});
     case Var::P2T12:
         return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 2>{}, std::false_type{});
+    case Var::L2T16:
+        return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 2>{}, std::false_type{});
     default: return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 1>{}, std::false_type{});
     }
 }
