@@ -81,6 +81,9 @@ cudaError_t launch_dense_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, f
 bool gru_tc_supported(const elmrnn* h);
 cudaError_t gru_tc_prepare(elmrnn* h);
 cudaError_t launch_gru_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
+bool fc_tc_supported(const elmrnn* h);
+cudaError_t fc_tc_prepare(elmrnn* h);
+cudaError_t launch_fc_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
 
 // ---- TSQR (tsqr.cu) ------------------------------------------------------------
 // Fold [H | Y] rows into per-CTA R slabs and reduce them to slab 0 (full storage).

@@ -440,6 +440,7 @@ static int tc_padded_s(int S) { return S <= 1 ? 1 : (S <= 2 ? 2 : 4); }
 
 bool tc_supported(const elmrnn* h) {
     if (h->arch == kArchGRU) return gru_tc_supported(h);
+    if (h->arch == kArchFC) return fc_tc_supported(h);
     if (h->arch != kArchLSTM) return false;
     if (h->M != 128 && h->M != 256) return false;
     if (h->S > 4) return false;
@@ -448,6 +449,7 @@ bool tc_supported(const elmrnn* h) {
 
 cudaError_t tc_prepare(elmrnn* h) {
     if (h->arch == kArchGRU) return gru_tc_prepare(h);
+    if (h->arch == kArchFC) return fc_tc_prepare(h);
     const int M = h->M;
     size_t bytes = (size_t)(M / 32) * (M / 64) * kTcStageBytes;
     cudaError_t e;
@@ -490,6 +492,7 @@ static cudaError_t launch_m(elmrnn* h, const float* X, int64_t ldx, int64_t N, f
 
 cudaError_t launch_dense_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh) {
     if (h->arch == kArchGRU) return launch_gru_tc(h, X, ldx, N, H, ldh);
+    if (h->arch == kArchFC) return launch_fc_tc(h, X, ldx, N, H, ldh);
     if (h->M == 256) return launch_m<256>(h, X, ldx, N, H, ldh);
     if (h->M == 128) return launch_m<128>(h, X, ldx, N, H, ldh);
     return cudaErrorNotSupported;

@@ -110,7 +110,8 @@ def test_H_parity(arch, N, S, M, Q, o, yfb):
 # tcgen05 LSTM builder (3-pass fp16 hi/lo split): ragged tiles, Q = 1, S padded 3 -> 4
 TC_CASES = [("lstm", 256, 333, 50, 1), ("lstm", 256, 129, 1, 1), ("lstm", 128, 1000, 10, 3),
             ("lstm", 128, 257, 30, 4), ("lstm", 256, 2100, 20, 2), ("lstm", 128, 64, 7, 1),
-            ("gru", 128, 333, 30, 4), ("gru", 128, 129, 1, 1), ("gru", 128, 1000, 10, 2), ("gru", 128, 300, 50, 3)]
+            ("gru", 128, 333, 30, 4), ("gru", 128, 129, 1, 1), ("gru", 128, 1000, 10, 2), ("gru", 128, 300, 50, 3),
+            ("fc", 128, 333, 30, 4), ("fc", 128, 129, 1, 1), ("fc", 128, 1000, 10, 2), ("fc", 128, 300, 2, 3)]
 
 
 @pytest.mark.parametrize("arch,M,N,Q,S", TC_CASES)
@@ -124,6 +125,19 @@ def test_tc_parity(arch, M, N, Q, S):
     assert err <= H_TOL, f"max |dH| = {err:.3e}"
     _, Hf = gpu_H(arch, S, M, Q, 4, X, force_path=1)
     assert np.abs(Hf - Ho).max() <= H_TOL
+
+
+@pytest.mark.parametrize("L,act,N,Q", [(3, 0, 700, 12), (1, 1, 300, 9), (5, 1, 520, 40), (40, 0, 260, 20)])
+def test_fc_tc_lag_ring(L, act, N, Q):
+    """FC tensor path with a lag window shorter than Q (ring wrap-around,
+    S2.2.4 prose reading R9), longer than Q, and tanh activations."""
+    X, _, _ = inputs(N, Q, 2, seed=L + Q)
+    e, Hg = gpu_H("fc", 2, 128, Q, 6, X, force_path=2, fc_lags=L, act=act)
+    assert e.path == 2
+    net = oracle_net("fc", 2, 128, Q, fc_lags=L, act=act)
+    Ho = orc.build_H(net, orc.gen_weights(net, 6), X, threads=8)
+    err = np.abs(Hg - Ho).max()
+    assert err <= H_TOL, f"max |dH| = {err:.3e}"
 
 
 def test_H_written_once_and_ld_respected():
