@@ -58,6 +58,7 @@ struct TcParams {
     int64_t ldh;
     const uint8_t* Uimg;   // [NCH][KS][hi|lo][16 KB] pre-swizzled images
     int S, Q;
+    int two_pass;          // 1: U on the fp16 grid (weight_grid = 1), U_lo = 0 -> hi.hi + lo.hi only
     int64_t ntiles;
     float k_sig, k_tanh;   // -log2(e) 2^-sigma, 2 log2(e) 2^-sigma
     unsigned long long* trace;   // optional event trace of CTA 0 (ELMRNN_TRACE), else null
@@ -157,13 +158,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
         // The whole warp runs the loop (warp-uniform state lives in uniform
         // registers); one elected lane issues.
         uint32_t st = 0, ph = 0;
+        const uint32_t bytes = p.two_pass ? kTcSliceBytes : kTcStageBytes;   // hi only when U_lo = 0
         for (int64_t s = 0; s < steps_total; ++s) {
             for (int c = 0; c < C::NCH * C::KS; ++c) {
                 ptx::mbar_wait(empty + st, ph ^ 1);
                 if (ptx::elect_one()) {
-                    ptx::mbar_arrive_expect_tx(full + st, kTcStageBytes);
-                    ptx::bulk_g2s(stages + st * kTcStageBytes, p.Uimg + (size_t)c * kTcStageBytes, kTcStageBytes,
-                                  full + st);
+                    ptx::mbar_arrive_expect_tx(full + st, bytes);
+                    ptx::bulk_g2s(stages + st * kTcStageBytes, p.Uimg + (size_t)c * kTcStageBytes, bytes, full + st);
                 }
                 __syncwarp();
                 if (++st == kTcStages) { st = 0; ph ^= 1; }
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
         constexpr uint32_t idesc = ptx::idesc_f16(128, 128);
         const uint32_t a_hi = tmem + C::A_HI, a_lo = tmem + C::A_LO;   // A operand in TMEM
         const uint64_t dbase = ptx::desc_sw128_kmajor(ptx::smem_u32(stages));
+        const bool two = p.two_pass != 0;
         uint32_t st = 0, ph = 0, ach = 0, aph = 0;
         for (int64_t s = 0; s < steps_total; ++s) {
             if (lane == 0) trace_ev(p, trace_cnt, 1, (int)s, 0);
@@ -196,12 +198,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                     const uint32_t tah = a_hi + ks * 32, tal = a_lo + ks * 32;
                     if (ptx::elect_one()) {
                         ptx::mma_f16_ts(d, tah, dbh, idesc, ks != 0);
-                        ptx::mma_f16_ts(d, tah, dbl, idesc, 1);
+                        if (!two) ptx::mma_f16_ts(d, tah, dbl, idesc, 1);
                         ptx::mma_f16_ts(d, tal, dbh, idesc, 1);
 #pragma unroll
                         for (int kk = 1; kk < 4; ++kk) {
                             ptx::mma_f16_ts(d, tah + kk * 8, dbh + 2 * kk, idesc, 1);
-                            ptx::mma_f16_ts(d, tah + kk * 8, dbl + 2 * kk, idesc, 1);
+                            if (!two) ptx::mma_f16_ts(d, tah + kk * 8, dbl + 2 * kk, idesc, 1);
                             ptx::mma_f16_ts(d, tal + kk * 8, dbh + 2 * kk, idesc, 1);
                         }
                         ptx::mma_commit(empty + st);                  // frees the U stage
@@ -396,6 +398,7 @@ cudaError_t launch_lstm_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, fl
     p.X = X; p.ldx = ldx; p.N = N; p.H = H; p.ldh = ldh;
     p.Uimg = static_cast<const uint8_t*>(h->tc_ops);
     p.S = h->S; p.Q = h->Q;
+    p.two_pass = h->weight_grid == 1;
     p.ntiles = (N + kTcRows - 1) / kTcRows;
     p.k_sig = -1.4426950408889634f * h->tc_inv_scale;
     p.k_tanh = 2.8853900817779268f * h->tc_inv_scale;

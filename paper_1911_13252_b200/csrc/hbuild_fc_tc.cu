@@ -55,6 +55,7 @@ struct FcParams {
     const uint8_t* Aimg;   // [Leff][KS][hi|lo][16 KB]: B images of A_k (row j, K index m)
     uint8_t* hist;         // [grid][NS][KS][hi|lo][16 KB]: A images of h(tau)
     int S, Q, L, NS, act;
+    int two_pass;          // 1: A_k on the fp16 grid (weight_grid = 1), A_lo = 0 -> hi.hi + lo.hi only
     int64_t ntiles;
     float k_act;           // sigmoid: -log2(e) 2^-sigma; tanh: 2 log2(e) 2^-sigma
     float wb[kFWbMax];     // per neuron j: [b, W_0..W_{S-1}] x 2^sigma
@@ -128,10 +129,10 @@ __global__ void __launch_bounds__(kFThreads, 1) k_fc_tc(const __grid_constant__ 
                         ptx::mbar_wait(empty + st, ph ^ 1);
                         if (ptx::elect_one()) {
                             uint8_t* sb = stages + st * kFStageBytes;
-                            ptx::mbar_arrive_expect_tx(full + st, kFStageBytes);
+                            const uint32_t bb = p.two_pass ? kFTile : kFPair;   // A_k hi only when A_lo = 0
+                            ptx::mbar_arrive_expect_tx(full + st, kFPair + bb);
                             ptx::bulk_g2s(sb, slot + ks * kFPair, kFPair, full + st);
-                            ptx::bulk_g2s(sb + kFPair, p.Aimg + (size_t)((k - 1) * kFKS + ks) * kFPair, kFPair,
-                                          full + st);
+                            ptx::bulk_g2s(sb + kFPair, p.Aimg + (size_t)((k - 1) * kFKS + ks) * kFPair, bb, full + st);
                         }
                         __syncwarp();
                         if (++st == kFStages) { st = 0; ph ^= 1; }
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_fc_tc(const __grid_constant__ 
         // ---------------- MMA issuer: 12 SS MMAs (4 K-steps x 3 passes) per stage
         constexpr uint32_t idesc = ptx::idesc_f16(128, kFM);
         const uint64_t dbase = ptx::desc_sw128_kmajor(ptx::smem_u32(stages));
+        const bool two = p.two_pass != 0;
         uint32_t st = 0, ph = 0, ach = 0, aph = 0;
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             for (int t = 2; t <= p.Q; ++t) {
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_fc_tc(const __grid_constant__ 
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk) {
                                 ptx::mma_f16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc, (first && kk == 0) ? 0u : 1u);
-                                ptx::mma_f16_ss(d, ah + 2 * kk, bl + 2 * kk, idesc, 1u);
+                                if (!two) ptx::mma_f16_ss(d, ah + 2 * kk, bl + 2 * kk, idesc, 1u);
                                 ptx::mma_f16_ss(d, al + 2 * kk, bh + 2 * kk, idesc, 1u);
                             }
                             ptx::mma_commit(empty + st);
@@ -301,6 +303,7 @@ cudaError_t launch_fc_ss(elmrnn* h, const float* X, int64_t ldx, int64_t N, floa
     p.X = X; p.ldx = ldx; p.N = N; p.H = H; p.ldh = ldh;
     p.Aimg = static_cast<const uint8_t*>(h->tc_ops);
     p.S = h->S; p.Q = h->Q; p.L = fc_leff(h); p.NS = p.L + 1; p.act = h->act;
+    p.two_pass = h->weight_grid == 1;
     p.ntiles = (N + kFRows - 1) / kFRows;
     p.k_act = (h->act == 1 ? 2.8853900817779268f : -1.4426950408889634f) * h->tc_inv_scale;
     std::copy(h->tc_wb.begin(), h->tc_wb.end(), p.wb);

@@ -50,6 +50,7 @@ struct GruParams {
     int64_t ldh;
     const uint8_t* Uimg;   // [3 chunks][KS][hi|lo][16 KB]
     int S, Q;
+    int two_pass;          // 1: U on the fp16 grid (weight_grid = 1), U_lo = 0 -> hi.hi + lo.hi only
     int64_t ntiles;
     float k_sig, k_tanh;   // -log2(e) 2^-sigma, 2 log2(e) 2^-sigma
     float wb[kGWbMax];     // per neuron j, gate g in (z, r, f): [b, W_0..W_{S-1}] x 2^sigma
@@ -126,13 +127,13 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
 
     if (warp == kGProdWarp) {
         uint32_t st = 0, ph = 0;
+        const uint32_t bytes = p.two_pass ? kGSliceBytes : kGStageBytes;   // hi only when U_lo = 0
         for (int64_t s = 0; s < steps_total; ++s) {
             for (int c = 0; c < kGStagesPerStep; ++c) {
                 ptx::mbar_wait(empty + st, ph ^ 1);
                 if (ptx::elect_one()) {
-                    ptx::mbar_arrive_expect_tx(full + st, kGStageBytes);
-                    ptx::bulk_g2s(stages + st * kGStageBytes, p.Uimg + (size_t)c * kGStageBytes, kGStageBytes,
-                                  full + st);
+                    ptx::mbar_arrive_expect_tx(full + st, bytes);
+                    ptx::bulk_g2s(stages + st * kGStageBytes, p.Uimg + (size_t)c * kGStageBytes, bytes, full + st);
                 }
                 __syncwarp();
                 if (++st == kGStages) { st = 0; ph ^= 1; }
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
     } else if (warp == kGMmaWarp) {
         constexpr uint32_t idesc = ptx::idesc_f16(128, 128);
         const uint64_t dbase = ptx::desc_sw128_kmajor(ptx::smem_u32(stages));
+        const bool two = p.two_pass != 0;
         uint32_t st = 0, ph = 0, ach = 0, aph = 0;
         for (int64_t s = 0; s < steps_total; ++s) {
             for (int q = 0; q < kGChunks; ++q) {
@@ -164,12 +166,12 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                     const uint32_t tah = abase + ks * 32, tal = abase + 64 + ks * 32;
                     if (ptx::elect_one()) {
                         ptx::mma_f16_ts(d, tah, dbh, idesc, ks != 0);
-                        ptx::mma_f16_ts(d, tah, dbl, idesc, 1);
+                        if (!two) ptx::mma_f16_ts(d, tah, dbl, idesc, 1);
                         ptx::mma_f16_ts(d, tal, dbh, idesc, 1);
 #pragma unroll
                         for (int kk = 1; kk < 4; ++kk) {
                             ptx::mma_f16_ts(d, tah + kk * 8, dbh + 2 * kk, idesc, 1);
-                            ptx::mma_f16_ts(d, tah + kk * 8, dbl + 2 * kk, idesc, 1);
+                            if (!two) ptx::mma_f16_ts(d, tah + kk * 8, dbl + 2 * kk, idesc, 1);
                             ptx::mma_f16_ts(d, tal + kk * 8, dbh + 2 * kk, idesc, 1);
                         }
                         ptx::mma_commit(empty + st);
@@ -351,6 +353,7 @@ cudaError_t launch_gru(elmrnn* h, const float* X, int64_t ldx, int64_t N, float*
     p.X = X; p.ldx = ldx; p.N = N; p.H = H; p.ldh = ldh;
     p.Uimg = static_cast<const uint8_t*>(h->tc_ops);
     p.S = h->S; p.Q = h->Q;
+    p.two_pass = h->weight_grid == 1;
     p.ntiles = (N + kGRows - 1) / kGRows;
     p.k_sig = -1.4426950408889634f * h->tc_inv_scale;
     p.k_tanh = 2.8853900817779268f * h->tc_inv_scale;

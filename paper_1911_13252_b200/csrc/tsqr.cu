@@ -128,7 +128,9 @@ __device__ __forceinline__ int col_of(int n) {
 // reflector, and after the barrier.
 __device__ unsigned long long* g_qr_trace = nullptr;
 __device__ __forceinline__ void qr_ev(int slot, int k) {
-    if (g_qr_trace && blockIdx.x == 0 && k < 4096) g_qr_trace[k * 4 + slot] = clock64();
+#ifdef ELM_QR_TRACE   // compiled in only for tracing builds: the pointer load sits on the critical path
+    if (g_qr_trace && blockIdx.x == 0 && k < 4096) g_qr_trace[k * 8 + slot] = clock64();
+#endif
 }
 
 // Fold the register tile (thread (j, half) holds rows half*TR.. of column j)
@@ -603,6 +605,224 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
     }
 }
 
+// ---- 2D register-tiled fold (fold2d) ------------------------------------------------------
+// Thread t = (column group cg = t / 4, row group rg = t % 4) holds TR rows
+// (rg*TR ..) of the TC tile columns TC*cg .. TC*cg+TC-1: a tile of 4*TR rows.
+// Compared with fold_tile (one column per thread) every reflector element
+// read from shared memory feeds TC columns; column dot products combine over
+// the 4 row-group lanes by butterfly shuffles.  Lane rg < TC of a group keeps
+// the prefetched R rows of column TC*cg + rg and owns its R entries.
+// TC = 3 at n = 257 gives 86 groups = 344 threads (11 warps, <= 168
+// registers per thread: 17 warps would cap it at 96).
+constexpr int kRG = 4;
+
+// Reflector of local column LC (compile-time) of this 4-lane group: x0 =
+// R[k][k] comes from the prefetch register of lane rg = LC.
+template <int TR, int TC, int LC>
+__device__ __forceinline__ void make_refl3(const double (&a)[TC][TR], double x0_own, double* v, double* coef,
+                                           double* Rkk, int rg) {
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < TR; i += 4) {
+        p0 = fma(a[LC][i], a[LC][i], p0);
+        p1 = fma(a[LC][i + 1], a[LC][i + 1], p1);
+        p2 = fma(a[LC][i + 2], a[LC][i + 2], p2);
+        p3 = fma(a[LC][i + 3], a[LC][i + 3], p3);
+    }
+    const unsigned gm = 0xFu << (threadIdx.x & 28);   // the 4 lanes of this group
+    double s2 = (p0 + p1) + (p2 + p3);
+    s2 += __shfl_xor_sync(gm, s2, 1);
+    s2 += __shfl_xor_sync(gm, s2, 2);
+    const double x0 = __shfl_sync(gm, x0_own, ((int)threadIdx.x & 28) | LC);
+    double g = 0.0, u0 = 0.0;
+    if (s2 != 0.0) {
+        const double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * sqrt_fast(fma(x0, x0, s2));
+        const double uu = x0 - beta;
+        if (fabs(beta * uu) > 1e-280) {   // see make_reflector
+            u0 = uu;
+            g = rcp_fast(beta * uu);
+            double2* vv = reinterpret_cast<double2*>(v + rg * TR);
+#pragma unroll
+            for (int i = 0; i < TR; i += 2) vv[i / 2] = make_double2(a[LC][i], a[LC][i + 1]);
+            if (rg == LC) *Rkk = beta;   // the lane that owns column k's R entries
+        }
+    }
+    if (rg == 0) {
+        coef[0] = g;
+        coef[1] = u0;
+    }
+}
+
+// Apply reflector (g, u0, v) to local column C of every group in the warp:
+// partial dot over this lane's TR rows (+ u0 R[k][col] on the R-owning lane),
+// butterfly over the 4 row-group lanes, x += f v.  Columns <= k or >= n get
+// f = 0 (no-op).  Returns f for the R update.
+template <int TR, int TC, int C>
+__device__ __forceinline__ double apply_col(double (&a)[TC][TR], const double2 (&v)[TR / 2], double g, double u0,
+                                            double rq0, int rg, bool live) {
+    double w0 = (rg == C) ? u0 * rq0 : 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < TR; i += 4) {
+        w0 = fma(v[i / 2].x, a[C][i], w0);
+        w1 = fma(v[i / 2].y, a[C][i + 1], w1);
+        w2 = fma(v[i / 2 + 1].x, a[C][i + 2], w2);
+        w3 = fma(v[i / 2 + 1].y, a[C][i + 3], w3);
+    }
+    double w = (w0 + w1) + (w2 + w3);
+    w += __shfl_xor_sync(0xffffffffu, w, 1);
+    w += __shfl_xor_sync(0xffffffffu, w, 2);
+    const double f = live ? g * w : 0.0;
+#pragma unroll
+    for (int i = 0; i < TR; i += 2) {
+        a[C][i] = fma(f, v[i / 2].x, a[C][i]);
+        a[C][i + 1] = fma(f, v[i / 2].y, a[C][i + 1]);
+    }
+    return f;
+}
+
+template <int TR, int TC, int C>
+__device__ __forceinline__ void apply_rest(double (&a)[TC][TR], const double2 (&v)[TR / 2], double g, double u0,
+                                           double rq0, int rg, int cb, int k, int n, double& fR) {
+    if constexpr (C < TC) {
+        const double f = apply_col<TR, TC, C>(a, v, g, u0, rq0, rg, cb + C > k && cb + C < n);
+        if (rg == C) fR = f;
+    }
+}
+
+// One column step k of the lean fold: LC = (k+1) % TC is the local index of
+// column k+1, so every register index is compile-time.  The warp holding
+// column k+1 first updates local column LC of all its groups, then the owner
+// group builds reflector k+1 and publishes it, then the warp updates its other
+// columns; one block barrier per column.
+template <int TR, int TC, int LC>
+__device__ __forceinline__ void fold_step(double (&a)[TC][TR], int n, int k, double* __restrict__ R, double* vbuf,
+                                          double* coefs, double& rq0, double& rq1, int rg, int grp, int cb, int cR) {
+    constexpr int ROWS = kRG * TR;
+    const double g = coefs[2 * (k & 1)], u0 = coefs[2 * (k & 1) + 1];
+    // warp-uniform skip: the warp's last column is <= k, or reflector k is the identity
+    const bool warp_live = g != 0.0 && (int)((threadIdx.x | 31) >> 2) * TC + TC - 1 > k;
+    if (warp_live) {
+        double2 v[TR / 2];
+        const double2* vs = reinterpret_cast<const double2*>(vbuf + (k & 1) * ROWS + rg * TR);
+#pragma unroll
+        for (int i = 0; i < TR / 2; ++i) v[i] = vs[i];
+        double fR = 0.0;
+        const bool crit = k + 1 < n && grp == (k + 1) / TC;
+        if (crit && rg == 0) qr_ev(1, k);
+        {
+            const double f = apply_col<TR, TC, LC>(a, v, g, u0, rq0, rg, cb + LC > k && cb + LC < n);
+            if (rg == LC) fR = f;
+        }
+        if (crit && rg == 0) qr_ev(2, k);
+        if (crit)
+            make_refl3<TR, TC, LC>(a, rq1, vbuf + ((k + 1) & 1) * ROWS, coefs + 2 * ((k + 1) & 1),
+                                   R + (size_t)(k + 1) * n + (k + 1), rg);
+        if (crit && rg == 0) qr_ev(4, k);
+        apply_rest<TR, TC, (LC + 1) % TC == LC ? TC : (LC + 1) % TC>(a, v, g, u0, rq0, rg, cb, k, n, fR);
+        apply_rest<TR, TC, (LC + 2) % TC == LC || TC < 3 ? TC : (LC + 2) % TC>(a, v, g, u0, rq0, rg, cb, k, n, fR);
+        apply_rest<TR, TC, (LC + 3) % TC == LC || TC < 4 ? TC : (LC + 3) % TC>(a, v, g, u0, rq0, rg, cb, k, n, fR);
+        if (rg < TC && cR > k && cR < n) R[(size_t)k * n + cR] = fma(fR, u0, rq0);
+        if (crit && rg == 0) qr_ev(5, k);
+    } else if (k + 1 < n && grp == (k + 1) / TC) {
+        make_refl3<TR, TC, LC>(a, rq1, vbuf + ((k + 1) & 1) * ROWS, coefs + 2 * ((k + 1) & 1),
+                               R + (size_t)(k + 1) * n + (k + 1), rg);
+    }
+}
+
+template <int TR, int TC>
+__device__ void fold2d(double (&a)[TC][TR], int n, int k0, double* __restrict__ R, double* vbuf, double* coefs) {
+    constexpr int ROWS = kRG * TR;
+    const int tid = threadIdx.x, rg = tid & 3, grp = tid >> 2, cb = TC * grp;
+    const int cR = cb + rg;   // column whose R rows this lane prefetches and owns (rg < TC)
+    const bool hasR = rg < TC && cR < n;
+    const double* Rc = R + cR;
+    auto ld = [&](int row) -> double { return (hasR && row < n && cR >= row) ? Rc[(size_t)row * n] : 0.0; };
+    double rq0 = ld(k0), rq1 = ld(k0 + 1), rq2 = ld(k0 + 2);
+    if (grp == k0 / TC) {
+        switch (k0 % TC) {
+        case 0: make_refl3<TR, TC, 0>(a, rq0, vbuf + (k0 & 1) * ROWS, coefs + 2 * (k0 & 1), R + (size_t)k0 * n + k0, rg); break;
+        case 1: if constexpr (TC > 1) make_refl3<TR, TC, 1 % TC>(a, rq0, vbuf + (k0 & 1) * ROWS, coefs + 2 * (k0 & 1), R + (size_t)k0 * n + k0, rg); break;
+        case 2: if constexpr (TC > 2) make_refl3<TR, TC, 2 % TC>(a, rq0, vbuf + (k0 & 1) * ROWS, coefs + 2 * (k0 & 1), R + (size_t)k0 * n + k0, rg); break;
+        default: if constexpr (TC > 3) make_refl3<TR, TC, 3 % TC>(a, rq0, vbuf + (k0 & 1) * ROWS, coefs + 2 * (k0 & 1), R + (size_t)k0 * n + k0, rg); break;
+        }
+    }
+    __syncthreads();
+    for (int k = k0; k < n; ++k) {
+        if (tid == 0) qr_ev(0, k);
+        switch ((k + 1) % TC) {
+        case 0: fold_step<TR, TC, 0>(a, n, k, R, vbuf, coefs, rq0, rq1, rg, grp, cb, cR); break;
+        case 1: if constexpr (TC > 1) fold_step<TR, TC, 1 % TC>(a, n, k, R, vbuf, coefs, rq0, rq1, rg, grp, cb, cR); break;
+        case 2: if constexpr (TC > 2) fold_step<TR, TC, 2 % TC>(a, n, k, R, vbuf, coefs, rq0, rq1, rg, grp, cb, cR); break;
+        default: if constexpr (TC > 3) fold_step<TR, TC, 3 % TC>(a, n, k, R, vbuf, coefs, rq0, rq1, rg, grp, cb, cR); break;
+        }
+        if (tid == 0) qr_ev(6, k);
+        rq0 = rq1;
+        rq1 = rq2;
+        rq2 = ld(k + 3);
+        if (tid == 0) qr_ev(7, k);
+        __syncthreads();
+        if (tid == 0) qr_ev(3, k);
+    }
+}
+
+template <int TR, int TC>
+__global__ void __launch_bounds__(352, 1)
+    k_tsqr_leaf2(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t N, int M,
+                 double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag) {
+    constexpr int ROWS = kRG * TR;
+    __shared__ __align__(16) double vbuf[2 * ROWS];
+    __shared__ double coefs[4];
+    const int n = M + 1, tid = threadIdx.x, rg = tid & 3, cb = TC * (tid >> 2);
+    double* R = Rws + (size_t)blockIdx.x * n * n;
+    for (int idx = tid; idx < n * n; idx += blockDim.x) R[idx] = 0.0;
+    __syncthreads();
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+    const int64_t r1 = min(N, r0 + rows_per_cta);
+    bool bad = false;
+    for (int64_t base = r0; base < r1; base += ROWS) {
+        double a[TC][TR];
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+            const int64_t row = base + rg * TR + i;
+#pragma unroll
+            for (int c = 0; c < TC; ++c) {
+                const int col = cb + c;
+                float x = 0.0f;
+                if (row < r1 && col < n) x = col < M ? __ldg(H + row * ldh + col) : __ldg(Y + row);
+                bad |= !isfinite(x);
+                a[c][i] = (double)x;
+            }
+        }
+        fold2d<TR, TC>(a, n, 0, R, vbuf, coefs);
+    }
+    if (bad) atomicOr(flag, 1);
+}
+
+template <int TR, int TC>
+__global__ void __launch_bounds__(352, 1) k_tsqr_merge2(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n) {
+    constexpr int ROWS = kRG * TR;
+    __shared__ __align__(16) double vbuf[2 * ROWS];
+    __shared__ double coefs[4];
+    const int64_t c = (int64_t)blockIdx.x * 2 * stride, partner = c + stride;
+    if (partner >= slabs) return;
+    double* Ra = Rws + (size_t)c * n * n;
+    const double* Rb = Rws + (size_t)partner * n * n;
+    const int tid = threadIdx.x, rg = tid & 3, cb = TC * (tid >> 2);
+    for (int s = 0; s * ROWS < n; ++s) {
+        double a[TC][TR];
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+            const int row = s * ROWS + rg * TR + i;
+#pragma unroll
+            for (int cc = 0; cc < TC; ++cc) {
+                const int col = cb + cc;
+                a[cc][i] = (row < n && col < n && col >= row) ? Rb[(size_t)row * n + col] : 0.0;
+            }
+        }
+        fold2d<TR, TC>(a, n, s * ROWS, Ra, vbuf, coefs);
+    }
+}
+
 // ---- host side ---------------------------------------------------------------------
 
 // Variants: n <= 288: 2 threads x 24 rows per column (48-row tiles, <= 576
@@ -643,11 +863,21 @@ static auto dispatch(Var v, F&& f) {
     }
 }
 
+// 2D register-tiled leaf + merge (fold2d): n <= 264 (4 ceil(n/3) <= 352 threads).
+// ELMRNN_TSQR_2D=0/1 overrides the default (testing aid).
+constexpr int kTR2 = 16, kTC2 = 3;
+static bool use_2d(int n) {
+    if (n > 264) return false;
+    if (const char* e = std::getenv("ELMRNN_TSQR_2D")) return std::atoi(e) != 0;
+    return false;
+}
+static int threads_2d(int n) { return (4 * ((n + kTC2 - 1) / kTC2) + 31) / 32 * 32; }
+
 int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
     const int n = h->M + 1;
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
-    int per_sm = dispatch(v, [&](auto tr, auto p, auto b) {
+    int per_sm = use_2d(n) ? 1 : dispatch(v, [&](auto tr, auto p, auto b) {
         int ps = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &ps, k_tsqr_leaf<decltype(tr)::value, decltype(p)::value, decltype(b)::value>, threads, var_smem(v, n));
@@ -685,6 +915,14 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
     const int threads = var_threads(v, n);
     const char* lv = std::getenv("ELMRNN_TSQR_LEVELS");   // testing aid: stop the tree early
     const int64_t max_stride = lv ? ((int64_t)1 << std::atoi(lv)) : slabs;
+    if (use_2d(n)) {
+        for (int64_t stride = 1; stride < slabs && stride < max_stride; stride *= 2) {
+            int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
+            k_tsqr_merge2<kTR2, kTC2><<<(unsigned)pairs, threads_2d(n), 0, h->stream>>>(h->Rws, slabs, stride, n);
+            h->launches++;
+        }
+        return cudaGetLastError();
+    }
     return dispatch(v, [&](auto tr, auto p, auto b) {
         for (int64_t stride = 1; stride < slabs && stride < max_stride; stride *= 2) {
             int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
@@ -699,14 +937,14 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
 static unsigned long long* qr_trace_setup() {
     if (!std::getenv("ELMRNN_TRACE_QR")) return nullptr;
     unsigned long long* buf = nullptr;
-    cudaMalloc(&buf, sizeof(unsigned long long) * 4 * 4096);
-    cudaMemset(buf, 0, sizeof(unsigned long long) * 4 * 4096);
+    cudaMalloc(&buf, sizeof(unsigned long long) * 8 * 4096);
+    cudaMemset(buf, 0, sizeof(unsigned long long) * 8 * 4096);
     cudaMemcpyToSymbol(g_qr_trace, &buf, sizeof(buf));
     return buf;
 }
 static void qr_trace_dump(unsigned long long* buf) {
     if (!buf) return;
-    std::vector<unsigned long long> hb(4 * 4096);
+    std::vector<unsigned long long> hb(8 * 4096);
     cudaDeviceSynchronize();
     cudaMemcpy(hb.data(), buf, sizeof(unsigned long long) * hb.size(), cudaMemcpyDeviceToHost);
     unsigned long long* null = nullptr;
@@ -714,7 +952,11 @@ static void qr_trace_dump(unsigned long long* buf) {
     cudaFree(buf);
     if (FILE* f = std::fopen(std::getenv("ELMRNN_TRACE_QR"), "w")) {
         for (int k = 0; k < 4096; ++k)
-            if (hb[4 * k]) std::fprintf(f, "%d,%llu,%llu,%llu,%llu\n", k, hb[4 * k], hb[4 * k + 1], hb[4 * k + 2], hb[4 * k + 3]);
+            if (hb[8 * k]) {
+                std::fprintf(f, "%d", k);
+                for (int s2 = 0; s2 < 8; ++s2) std::fprintf(f, ",%llu", hb[8 * k + s2]);
+                std::fprintf(f, "\n");
+            }
         std::fclose(f);
     }
 }
@@ -727,10 +969,16 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
     cudaError_t e;
     if ((e = ensure_solve_ws(h, slabs))) return e;
     if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream))) return e;
-    const int rows_tile = var_rows(v);
+    const int rows_tile = use_2d(n) ? kRG * kTR2 : var_rows(v);
     int64_t rows = (N + slabs - 1) / slabs;
     rows = (rows + rows_tile - 1) / rows_tile * rows_tile;
     const int threads = var_threads(v, n);
+    if (use_2d(n)) {
+        k_tsqr_leaf2<kTR2, kTC2><<<(unsigned)slabs, threads_2d(n), 0, h->stream>>>(H, ldh, Y, N, h->M, h->Rws, rows, h->flag);
+        h->launches++;
+        if ((e = cudaGetLastError())) return e;
+        return tree(h, slabs);
+    }
     e = dispatch(v, [&](auto tr, auto p, auto b) {
         k_tsqr_leaf<decltype(tr)::value, decltype(p)::value, decltype(b)::value>
             <<<(unsigned)slabs, threads, var_smem(v, n), h->stream>>>(H, ldh, Y, N, h->M, h->Rws, rows, h->flag);

@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libelmrnn.so")
+LIB_PATH = os.environ.get("ELMRNN_LIB") or os.path.join(_HERE, "libelmrnn.so")   # override: testing aid
 
 ARCHS = {"elman": 0, "jordan": 1, "narmax": 2, "fc": 3, "lstm": 4, "gru": 5}
 STATUS = {0: "OK", 1: "WARN_RIDGE", -1: "ERR_ARG", -2: "ERR_SHAPE", -3: "ERR_UNDERDETERMINED",

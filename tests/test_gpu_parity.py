@@ -140,6 +140,21 @@ def test_fc_tc_lag_ring(L, act, N, Q):
     assert err <= H_TOL, f"max |dH| = {err:.3e}"
 
 
+@pytest.mark.parametrize("arch,M,N,Q,S", [("lstm", 256, 700, 20, 1), ("lstm", 128, 300, 9, 2),
+                                           ("gru", 128, 500, 30, 4), ("fc", 128, 400, 12, 3)])
+def test_tc_two_pass_fp16_grid(arch, M, N, Q, S):
+    """weight_grid = 1 (fp16-representable U / A_k, SURVEY 8(c) "2xFP16 A-split"):
+    the tensor path drops the hi.lo pass; parity against the oracle run on the
+    same grid-rounded weights."""
+    X, _, _ = inputs(N, Q, S, seed=M + Q + 1)
+    e, Hg = gpu_H(arch, S, M, Q, 8, X, force_path=2, weight_grid=1)
+    assert e.path == 2
+    net = oracle_net(arch, S, M, Q, weight_grid=1)
+    Ho = orc.build_H(net, orc.gen_weights(net, 8), X, threads=8)
+    err = np.abs(Hg - Ho).max()
+    assert err <= H_TOL, f"max |dH| = {err:.3e}"
+
+
 def test_H_written_once_and_ld_respected():
     N, M, Q = 100, 20, 10
     X, _, _ = inputs(N, Q, 1)
