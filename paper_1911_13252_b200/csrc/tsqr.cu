@@ -127,6 +127,13 @@ __device__ __forceinline__ int col_of(int n) {
 // clock at loop top (thread 0), after the update of thread k+1, after its
 // reflector, and after the barrier.
 __device__ unsigned long long* g_qr_trace = nullptr;
+__device__ __forceinline__ void qr_ev_t(int slot, int k) {   // globaltimer (ns) variant
+#ifdef ELM_QR_TRACE
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if (g_qr_trace && blockIdx.x == 0 && k < 4096) g_qr_trace[k * 8 + slot] = t;
+#endif
+}
 __device__ __forceinline__ void qr_ev(int slot, int k) {
 #ifdef ELM_QR_TRACE   // compiled in only for tracing builds: the pointer load sits on the critical path
     if (g_qr_trace && blockIdx.x == 0 && k < 4096) g_qr_trace[k * 8 + slot] = clock64();
@@ -823,6 +830,356 @@ __global__ void __launch_bounds__(352, 1) k_tsqr_merge2(double* __restrict__ Rws
     }
 }
 
+// ---- blocked compact-WY fold (k_tsqr_leaf_wy / k_tsqr_merge_wy) ------------------------
+// The north star's "blocked Householder TSQR: panel factorisation with warp-level
+// reductions, trailing update as a blocked-reflector update".  A tile of ROWS
+// rows lives in SHARED memory as fp64 (so 2-4 CTAs fit per SM and one CTA's
+// latency-bound panel overlaps another's FMA-bound trailing update); R stays
+// in its L2-resident slab.  Per panel of kNBW = 16 columns:
+//  1. warp 0 factors [R diag block; tile panel] column by column in registers
+//     (lane = (rg, column pair); reductions are 4-lane butterflies over rg;
+//     no block barrier inside the panel) and leaves the reflector tails v_i in
+//     the tile's panel columns, (g_i, u0_i) and the R block in shared memory;
+//  2. all threads form G = striu(V^T V);
+//  3. every trailing column pair applies Q^T = I + U T'^T U^T at once:
+//     W = U^T C,  W' = T'^T W,  C_R += u0 W',  C_A += V W',  where the
+//     UT transform gives T'^T = (diag(1/g) - striu(U^T U))^{-T}, so W' follows
+//     from a 16-step forward substitution per column and T' is never formed
+//     (u_a^T u_b = v_a^T v_b for a != b: the R parts of u are distinct unit rows).
+constexpr int kNBW = 16;
+
+// Shared-memory load the compiler may not hoist (keeps the 16 u0 / G values
+// out of registers across the trailing loops).
+__device__ __forceinline__ double lds_nohoist(const double* p) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return v;
+}
+
+__host__ __device__ constexpr int wy_ldc(int n) { return (n + 7) & ~7; }   // >= n, whole 8-column MMA tiles
+__host__ __device__ constexpr size_t wy_smem_bytes(int rows, int n) {
+    return ((size_t)rows * wy_ldc(n) + kNBW * kNBW * 3 + 4 * kNBW) * sizeof(double);
+}
+
+template <int ROWS>
+__device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, int nbp, double* Rd, double* cgv,
+                                      double* cuv) {
+    constexpr int RPL = ROWS / 4;   // rows per lane: rows rg, rg+4, ... (interleaved: no bank conflicts)
+    const int lane = threadIdx.x & 31, rg = lane >> 3, cp = lane & 7;
+    const int c0 = 2 * cp, c1 = c0 + 1;
+    double a0[RPL], a1[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+        const double* row = C + (size_t)(rg + 4 * r) * LDC + p;
+        a0[r] = c0 < nbp ? row[c0] : 0.0;
+        a1[r] = c1 < nbp ? row[c1] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < kNBW; ++i) {
+        if (i >= nbp) break;
+        constexpr unsigned F = 0xffffffffu;
+        const int src = (lane & 24) | (i >> 1);   // owner lane of column i with this lane's rows
+        // ---- reflector of panel column i (owner lanes cp == i/2; all 4 compute it)
+        double s2a = 0.0, s2b = 0.0;
+#pragma unroll
+        for (int r = 0; r < RPL; r += 2) {
+            const double x = (i & 1) ? a1[r] : a0[r], y = (i & 1) ? a1[r + 1] : a0[r + 1];
+            s2a = fma(x, x, s2a);
+            s2b = fma(y, y, s2b);
+        }
+        double s2 = s2a + s2b;
+        s2 += __shfl_xor_sync(F, s2, 8);
+        s2 += __shfl_xor_sync(F, s2, 16);
+        double g = 0.0, u0 = 0.0;
+        if (cp == (i >> 1)) {
+            const double x0 = Rd[i * kNBW + i];
+            if (s2 != 0.0) {
+                const double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * sqrt(fma(x0, x0, s2));
+                const double uu = x0 - beta;
+                if (fabs(beta * uu) > 1e-280) {   // see make_reflector
+                    u0 = uu;
+                    g = 1.0 / (beta * uu);
+                    if (rg == 0) Rd[i * kNBW + i] = beta;
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) C[(size_t)(rg + 4 * r) * LDC + p + i] = (i & 1) ? a1[r] : a0[r];
+            if (rg == 0) {
+                cgv[i] = g;
+                cuv[i] = u0;
+            }
+        }
+        g = __shfl_sync(F, g, i >> 1);
+        u0 = __shfl_sync(F, u0, i >> 1);
+        if (g != 0.0 && i + 1 < nbp) {
+            // ---- apply H_i to the panel columns right of i; v by shuffle from the owner
+            double v[RPL];
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) v[r] = __shfl_sync(F, (i & 1) ? a1[r] : a0[r], src);
+            double w0 = (rg == 0 && c0 > i && c0 < nbp) ? u0 * Rd[i * kNBW + c0] : 0.0;
+            double w1 = (rg == 0 && c1 > i && c1 < nbp) ? u0 * Rd[i * kNBW + c1] : 0.0;
+            double w0b = 0.0, w1b = 0.0;
+#pragma unroll
+            for (int r = 0; r < RPL; r += 2) {
+                w0 = fma(v[r], a0[r], w0);
+                w1 = fma(v[r], a1[r], w1);
+                w0b = fma(v[r + 1], a0[r + 1], w0b);
+                w1b = fma(v[r + 1], a1[r + 1], w1b);
+            }
+            w0 += w0b;
+            w1 += w1b;
+            w0 += __shfl_xor_sync(F, w0, 8);
+            w1 += __shfl_xor_sync(F, w1, 8);
+            w0 += __shfl_xor_sync(F, w0, 16);
+            w1 += __shfl_xor_sync(F, w1, 16);
+            const double f0 = (c0 > i && c0 < nbp) ? g * w0 : 0.0;
+            const double f1 = (c1 > i && c1 < nbp) ? g * w1 : 0.0;
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) {
+                a0[r] = fma(f0, v[r], a0[r]);
+                a1[r] = fma(f1, v[r], a1[r]);
+            }
+            if (rg == 0) {
+                if (c0 > i && c0 < nbp) Rd[i * kNBW + c0] = fma(f0, u0, Rd[i * kNBW + c0]);
+                if (c1 > i && c1 < nbp) Rd[i * kNBW + c1] = fma(f1, u0, Rd[i * kNBW + c1]);
+            }
+        }
+    }
+    __syncwarp();
+}
+
+// f64 tensor-core MMA, m8n8k4: A row-major 8x4 (lane: A[lane/4][lane%4]), B col 4x8
+// (lane: B[lane%4][lane/4]), C/D 8x8 (lane: D[lane/4][2(lane%4) + {0,1}]).
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+// Trailing update of columns [pe, n) by the panel's block reflector, on the
+// f64 tensor cores: each warp takes 8-column tiles;
+//   GEMM 1  W (16 x 8) = u0 o R[p.., j] + V^T C        (K = ROWS)
+//   solve   W' = T'^T W (16-step forward substitution across the 8 lanes of a column)
+//   R[p+i][j] += u0_i W'_i
+//   GEMM 2  C (ROWS x 8) += V W'                        (K = 16)
+// The V fragments of both GEMMs are loaded once per panel and stay in registers.
+template <int ROWS>
+__device__ __forceinline__ void wy_trailing(double* __restrict__ C, int LDC, int n, int p, int pe, int jend,
+                                            int warp, int nw, double* __restrict__ R, const double* Gs,
+                                            const double* cgv, const double* cuv) {
+    constexpr int KS1 = ROWS / 4, MT2 = ROWS / 8;
+    const int lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const double u0r[2] = {cuv[gid], cuv[8 + gid]};
+    const double* Vt = C + p;   // V[r][i] = Vt[r * LDC + i]
+    // R rows p.. of the warp's first tile, then prefetched one tile ahead
+    auto ldR = [&](int j0, double (&rr)[2][2]) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int j = j0 + 2 * tig + e;
+                rr[mt][e] = (j0 < jend && j < n) ? R[(size_t)(p + 8 * mt + gid) * n + j] : 0.0;
+            }
+    };
+    double rn[2][2];
+    ldR(pe + 8 * warp, rn);
+    for (int j0 = pe + 8 * warp; j0 < jend; j0 += 8 * nw) {
+        double d[2][2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            d[mt][0] = u0r[mt] * rn[mt][0];
+            d[mt][1] = u0r[mt] * rn[mt][1];
+        }
+        const double rcur[2][2] = {{rn[0][0], rn[0][1]}, {rn[1][0], rn[1][1]}};
+        ldR(j0 + 8 * nw, rn);
+#pragma unroll 8
+        for (int ks = 0; ks < KS1; ++ks) {
+            const double* row = C + (size_t)(4 * ks + tig) * LDC;
+            const double b = row[j0 + gid];
+            dmma(d[0], Vt[(size_t)(4 * ks + tig) * LDC + gid], b);
+            dmma(d[1], Vt[(size_t)(4 * ks + tig) * LDC + 8 + gid], b);
+        }
+        // W'_l = g_l (W_l + sum_{m<l} G[m][l] W'_m): finalise row l, push it down
+#pragma unroll
+        for (int l = 0; l < kNBW; ++l) {
+            const int mt = l >> 3;
+            if (gid == (l & 7)) {
+                const double gl = lds_nohoist(cgv + l);
+                d[mt][0] *= gl;
+                d[mt][1] *= gl;
+            }
+            if (l + 1 < kNBW) {
+                const double w0 = __shfl_sync(0xffffffffu, d[mt][0], (l & 7) * 4 + tig);
+                const double w1 = __shfl_sync(0xffffffffu, d[mt][1], (l & 7) * 4 + tig);
+#pragma unroll
+                for (int m2 = mt; m2 < 2; ++m2) {
+                    const int i = 8 * m2 + gid;
+                    if (i > l) {
+                        const double gg = lds_nohoist(Gs + l * kNBW + i);
+                        d[m2][0] = fma(gg, w0, d[m2][0]);
+                        d[m2][1] = fma(gg, w1, d[m2][1]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int j = j0 + 2 * tig + e;
+                if (j < n) R[(size_t)(p + 8 * mt + gid) * n + j] = fma(u0r[mt], d[mt][e], rcur[mt][e]);
+            }
+        // B fragments of W': B[k][n] = W'[4 kt + k][n], lane (k = tig, n = gid); W' row
+        // i = 4 kt + tig lives in D tile kt/2 on lanes (i % 8) * 4 + n / 2, element n % 2
+        double b2[4];
+#pragma unroll
+        for (int kt = 0; kt < 4; ++kt) {
+            const int srcl = ((4 * kt + tig) & 7) * 4 + (gid >> 1);
+            const double x0 = __shfl_sync(0xffffffffu, d[kt >> 1][0], srcl);
+            const double x1 = __shfl_sync(0xffffffffu, d[kt >> 1][1], srcl);
+            b2[kt] = (gid & 1) ? x1 : x0;
+        }
+#pragma unroll 4
+        for (int mt = 0; mt < MT2; ++mt) {
+            double2* cp2 = reinterpret_cast<double2*>(C + (size_t)(8 * mt + gid) * LDC + j0 + 2 * tig);
+            const double* vrow = Vt + (size_t)(8 * mt + gid) * LDC + tig;
+            const double2 cv = *cp2;
+            double acc[2] = {cv.x, cv.y};
+#pragma unroll
+            for (int kt = 0; kt < 4; ++kt) dmma(acc, vrow[4 * kt], b2[kt]);
+            *cp2 = make_double2(acc[0], acc[1]);
+        }
+    }
+}
+
+// Fold the shared-memory tile C (ROWS x n, columns < k0 zero) into R (n x n),
+// with one-panel look-ahead: while warps 1.. apply panel p's block reflector to
+// columns beyond panel p+1, warp 0 applies it to panel p+1's 16 columns and
+// factors panel p+1 -- the latency-bound panel chain overlaps the FMA-bound
+// trailing update.  Coefficients / G are double-buffered by panel parity.
+template <int ROWS>
+__device__ __forceinline__ void wy_gram(const double* C, int LDC, int p, int nbp, double* Gs) {
+    for (int e = threadIdx.x; e < kNBW * kNBW; e += blockDim.x) {
+        const int a = e / kNBW, b = e % kNBW;
+        double acc = 0.0, acc2 = 0.0;
+        if (a < b && b < nbp)
+            for (int r = 0; r < ROWS; r += 2) {
+                acc = fma(C[(size_t)r * LDC + p + a], C[(size_t)r * LDC + p + b], acc);
+                acc2 = fma(C[(size_t)(r + 1) * LDC + p + a], C[(size_t)(r + 1) * LDC + p + b], acc2);
+            }
+        Gs[e] = acc + acc2;
+    }
+}
+
+template <int ROWS>
+__device__ __forceinline__ void wy_panel_rd(double* C, int LDC, int n, int p, double* __restrict__ R, double* Rd,
+                                            double* cgv, double* cuv) {
+    const int lane = threadIdx.x & 31, nbp = min(kNBW, n - p);
+    for (int e = lane; e < kNBW * kNBW; e += 32) {
+        const int i = e / kNBW, c = e % kNBW;
+        Rd[e] = (i < nbp && c < nbp && c >= i) ? R[(size_t)(p + i) * n + p + c] : 0.0;
+    }
+    __syncwarp();
+    wy_panel<ROWS>(C, LDC, p, nbp, Rd, cgv, cuv);
+    for (int e = lane; e < kNBW * kNBW; e += 32) {
+        const int i = e / kNBW, c = e % kNBW;
+        if (i < nbp && c < nbp && c >= i) R[(size_t)(p + i) * n + p + c] = Rd[e];
+    }
+}
+
+template <int ROWS>
+__device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* __restrict__ R, double* Gs,
+                        double* Rd, double* cgv, double* cuv) {
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int p = k0, buf = 0;
+    if (warp == 0) wy_panel_rd<ROWS>(C, LDC, n, p, R, Rd, cgv, cuv);
+    __syncthreads();
+    wy_gram<ROWS>(C, LDC, p, min(kNBW, n - p), Gs);
+    __syncthreads();
+    for (;;) {
+        const int pe = p + min(kNBW, n - p);
+        if (pe >= n) break;   // no trailing columns (so below nbp == kNBW)
+        if (threadIdx.x == 0) qr_ev(0, p);
+        const int nbn = min(kNBW, n - pe);
+        double *G0 = Gs + buf * kNBW * kNBW, *g0 = cgv + buf * kNBW, *u0 = cuv + buf * kNBW;
+        if (warp == 0) {
+            // look-ahead: panel p+1's columns first, then factor it
+            wy_trailing<ROWS>(C, LDC, n, p, pe, nw == 1 ? n : pe + nbn, 0, 1, R, G0, g0, u0);
+            __syncwarp();
+            if (threadIdx.x == 0) qr_ev(1, p);
+            wy_panel_rd<ROWS>(C, LDC, n, pe, R, Rd, cgv + (buf ^ 1) * kNBW, cuv + (buf ^ 1) * kNBW);
+            if (threadIdx.x == 0) qr_ev(5, p);
+        } else {
+            wy_trailing<ROWS>(C, LDC, n, p, pe + nbn, n, warp - 1, nw - 1, R, G0, g0, u0);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) qr_ev(2, p);
+        p = pe;
+        buf ^= 1;
+        wy_gram<ROWS>(C, LDC, p, min(kNBW, n - p), Gs + buf * kNBW * kNBW);
+        __syncthreads();
+        if (threadIdx.x == 0) qr_ev(3, p - kNBW);
+    }
+}
+
+template <int ROWS>
+__global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
+    k_tsqr_leaf_wy(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t N, int M,
+                   double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag) {
+    extern __shared__ __align__(16) double wsm[];
+    const int n = M + 1, LDC = wy_ldc(n), tid = threadIdx.x, nt = blockDim.x;
+    double* C = wsm;
+    double* Gs = C + (size_t)ROWS * LDC;     // [2][16][16]
+    double* Rd = Gs + 2 * kNBW * kNBW;       // [16][16]
+    double* cgv = Rd + kNBW * kNBW;          // [2][16]
+    double* cuv = cgv + 2 * kNBW;            // [2][16]
+    double* R = Rws + (size_t)blockIdx.x * n * n;
+    for (int64_t e = tid; e < (int64_t)n * n; e += nt) R[e] = 0.0;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+    const int64_t r1 = min(N, r0 + rows_per_cta);
+    bool bad = false;
+    __syncthreads();
+    for (int64_t base = r0; base < r1; base += ROWS) {
+        for (int r = 0; r < ROWS; ++r) {
+            const int64_t row = base + r;
+            for (int c = tid; c < LDC; c += nt) {
+                float x = 0.0f;
+                if (row < r1 && c < n) x = c < M ? __ldg(H + row * ldh + c) : __ldg(Y + row);
+                bad |= !isfinite(x);
+                C[(size_t)r * LDC + c] = (double)x;
+            }
+        }
+        __syncthreads();
+        wy_fold<ROWS>(C, LDC, n, 0, R, Gs, Rd, cgv, cuv);
+    }
+    if (bad) atomicOr(flag, 1);
+}
+
+template <int ROWS>
+__global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1) k_tsqr_merge_wy(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n) {
+    extern __shared__ __align__(16) double wsm[];
+    const int64_t c = (int64_t)blockIdx.x * 2 * stride, partner = c + stride;
+    if (partner >= slabs) return;
+    const int LDC = wy_ldc(n), tid = threadIdx.x, nt = blockDim.x;
+    double* C = wsm;
+    double* Gs = C + (size_t)ROWS * LDC;     // [2][16][16]
+    double* Rd = Gs + 2 * kNBW * kNBW;       // [16][16]
+    double* cgv = Rd + kNBW * kNBW;          // [2][16]
+    double* cuv = cgv + 2 * kNBW;            // [2][16]
+    double* Ra = Rws + (size_t)c * n * n;
+    const double* Rb = Rws + (size_t)partner * n * n;
+    for (int s = 0; s * ROWS < n; ++s) {
+        for (int r = 0; r < ROWS; ++r) {
+            const int row = s * ROWS + r;
+            for (int cc = tid; cc < LDC; cc += nt)
+                C[(size_t)r * LDC + cc] = (row < n && cc < n && cc >= row) ? Rb[(size_t)row * n + cc] : 0.0;
+        }
+        __syncthreads();
+        wy_fold<ROWS>(C, LDC, n, s * ROWS, Ra, Gs, Rd, cgv, cuv);
+    }
+}
+
 // ---- host side ---------------------------------------------------------------------
 
 // Variants: n <= 288: 2 threads x 24 rows per column (48-row tiles, <= 576
@@ -873,11 +1230,48 @@ static bool use_2d(int n) {
 }
 static int threads_2d(int n) { return (4 * ((n + kTC2 - 1) / kTC2) + 31) / 32 * 32; }
 
+// Blocked compact-WY leaf + merge (wy_fold).  ELMRNN_TSQR_WY=0/1 overrides the default.
+// Measured (B200, profiles/): M = 256 WY 113 ms vs 147 ms per-column fold at
+// C4; M <= 128 the per-column fold is faster (C3 10.4 vs 11.8 ms).
+static bool use_wy(int n) {
+    if (const char* e = std::getenv("ELMRNN_TSQR_WY")) return std::atoi(e) != 0 && n <= 1024;
+    return n > 192 && n <= 1024;
+}
+static int wy_rows(int n) {
+    if (const char* e = std::getenv("ELMRNN_TSQR_WY_ROWS")) {   // testing aid
+        const int r = std::atoi(e);
+        if ((r == 96 || r == 64 || r == 32 || r == 16) && wy_smem_bytes(r, n) <= 220 * 1024) return r;
+    }
+    // 32-row tiles, 2-3 CTAs per SM (their panels overlap each other's trailing updates)
+    return wy_smem_bytes(32, n) <= 220 * 1024 ? 32 : 16;
+}
+static int wy_threads(int n) {
+    int w = n <= 320 ? 4 : std::min(8, ((n + 1) / 2 + 31) / 32);
+    if (const char* e = std::getenv("ELMRNN_TSQR_WY_WARPS")) w = std::max(1, std::min(8, std::atoi(e)));   // testing aid
+    return 32 * w;
+}
+template <class F>
+static auto wy_dispatch(int n, F&& f) {
+    switch (wy_rows(n)) {
+    case 96: return f(std::integral_constant<int, 96>{});
+    case 64: return f(std::integral_constant<int, 64>{});
+    case 32: return f(std::integral_constant<int, 32>{});
+    default: return f(std::integral_constant<int, 16>{});
+    }
+}
+
 int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
     const int n = h->M + 1;
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
-    int per_sm = use_2d(n) ? 1 : dispatch(v, [&](auto tr, auto p, auto b) {
+    int per_sm = use_wy(n) ? wy_dispatch(n, [&](auto rows) {
+        constexpr int RW = decltype(rows)::value;
+        const size_t sm = wy_smem_bytes(RW, n);
+        cudaFuncSetAttribute(k_tsqr_leaf_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        int ps = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_tsqr_leaf_wy<RW>, wy_threads(n), sm);
+        return ps < 1 ? 1 : ps;
+    }) : use_2d(n) ? 1 : dispatch(v, [&](auto tr, auto p, auto b) {
         int ps = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &ps, k_tsqr_leaf<decltype(tr)::value, decltype(p)::value, decltype(b)::value>, threads, var_smem(v, n));
@@ -915,6 +1309,19 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
     const int threads = var_threads(v, n);
     const char* lv = std::getenv("ELMRNN_TSQR_LEVELS");   // testing aid: stop the tree early
     const int64_t max_stride = lv ? ((int64_t)1 << std::atoi(lv)) : slabs;
+    if (use_wy(n)) {
+        return wy_dispatch(n, [&](auto rows) {
+            constexpr int RW = decltype(rows)::value;
+            const size_t sm = wy_smem_bytes(RW, n);
+            cudaFuncSetAttribute(k_tsqr_merge_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            for (int64_t stride = 1; stride < slabs && stride < max_stride; stride *= 2) {
+                int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
+                k_tsqr_merge_wy<RW><<<(unsigned)pairs, wy_threads(n), sm, h->stream>>>(h->Rws, slabs, stride, n);
+                h->launches++;
+            }
+            return cudaGetLastError();
+        });
+    }
     if (use_2d(n)) {
         for (int64_t stride = 1; stride < slabs && stride < max_stride; stride *= 2) {
             int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
@@ -969,10 +1376,23 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
     cudaError_t e;
     if ((e = ensure_solve_ws(h, slabs))) return e;
     if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream))) return e;
-    const int rows_tile = use_2d(n) ? kRG * kTR2 : var_rows(v);
+    const int rows_tile = use_wy(n) ? wy_rows(n) : use_2d(n) ? kRG * kTR2 : var_rows(v);
     int64_t rows = (N + slabs - 1) / slabs;
     rows = (rows + rows_tile - 1) / rows_tile * rows_tile;
     const int threads = var_threads(v, n);
+    if (use_wy(n)) {
+        e = wy_dispatch(n, [&](auto rws) {
+            constexpr int RW = decltype(rws)::value;
+            const size_t sm = wy_smem_bytes(RW, n);
+            cudaFuncSetAttribute(k_tsqr_leaf_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_tsqr_leaf_wy<RW><<<(unsigned)slabs, wy_threads(n), sm, h->stream>>>(H, ldh, Y, N, h->M, h->Rws, rows,
+                                                                                 h->flag);
+            h->launches++;
+            return cudaGetLastError();
+        });
+        if (e) return e;
+        return tree(h, slabs);
+    }
     if (use_2d(n)) {
         k_tsqr_leaf2<kTR2, kTC2><<<(unsigned)slabs, threads_2d(n), 0, h->stream>>>(H, ldh, Y, N, h->M, h->Rws, rows, h->flag);
         h->launches++;

@@ -154,7 +154,11 @@ class ELMRNN:
             lib().elmrnn_destroy(self._h)
             self._h = None
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:   # interpreter shutdown: module globals may already be gone
+            pass
 
     @property
     def path(self) -> int:
