@@ -1108,15 +1108,28 @@ __device__ __forceinline__ void wy_gram(const double* C, int LDC, int p, int nbp
     }
 }
 
+// R diagonal block of panel p (16 x 16, upper part) <-> registers / shared memory.
+// The panel warp reads the NEXT panel's block one step early (its R rows are
+// not touched by the current step), so the load latency leaves the panel chain.
+__device__ __forceinline__ void rd_load(const double* __restrict__ R, int n, int p, double (&rr)[8]) {
+    const int lane = threadIdx.x & 31, nbp = min(kNBW, n - p);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const int e = lane + 32 * t, i = e / kNBW, c = e % kNBW;
+        rr[t] = (p < n && i < nbp && c < nbp && c >= i) ? R[(size_t)(p + i) * n + p + c] : 0.0;
+    }
+}
+__device__ __forceinline__ void rd_put(double* Rd, const double (&rr)[8]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) Rd[lane + 32 * t] = rr[t];
+    __syncwarp();
+}
+
 template <int ROWS>
 __device__ __forceinline__ void wy_panel_rd(double* C, int LDC, int n, int p, double* __restrict__ R, double* Rd,
                                             double* cgv, double* cuv) {
     const int lane = threadIdx.x & 31, nbp = min(kNBW, n - p);
-    for (int e = lane; e < kNBW * kNBW; e += 32) {
-        const int i = e / kNBW, c = e % kNBW;
-        Rd[e] = (i < nbp && c < nbp && c >= i) ? R[(size_t)(p + i) * n + p + c] : 0.0;
-    }
-    __syncwarp();
     wy_panel<ROWS>(C, LDC, p, nbp, Rd, cgv, cuv);
     for (int e = lane; e < kNBW * kNBW; e += 32) {
         const int i = e / kNBW, c = e % kNBW;
@@ -1133,7 +1146,13 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
     const int pw = (int)(blockIdx.x % nw), tw = warp < pw ? warp : warp - 1;
     const bool lane0 = (threadIdx.x & 31) == 0 && warp == pw;
     int p = k0, buf = 0;
-    if (warp == pw) wy_panel_rd<ROWS>(C, LDC, n, p, R, Rd, cgv, cuv);
+    double rdn[8];   // panel warp: next panel's R diagonal block
+    if (warp == pw) {
+        rd_load(R, n, p, rdn);
+        rd_put(Rd, rdn);
+        rd_load(R, n, p + kNBW, rdn);
+        wy_panel_rd<ROWS>(C, LDC, n, p, R, Rd, cgv, cuv);
+    }
     __syncthreads();
     wy_gram<ROWS>(C, LDC, p, min(kNBW, n - p), Gs);
     __syncthreads();
@@ -1146,9 +1165,13 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
         if (nw == 1) {
             wy_trailing<ROWS>(C, LDC, n, p, pe, n, 0, 1, R, G0, g0, u0);
             __syncwarp();
+            rd_put(Rd, rdn);
+            rd_load(R, n, pe + kNBW, rdn);
             wy_panel_rd<ROWS>(C, LDC, n, pe, R, Rd, cgv + (buf ^ 1) * kNBW, cuv + (buf ^ 1) * kNBW);
         } else if (warp == pw) {
             // look-ahead: wait until panel p+1's columns carry panel p's update, factor it
+            rd_put(Rd, rdn);
+            rd_load(R, n, pe + kNBW, rdn);
             named_bar_sync(1, nw * 32);
             if (lane0) qr_ev(1, p);
             wy_panel_rd<ROWS>(C, LDC, n, pe, R, Rd, cgv + (buf ^ 1) * kNBW, cuv + (buf ^ 1) * kNBW);
@@ -1307,6 +1330,13 @@ static auto wy_dispatch(int n, F&& f) {
     }
 }
 
+template <class F>
+static auto wy_dispatch_merge(int n, F&& f) {
+    if (wy_smem_bytes(96, n) <= 220 * 1024) return f(std::integral_constant<int, 96>{});
+    if (wy_smem_bytes(64, n) <= 220 * 1024) return f(std::integral_constant<int, 64>{});
+    return wy_dispatch(n, f);
+}
+
 int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
     const int n = h->M + 1;
     const Var v = pick_var(n);
@@ -1357,7 +1387,9 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
     const char* lv = std::getenv("ELMRNN_TSQR_LEVELS");   // testing aid: stop the tree early
     const int64_t max_stride = lv ? ((int64_t)1 << std::atoi(lv)) : slabs;
     if (use_wy(n)) {
-        return wy_dispatch(n, [&](auto rows) {
+        // merges are latency-bound (one CTA per pair, few pairs at the top of the
+        // tree): the tallest tile that fits means the fewest panel steps per fold
+        return wy_dispatch_merge(n, [&](auto rows) {
             constexpr int RW = decltype(rows)::value;
             const size_t sm = wy_smem_bytes(RW, n);
             cudaFuncSetAttribute(k_tsqr_merge_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -257,6 +257,34 @@ def test_virtual_ranks_merge_equals_single():
     assert (b2 - b1).norm() / b1.norm() <= 1e-12
 
 
+def _packed_to_R(Rpk, n):
+    R = np.zeros((n, n))
+    off = 0
+    for k in range(n):
+        R[k, k:] = Rpk[off: off + n - k]
+        off += n - k
+    return R
+
+
+@pytest.mark.parametrize("M,N", [(200, 1001), (256, 20011), (300, 5003), (511, 3001), (129, 777)])
+def test_tsqr_wy_and_fold_agree(M, N, monkeypatch):
+    """The blocked compact-WY TSQR (k_tsqr_leaf_wy, UT-transform trailing update on
+    f64 tensor cores) and the per-column fold produce the same R of [H | Y] as
+    numpy's Householder QR (LAPACK geqrf), up to row signs (reading R18)."""
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    H = torch.rand(N, M, device="cuda", generator=g) - 0.5
+    Y = torch.rand(N, device="cuda", generator=g) - 0.5
+    n = M + 1
+    Rn = np.abs(np.linalg.qr(np.column_stack([H.double().cpu().numpy(), Y.double().cpu().numpy()]), mode="r"))
+    scale = Rn.max()
+    for wy in ("1", "0"):
+        monkeypatch.setenv("ELMRNN_TSQR_WY", wy)
+        e = E("lstm", 1, M, 4, 1, force_path=1)
+        R = _packed_to_R(e.solve_local(H, Y).cpu().numpy(), n)
+        assert np.isfinite(R).all()
+        assert np.abs(np.abs(R) - Rn).max() <= 1e-12 * scale, wy
+
+
 def test_ridge_and_nonfinite():
     from paper_1911_13252_b200 import ElmrnnError
     e = E("elman", 1, 4, 3, 1)
