@@ -135,11 +135,11 @@ def make_inputs(cfg: str, N_total: int, rank: int, world: int):
 
 
 # ------------------------------------------------------------------- cpu baseline (oracle)
-def cpu_oracle_rate(cfg: str, n_sub: int, X, Y, threads: int):
+def cpu_oracle_rate(cfg: str, n_sub: int, X, Y, threads: int, weight_grid: int = 0):
     """Time the fp64 oracle (as it stands) on n_sub rows: H build + QR."""
     from oracle import oracle as orc
     c = sy.CONFIGS[cfg]
-    net = orc.Net(c["arch"], S=c["S"], M=c["M"], Q=c["Q"])
+    net = orc.Net(c["arch"], S=c["S"], M=c["M"], Q=c["Q"], weight_grid=weight_grid)
     blocks = orc.gen_weights(net, 1)
     t0 = time.perf_counter()
     H = orc.build_H(net, blocks, X[:n_sub], threads=threads)
@@ -167,8 +167,8 @@ def run_reference(args, rank: int, world: int):
     X, Y, _ = make_inputs(cfg, n, 0, 1)
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
-        cpu_oracle_rate(cfg, n, X, Y, threads)
-    times = [cpu_oracle_rate(cfg, n, X, Y, threads)[1] for _ in range(args.steps)]
+        cpu_oracle_rate(cfg, n, X, Y, threads, args.weight_grid)
+    times = [cpu_oracle_rate(cfg, n, X, Y, threads, args.weight_grid)[1] for _ in range(args.steps)]
     tot = sum(times)
     value = n * args.steps / tot
     sample = (f"{n} windows of {WORKLOAD_NAMES[cfg]} per step: fp64 oracle H build ({threads} threads, "
@@ -195,6 +195,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines)")
     ap.add_argument("--force-path", type=int, default=0)
+    ap.add_argument("--weight-grid", type=int, default=0, choices=[0, 1],
+                    help="1: recurrent weights on the fp16 grid (SURVEY 8(c) '2xFP16 A-split'; 2-pass MMA)")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay the step as a CUDA graph (auto: configs whose step is launch-latency bound)")
     args = ap.parse_args()
@@ -225,7 +227,8 @@ def main():
     Yd = Yh.cuda()
     Hd = torch.empty((N_local, c["M"]), dtype=torch.float32, device="cuda")
     beta = torch.empty(c["M"], dtype=torch.float64, device="cuda")
-    model = ELMRNN(c["arch"], c["S"], c["M"], c["Q"], seed=1, force_path=args.force_path)
+    model = ELMRNN(c["arch"], c["S"], c["M"], c["Q"], seed=1, force_path=args.force_path,
+                   weight_grid=args.weight_grid)
     stream = torch.cuda.current_stream()
 
     def step(ev_b0=None, ev_b1=None):
@@ -303,13 +306,25 @@ def main():
         beta_h = torch.empty(c["M"], dtype=torch.float64).pin_memory()
         barrier()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        for _ in range(K):
-            Xd.copy_(Xh, non_blocking=True)
+        cs = torch.cuda.Stream()
+
+        def e2e_step():
+            # public API from pinned host inputs: the X copy is chunked and
+            # overlapped with the build (ELMRNN.build_H_from_host), Y rides along
             Yd.copy_(Yh, non_blocking=True)
-            step()
+            model.build_H_from_host(Xh, Xd, Hd, chunks=4, copy_stream=cs)
+            if world == 1:
+                model.solve_beta(Hd, Yd, beta, info=False)
+            else:
+                par.solve_sharded(model, Hd, Yd, N_total, beta)
             beta_h.copy_(beta, non_blocking=True)
             stream.synchronize()
+
+        e2e_step()   # untimed warm-up of the e2e path (side stream, events)
+        barrier()
+        t0.record(stream)
+        for _ in range(K):
+            e2e_step()
         t1.record(stream)
         barrier()
         ems = t0.elapsed_time(t1)
@@ -337,8 +352,10 @@ def main():
     elif path == 2:
         bound, unit = "tensor", "TFLOP/s"
         achieved = flops / (build_ms / 1e3) / 1e12
-        peak = peaks["bf16_tflops"] / 3.0
-        peak_note = f"{src} bf16 dense burst / 3 (3-pass fp16 split emulating fp32)"
+        passes = 2 if args.weight_grid == 1 else 3
+        peak = peaks["bf16_tflops"] / passes
+        peak_note = (f"{src} bf16 dense burst / {passes} ({passes}-pass fp16 split emulating fp32"
+                     + (", fp16-grid weights)" if passes == 2 else ")"))
     else:
         bound, unit = "alu", "TFLOP/s"
         achieved = flops / (build_ms / 1e3) / 1e12
@@ -355,7 +372,7 @@ def main():
     if not args.no_cpu_baseline and not args.profile and world == 1:
         n_sub = oracle_sample_rows(cfg)
         threads = os.cpu_count() or 1
-        rate, dt = cpu_oracle_rate(cfg, n_sub, X, Y, threads)
+        rate, dt = cpu_oracle_rate(cfg, n_sub, X, Y, threads, args.weight_grid)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
                "sample": f"{n_sub} windows of the same workload, fp64 H build ({threads} threads) + fp64 "
                          f"Householder QR (1 thread), {dt:.1f} s"}
@@ -364,7 +381,7 @@ def main():
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32+f64", "data": "synthetic",
             "config": {"workload": WORKLOAD_NAMES[cfg], "N_total": N_total, "rows_per_gpu": N_local,
-                       "path": "tcgen05" if path == 2 else "fp32-fma", "weights": "fp32 (grid 0), seed 1",
+                       "path": "tcgen05" if path == 2 else "fp32-fma", "weights": ("fp16 grid (weight_grid=1)" if args.weight_grid == 1 else "fp32 (grid 0)") + ", seed 1",
                        "qr": "fp64 Householder TSQR", "parallelism": f"dp{world} rows + all-gather R",
                        "l2": ("256 MB L2 flush between timed steps (inputs fit in L2)" if small and world == 1
                               else "no flush: X and H exceed the 126 MB L2"),

@@ -1139,11 +1139,9 @@ __device__ __forceinline__ void wy_panel_rd(double* C, int LDC, int n, int p, do
 
 template <int ROWS>
 __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* __restrict__ R, double* Gs,
-                        double* Rd, double* cgv, double* cuv) {
+                        double* Rd, double* cgv, double* cuv, int pw) {
     const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    // the panel warp rotates with the CTA index so co-resident CTAs' latency-bound
-    // panels land on different SM sub-partitions (warp slot % 4)
-    const int pw = (int)(blockIdx.x % nw), tw = warp < pw ? warp : warp - 1;
+    const int tw = warp < pw ? warp : warp - 1;
     const bool lane0 = (threadIdx.x & 31) == 0 && warp == pw;
     int p = k0, buf = 0;
     double rdn[8];   // panel warp: next panel's R diagonal block
@@ -1192,10 +1190,29 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
     }
 }
 
+// Panel warp of this CTA: co-resident CTAs (typically blocks b, b+148, ...)
+// take distinct warp indices, so their latency-bound panels run on different
+// SM sub-partitions (warp slot % 4).  sm_slot: per-SM arrival counters,
+// zeroed before the launch (null: use the block index).
+__device__ __forceinline__ int wy_panel_warp(int* sm_slot) {
+    __shared__ int pw_s;
+    if (threadIdx.x == 0) {
+        int local = (int)blockIdx.x;
+        if (sm_slot) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            local = atomicAdd(sm_slot + (smid & 1023), 1);
+        }
+        pw_s = local % (int)(blockDim.x >> 5);
+    }
+    __syncthreads();
+    return pw_s;
+}
+
 template <int ROWS>
 __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
     k_tsqr_leaf_wy(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t N, int M,
-                   double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag) {
+                   double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag, int* sm_slot) {
     extern __shared__ __align__(16) double wsm[];
     const int n = M + 1, LDC = wy_ldc(n), tid = threadIdx.x, nt = blockDim.x;
     double* C = wsm;
@@ -1208,7 +1225,7 @@ __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
     const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
     const int64_t r1 = min(N, r0 + rows_per_cta);
     bool bad = false;
-    __syncthreads();
+    const int pw = wy_panel_warp(sm_slot);
     for (int64_t base = r0; base < r1; base += ROWS) {
         for (int r = 0; r < ROWS; ++r) {
             const int64_t row = base + r;
@@ -1220,7 +1237,7 @@ __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
             }
         }
         __syncthreads();
-        wy_fold<ROWS>(C, LDC, n, 0, R, Gs, Rd, cgv, cuv);
+        wy_fold<ROWS>(C, LDC, n, 0, R, Gs, Rd, cgv, cuv, pw);
     }
     if (bad) atomicOr(flag, 1);
 }
@@ -1245,7 +1262,7 @@ __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1) k_tsqr_merge_wy(doubl
                 C[(size_t)r * LDC + cc] = (row < n && cc < n && cc >= row) ? Rb[(size_t)row * n + cc] : 0.0;
         }
         __syncthreads();
-        wy_fold<ROWS>(C, LDC, n, s * ROWS, Ra, Gs, Rd, cgv, cuv);
+        wy_fold<ROWS>(C, LDC, n, s * ROWS, Ra, Gs, Rd, cgv, cuv, (int)(blockIdx.x % (blockDim.x >> 5)));
     }
 }
 
@@ -1372,8 +1389,8 @@ cudaError_t ensure_solve_ws(elmrnn* h, int64_t slabs) {
         if ((e = cudaMalloc(&h->Rws, (size_t)(slabs + 1) * n * n * sizeof(double)))) return e;
         h->Rws_slabs = slabs + 1;
     }
-    if (!h->sdev) {
-        if ((e = cudaMalloc(&h->sdev, sizeof(SolveDev)))) return e;
+    if (!h->sdev) {   // SolveDev + 1024 ints of per-SM counters (k_tsqr_leaf_wy)
+        if ((e = cudaMalloc(&h->sdev, sizeof(SolveDev) + 1024 * sizeof(int)))) return e;
         if ((e = cudaMalloc(&h->flag, sizeof(int)))) return e;
         if ((e = cudaMallocHost(&h->shost, sizeof(SolveDev)))) return e;
     }
@@ -1464,8 +1481,10 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
             constexpr int RW = decltype(rws)::value;
             const size_t sm = wy_smem_bytes(RW, n);
             cudaFuncSetAttribute(k_tsqr_leaf_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            int* slot = reinterpret_cast<int*>(h->sdev + 1);   // per-SM arrival counters (ensure_solve_ws)
+            cudaMemsetAsync(slot, 0, 1024 * sizeof(int), h->stream);
             k_tsqr_leaf_wy<RW><<<(unsigned)slabs, wy_threads(n), sm, h->stream>>>(H, ldh, Y, N, h->M, h->Rws, rows,
-                                                                                 h->flag);
+                                                                                 h->flag, slot);
             h->launches++;
             return cudaGetLastError();
         });

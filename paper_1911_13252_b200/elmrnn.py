@@ -190,6 +190,28 @@ class ELMRNN:
         self._check(lib().elmrnn_build_H(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, N, _ptr(H), ldh))
         return H
 
+    def build_H_from_host(self, Xh: torch.Tensor, Xd: torch.Tensor, H: torch.Tensor, chunks: int = 8,
+                          copy_stream: torch.cuda.Stream | None = None):
+        """elmrnn_build_H over row chunks of a pinned host X: the host->device copy
+        of chunk k+1 (on `copy_stream`) overlaps the build of chunk k (current
+        stream).  Rows are independent (every sample's window runs on its own),
+        so this is only copy scheduling; Xd is the device staging buffer."""
+        N = Xh.shape[0]
+        cs = copy_stream or torch.cuda.Stream()
+        cur = torch.cuda.current_stream()
+        cs.wait_stream(cur)   # Xd / H may still be in use by earlier work on this stream
+        cuts = [N * k // chunks for k in range(chunks + 1)]
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            if b <= a:
+                continue
+            with torch.cuda.stream(cs):
+                Xd[a:b].copy_(Xh[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+            cur.wait_event(ev)
+            self.build_H(Xd[a:b], None, H[a:b])
+        return H
+
     def solve_beta(self, H: torch.Tensor, Y: torch.Tensor, beta: torch.Tensor | None = None, info: bool = True):
         """elmrnn_solve_beta -> (beta fp64 [M], SolveInfo or None)."""
         _dev_check(H, "H", torch.float32)

@@ -169,6 +169,22 @@ def test_H_written_once_and_ld_respected():
     assert np.abs(H[:, :M].cpu().numpy() - ref).max() <= H_TOL
 
 
+@pytest.mark.parametrize("arch,M", [("lstm", 128), ("gru", 32), ("elman", 20)])
+def test_build_H_from_host_chunked(arch, M):
+    """The chunked, copy-overlapped build from pinned host X equals build_H."""
+    N, Q = 3001, 9
+    X, _, _ = inputs(N, Q, 1)
+    e = E(arch, 1, M, Q, 5)
+    Xd = torch.from_numpy(X).cuda()
+    H1 = e.build_H(Xd)
+    Xh = torch.from_numpy(X).pin_memory()
+    Xs = torch.empty_like(Xd)
+    H2 = torch.empty_like(H1)
+    e.build_H_from_host(Xh, Xs, H2, chunks=7)
+    torch.cuda.synchronize()
+    assert torch.equal(H1, H2)
+
+
 def test_empty_and_errors():
     from paper_1911_13252_b200 import ElmrnnError
     e = E("gru", 1, 8, 4, 1)

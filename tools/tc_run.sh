@@ -1,5 +1,7 @@
 #!/bin/bash
 set -o pipefail
-timeout 900 python tools/qr3.py 32 4 2>&1
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "wy_and_fold or solve_parity or virtual" 2>&1 | tail -2
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -6
+python -m paper_1911_13252_b200.build >/dev/null
+for wg in 0 1; do
+timeout 600 python bench.py --steps 3 --no-cpu-baseline --weight-grid $wg 2>&1 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('wg', $wg, 'value', round(d['value']), 'e2e', round(d['e2e']['value']), 'phases', {k: round(v,1) for k,v in d['config']['phases_ms'].items()}, 'roof', round(d['roofline']['achieved']), round(d['roofline']['frac'],3), 'clk', d['clocks'])"
+done
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -k "two_pass" 2>&1 | tail -1
