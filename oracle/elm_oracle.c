@@ -19,6 +19,11 @@
  *   S2.2.4 fully connected, P:125-127 (prose reading R9: all neurons, Q lags)
  *   S2.2.5 LSTM, P:128-142 ; S2.2.6 GRU, P:144-150 (dense U, reading R10/R11)
  *   S4.2   QR solve, P:327-328     : H = QR, z = Q^T Y, R beta = z
+ * Paper-literal per-cell variants (readings R9/R10):
+ *   LSTM / GRU with DIAGONAL recurrent weights u_g[j] (the only
+ *   structure consistent with Alg. 2's cell independence), and FC by the
+ *   letter of Eq. 8: own history scaled by
+ *   sum_l alpha[j,l,k].
  *
  * Readings R1..R25 are listed in DESIGN.md.  Everything is computed in fp64
  * from fp32 inputs and fp32 (or grid-rounded) weights widened exactly.
@@ -36,7 +41,8 @@
 #include <omp.h>
 #endif
 
-enum { ARCH_ELMAN = 0, ARCH_JORDAN, ARCH_NARMAX, ARCH_FC, ARCH_LSTM, ARCH_GRU };
+enum { ARCH_ELMAN = 0, ARCH_JORDAN, ARCH_NARMAX, ARCH_FC, ARCH_LSTM, ARCH_GRU,
+       ARCH_LSTM_DIAG, ARCH_GRU_DIAG, ARCH_FC_EQ8 };
 
 /* ------------------------------------------------------------------------ */
 /* Weights: counter-based generator (reading R1/R2).    */
@@ -103,6 +109,20 @@ static int64_t orc_block_info(int arch, int S, int M, int Q, int F, int R, int f
         if (block_id == 2) return (int64_t)M * F;
         if (block_id == 3) return (int64_t)M * R;
         return -1;
+    case ARCH_FC_EQ8:   /* same blocks as FC; alpha[j,l,k] = A[k-1][l][j]; no MMA */
+        if (block_id == 0) return (int64_t)S * M;
+        if (block_id == 1) return M;
+        if (block_id == 2) {
+            if (!unit) *scale = 1.0 / sqrt((double)M * (double)fc_lags);
+            return (int64_t)fc_lags * M * M;
+        }
+        return -1;
+    case ARCH_LSTM_DIAG:
+    case ARCH_GRU_DIAG: {   /* per gate: W_g [S][M], u_g [M] (diagonal, fan-in 1), b_g [M] */
+        int G = (arch == ARCH_LSTM_DIAG) ? 4 : 3;
+        if (block_id < 0 || block_id >= 3 * G) return -1;
+        return (block_id % 3 == 0) ? (int64_t)S * M : M;
+    }
     case ARCH_FC:
         if (block_id == 0) return (int64_t)S * M;
         if (block_id == 1) return M;
@@ -134,10 +154,10 @@ uint64_t orc_rng_u64(uint64_t z) { return orc_splitmix64(z); }
 
 int orc_num_blocks(int arch) {
     switch (arch) {
-    case ARCH_ELMAN: case ARCH_JORDAN: case ARCH_FC: return 3;
+    case ARCH_ELMAN: case ARCH_JORDAN: case ARCH_FC: case ARCH_FC_EQ8: return 3;
     case ARCH_NARMAX: return 4;
-    case ARCH_LSTM: return 12;
-    case ARCH_GRU: return 9;
+    case ARCH_LSTM: case ARCH_LSTM_DIAG: return 12;
+    case ARCH_GRU: case ARCH_GRU_DIAG: return 9;
     }
     return -1;
 }
@@ -313,13 +333,65 @@ static void orc_row_gru(const orc_net* n, const float* Xi, double* work /*[5M]*/
     for (int j = 0; j < M; ++j) Hrow[j] = h[j];
 }
 
+/* Eq. 8 by the letter:
+ *   a_j(t) = W[:,j].x(t) + b_j + sum_{k=1}^{min(t-1,L)} sum_{l=1}^{M} alpha[j,l,k] h_j(t-k)
+ * with alpha[j,l,k] = A[k-1][l][j] (the FC block).  Cell independent. */
+static void orc_row_fc_eq8(const orc_net* n, const float* Xi, double* hist /*[Q+1]*/, double* Hrow) {
+    const float *W = n->blk[0], *b = n->blk[1], *A = n->blk[2];
+    int M = n->M, L = n->fc_lags;
+    for (int j = 0; j < M; ++j) {
+        hist[0] = 0.0;
+        for (int t = 1; t <= n->Q; ++t) {
+            double a = orc_wx_b(W, b, Xi, n->S, M, t, j);
+            for (int k = 1; k <= t - 1 && k <= L; ++k)
+                for (int l = 0; l < M; ++l) a += (double)A[((int64_t)(k - 1) * M + l) * M + j] * hist[t - k];
+            hist[t] = orc_g(a, n->act);
+        }
+        Hrow[j] = hist[n->Q];
+    }
+}
+
+/* LSTM with diagonal recurrent weights: per neuron j, gates
+ * (o, c, lambda, in) = 0..3, a_g = W_g[:,j].x(t) + u_g[j] h_j(t-1) + b_g[j];
+ * c = sigma(a_lambda) c + sigma(a_in) tanh(a_c);  h = sigma(a_o) tanh(c). */
+static void orc_row_lstm_diag(const orc_net* n, const float* Xi, double* Hrow) {
+    for (int j = 0; j < n->M; ++j) {
+        double h = 0.0, c = 0.0;
+        for (int t = 1; t <= n->Q; ++t) {
+            double a[4];
+            for (int g = 0; g < 4; ++g)
+                a[g] = orc_wx_b(n->blk[3 * g], n->blk[3 * g + 2], Xi, n->S, n->M, t, j) +
+                       (double)n->blk[3 * g + 1][j] * h;
+            c = orc_sigmoid(a[2]) * c + orc_sigmoid(a[3]) * tanh(a[1]);
+            h = orc_sigmoid(a[0]) * tanh(c);
+        }
+        Hrow[j] = h;
+    }
+}
+
+/* GRU (Cho form, R11/R12) with diagonal recurrent weights: gates (z, r, f),
+ *   z = sigma(W_z x + u_z h + b_z), r = sigma(W_r x + u_r h + b_r),
+ *   n = tanh(W_f x + u_f (r h) + b_f), h = (1 - z) h + z n. */
+static void orc_row_gru_diag(const orc_net* n, const float* Xi, double* Hrow) {
+    for (int j = 0; j < n->M; ++j) {
+        double h = 0.0;
+        for (int t = 1; t <= n->Q; ++t) {
+            double z = orc_sigmoid(orc_wx_b(n->blk[0], n->blk[2], Xi, n->S, n->M, t, j) + (double)n->blk[1][j] * h);
+            double r = orc_sigmoid(orc_wx_b(n->blk[3], n->blk[5], Xi, n->S, n->M, t, j) + (double)n->blk[4][j] * h);
+            double nn = tanh(orc_wx_b(n->blk[6], n->blk[8], Xi, n->S, n->M, t, j) + (double)n->blk[7][j] * (r * h));
+            h = (1.0 - z) * h + z * nn;
+        }
+        Hrow[j] = h;
+    }
+}
+
 /* Alg. 1 line 2: H(Q) for every sample row; rows are independent
  * (the parallel decomposition of P:250), so an OpenMP row split gives
  * bitwise-identical results for any thread count. */
 int orc_build_H(int arch, int S, int M, int Q, int F, int R, int act, int fc_lags,
                 const float* const* blocks, const float* X, int64_t ldx,
                 const float* Yfb, int64_t ldy, int64_t N, double* H, int64_t ldh, int threads) {
-    if (arch < 0 || arch > ARCH_GRU || S < 1 || M < 1 || Q < 1) return -1;
+    if (arch < 0 || arch > ARCH_FC_EQ8 || S < 1 || M < 1 || Q < 1) return -1;
     orc_net net = { arch, S, M, Q, F, R, act, fc_lags, blocks };
     int64_t wlen = (int64_t)(Q + 1) * M + 8 * M + Q + 8;
 #ifdef _OPENMP
@@ -341,6 +413,9 @@ int orc_build_H(int arch, int S, int M, int Q, int F, int R, int act, int fc_lag
             case ARCH_FC: orc_row_fc(&net, Xi, work, Hrow); break;
             case ARCH_LSTM: orc_row_lstm(&net, Xi, work, Hrow); break;
             case ARCH_GRU: orc_row_gru(&net, Xi, work, Hrow); break;
+            case ARCH_LSTM_DIAG: orc_row_lstm_diag(&net, Xi, Hrow); break;
+            case ARCH_GRU_DIAG: orc_row_gru_diag(&net, Xi, Hrow); break;
+            case ARCH_FC_EQ8: orc_row_fc_eq8(&net, Xi, work, Hrow); break;
             }
         }
         free(work);

@@ -26,8 +26,12 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "elm_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-ARCHS = {"elman": 0, "jordan": 1, "narmax": 2, "fc": 3, "lstm": 4, "gru": 5}
-GATES = {"lstm": ("o", "c", "lambda", "in"), "gru": ("z", "r", "f")}
+ARCHS = {"elman": 0, "jordan": 1, "narmax": 2, "fc": 3, "lstm": 4, "gru": 5,
+         # paper-literal per-cell variants: diagonal-U LSTM/GRU
+         # and FC by the letter of Eq. 8
+         "lstm_diag": 6, "gru_diag": 7, "fc_eq8": 8}
+GATES = {"lstm": ("o", "c", "lambda", "in"), "gru": ("z", "r", "f"),
+         "lstm_diag": ("o", "c", "lambda", "in"), "gru_diag": ("z", "r", "f")}
 
 
 def build(force: bool = False) -> str:
@@ -119,8 +123,10 @@ def block_shape(net: Net, block_id: int):
         return [(S, M), (M,), (M, Q)][block_id]
     if a == "narmax":
         return [(S, M), (M,), (M, F), (M, R)][block_id]
-    if a == "fc":
+    if a in ("fc", "fc_eq8"):
         return [(S, M), (M,), (L, M, M)][block_id]
+    if a in ("lstm_diag", "gru_diag"):
+        return [(S, M), (M,), (M,)][block_id % 3]
     return [(S, M), (M, M), (M,)][block_id % 3]
 
 
