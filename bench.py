@@ -42,13 +42,20 @@ WORKLOAD_NAMES = {
     "C3fc": "C3 fully connected (Q lags) N=1M Q=30 M=128 d=4, sinusoid mixture",
     "C3gru": "C3 GRU N=1M Q=30 M=128 d=4, sinusoid mixture",
     "C4": "C4 LSTM N=4M Q=50 M=256 d=1, Mackey-Glass + noise",
+    "C3lstm_diag": "C3 shape, LSTM with diagonal U (paper-literal per-cell) N=1M Q=30 M=128 d=4",
+    "C3gru_diag": "C3 shape, GRU with diagonal U (paper-literal per-cell) N=1M Q=30 M=128 d=4",
+    "C3fc_eq8": "C3 shape, fully connected by the letter of Eq. 8 (per-cell) N=1M Q=30 M=128 d=4",
 }
 
 
 def algorithmic_flops_per_sample(arch: str, S: int, M: int, Q: int) -> float:
     """Minimal exact work for H(Q), FMA = 2."""
-    if arch == "elman":
+    if arch in ("elman", "fc_eq8"):   # Eq. 8 after the per-lag column sums (init) is Eq. 5
         return 2 * S * M * Q + M * Q * (Q - 1)
+    if arch == "lstm_diag":
+        return Q * M * (8 * S + 8 + 6)
+    if arch == "gru_diag":
+        return Q * M * (6 * S + 6 + 5)
     if arch in ("jordan", "narmax"):
         return 2 * S * M + 2 * M * (Q - 1)
     if arch == "fc":
@@ -344,7 +351,7 @@ def main():
     peaks, src = load_peaks()
     flops = algorithmic_flops_per_sample(c["arch"], c["S"], c["M"], c["Q"]) * N_local
     path = model.path
-    if c["arch"] in ("jordan", "narmax", "elman"):
+    if c["arch"] in ("jordan", "narmax", "elman", "fc_eq8"):
         bound, unit = "hbm", "GB/s"
         achieved = algorithmic_bytes_per_sample(c["arch"], c["S"], c["M"], c["Q"]) * N_local / (build_ms / 1e3) / 1e9
         peak = peaks["hbm_gbs"]

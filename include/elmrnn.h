@@ -44,14 +44,20 @@ extern "C" {
 
 typedef struct elmrnn* elmrnn_t;
 
-/* The six architectures of S2.2. */
+/* The six architectures of S2.2, plus three paper-literal per-cell variants. */
 typedef enum {
     ELMRNN_ELMAN = 0,   /* Eq. 5: self recurrence over Q lags            */
     ELMRNN_JORDAN = 1,  /* Eq. 6: output feedback, teacher forced (R7)   */
     ELMRNN_NARMAX = 2,  /* Eq. 7: output (+ error, e == 0) feedback (R8) */
     ELMRNN_FC = 3,      /* S2.2.4: all neurons, Q lags (prose, R9)       */
     ELMRNN_LSTM = 4,    /* S2.2.5: dense U, gates (o, c, lambda, in)     */
-    ELMRNN_GRU = 5      /* S2.2.6: dense U, Cho form, gates (z, r, f)    */
+    ELMRNN_GRU = 5,     /* S2.2.6: dense U, Cho form, gates (z, r, f)    */
+    /* Paper-literal per-cell variants: cell independent, as
+     * Alg. 2's thread decomposition and Table 2 assume. */
+    ELMRNN_LSTM_DIAG = 6, /* S2.2.5 with diagonal recurrent weights u_g[j] */
+    ELMRNN_GRU_DIAG = 7,  /* S2.2.6 (Cho) with diagonal recurrent weights u_g[j]        */
+    ELMRNN_FC_EQ8 = 8     /* Eq. 8 by the letter: own history scaled by
+                           * sum_l alpha[j,l,k]                         */
 } elmrnn_arch;
 
 typedef enum {

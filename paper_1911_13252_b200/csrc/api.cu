@@ -39,7 +39,7 @@ elmrnn_status elmrnn_init_ex(elmrnn_t* out, int arch, int d, int M, int Q, uint6
     elmrnn_opts o;
     elmrnn_opts_default(&o);
     if (opts) o = *opts;
-    if (arch < ELMRNN_ELMAN || arch > ELMRNN_GRU) return fail(nullptr, ELMRNN_ERR_ARG, "arch out of range");
+    if (arch < ELMRNN_ELMAN || arch > ELMRNN_FC_EQ8) return fail(nullptr, ELMRNN_ERR_ARG, "arch out of range");
     if (d < 1 || M < 1 || Q < 1) return fail(nullptr, ELMRNN_ERR_ARG, "d, M and Q must be >= 1");
     if (o.F < 0) o.F = Q;
     if (o.R < 0) o.R = Q;
@@ -47,7 +47,7 @@ elmrnn_status elmrnn_init_ex(elmrnn_t* out, int arch, int d, int M, int Q, uint6
     if (o.act < 0 || o.act > 1 || o.rec_scale < 0 || o.rec_scale > 1 || o.weight_grid < 0 || o.weight_grid > 2 ||
         o.force_path < 0 || o.force_path > 2 || o.fc_lags < 1)
         return fail(nullptr, ELMRNN_ERR_ARG, "invalid option value");
-    if (arch == ELMRNN_ELMAN && !elman_supported(Q))
+    if ((arch == ELMRNN_ELMAN || arch == ELMRNN_FC_EQ8) && !elman_supported(Q))
         return fail(nullptr, ELMRNN_ERR_UNSUPPORTED, "Elman supports Q <= 128");
     if (M > 1023) return fail(nullptr, ELMRNN_ERR_UNSUPPORTED, "M <= 1023 (TSQR: one thread per column of [H|Y])");
 
@@ -68,6 +68,8 @@ elmrnn_status elmrnn_init_ex(elmrnn_t* out, int arch, int d, int M, int Q, uint6
     case ELMRNN_ELMAN: case ELMRNN_JORDAN: h->rec_len = (int64_t)Q * M; break;
     case ELMRNN_NARMAX: h->rec_len = (int64_t)(o.F > 0 ? o.F : 1) * M; break;
     case ELMRNN_FC: h->rec_len = (int64_t)o.fc_lags * M * M; break;
+    case ELMRNN_FC_EQ8: h->rec_len = (int64_t)Q * M; break;
+    case ELMRNN_LSTM_DIAG: case ELMRNN_GRU_DIAG: h->rec_len = GM; break;
     default: h->rec_len = (int64_t)M * GM; break;
     }
     if ((e = cudaMalloc(&h->W, sizeof(float) * d * GM)) || (e = cudaMalloc(&h->b, sizeof(float) * GM)) ||
@@ -101,7 +103,8 @@ static elmrnn_status build_impl(elmrnn* h, const float* X, int64_t ldx, const fl
                                 float* H, int64_t ldh) {
     cudaError_t e;
     switch (h->arch) {
-    case ELMRNN_ELMAN: e = launch_elman(h, X, ldx, N, H, ldh); break;
+    case ELMRNN_ELMAN: case ELMRNN_FC_EQ8: e = launch_elman(h, X, ldx, N, H, ldh); break;
+    case ELMRNN_LSTM_DIAG: case ELMRNN_GRU_DIAG: e = launch_diag_gated(h, X, ldx, N, H, ldh); break;
     case ELMRNN_JORDAN: case ELMRNN_NARMAX: e = launch_teacher_forced(h, X, ldx, Yfb, ldy, N, H, ldh); break;
     default:
         e = h->path == 2 ? launch_dense_tc(h, X, ldx, N, H, ldh) : launch_dense_fma(h, X, ldx, N, H, ldh);

@@ -11,8 +11,11 @@
 namespace elm {
 
 constexpr int kArchElman = 0, kArchJordan = 1, kArchNarmax = 2, kArchFC = 3, kArchLSTM = 4, kArchGRU = 5;
+constexpr int kArchLSTMDiag = 6, kArchGRUDiag = 7, kArchFCEq8 = 8;   // paper-literal per-cell variants
 
-inline int gates_of(int arch) { return arch == kArchLSTM ? 4 : (arch == kArchGRU ? 3 : 1); }
+inline int gates_of(int arch) {
+    return (arch == kArchLSTM || arch == kArchLSTMDiag) ? 4 : ((arch == kArchGRU || arch == kArchGRUDiag) ? 3 : 1);
+}
 
 // Device-side solve diagnostics (copied to the host struct on request).
 struct SolveDev {
@@ -69,6 +72,7 @@ int num_blocks(int arch);
 
 // ---- H builders --------------------------------------------------------------
 cudaError_t launch_elman(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
+cudaError_t launch_diag_gated(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
 cudaError_t launch_teacher_forced(elmrnn* h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy,
                                   int64_t N, float* H, int64_t ldh);
 cudaError_t launch_dense_fma(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);

@@ -9,6 +9,7 @@
 // tensor-core contraction (FC A, LSTM/GRU U) may be rounded to the fp16 grid
 // (RNE) or the tf32 grid (RNA) (opts.weight_grid).  The kernel writes straight
 // into the packed device layouts the builders read.
+#include <algorithm>
 #include <cmath>
 
 #include <cuda_fp16.h>
@@ -55,12 +56,24 @@ __global__ void k_gen_block(uint64_t key, double scale, int grid, int64_t rows, 
     }
 }
 
+// alphaT[k][j] = sum_l A[k][l][j] for k < min(L, Q), 0 otherwise (A logical [L][M][M])
+__global__ void k_colsum_lags(const float* __restrict__ A, int M, int L, int Q, float* __restrict__ alT) {
+    const int64_t n = (int64_t)Q * M;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(e / M), j = (int)(e % M);
+        double s = 0.0;
+        if (k < L)
+            for (int l = 0; l < M; ++l) s += (double)A[((int64_t)k * M + l) * M + j];
+        alT[e] = (float)s;
+    }
+}
+
 int num_blocks(int arch) {
     switch (arch) {
-    case kArchElman: case kArchJordan: case kArchFC: return 3;
+    case kArchElman: case kArchJordan: case kArchFC: case kArchFCEq8: return 3;
     case kArchNarmax: return 4;
-    case kArchLSTM: return 12;
-    case kArchGRU: return 9;
+    case kArchLSTM: case kArchLSTMDiag: return 12;
+    case kArchGRU: case kArchGRUDiag: return 9;
     }
     return -1;
 }
@@ -96,6 +109,20 @@ static bool block_desc(const elmrnn* h, int id, int64_t* rows, int64_t* cols, do
             return true;
         }
         return false;
+    case kArchFCEq8:   // the FC blocks; per-cell use only (no MMA, no grid rounding)
+        if (id == 0) { *rows = S; *cols = M; return true; }
+        if (id == 1) { *rows = 1; *cols = M; return true; }
+        if (id == 2) {
+            *rows = (int64_t)h->fc_lags * M; *cols = M;
+            if (!unit) *scale = 1.0 / std::sqrt((double)M * (double)h->fc_lags);
+            return true;
+        }
+        return false;
+    case kArchLSTMDiag: case kArchGRUDiag:   // per gate W [S][M], u [M] (fan-in 1), b [M]
+        if (id < 0 || id >= 3 * h->G) return false;
+        if (id % 3 == 0) { *rows = S; *cols = M; return true; }
+        *rows = 1; *cols = M;
+        return true;
     case kArchLSTM: case kArchGRU: {
         if (id < 0 || id >= 3 * h->G) return false;
         int kind = id % 3;
@@ -137,7 +164,8 @@ static cudaError_t launch_gen(elmrnn* h, int id, float* dst, int64_t ld, int64_t
 //   W   [S][G*M]   (gate g in columns g*M .. g*M+M-1)
 //   b   [G*M]
 //   rec Elman/Jordan alpha^T [Q][M]; NARMAX W'^T [F][M]; FC A [L*M][M];
-//       LSTM/GRU U_cat [M][G*M]
+//       LSTM/GRU U_cat [M][G*M]; diagonal LSTM/GRU u [G*M];
+//       FC by Eq. 8: alpha^T [Q][M] with alpha[k][j] = sum_l A[k][l][j]
 cudaError_t gen_weights(elmrnn* h) {
     cudaError_t e;
     const int M = h->M, GM = h->G * h->M;
@@ -154,6 +182,30 @@ cudaError_t gen_weights(elmrnn* h) {
         if ((e = launch_gen(h, 0, h->W, M, 0, 0))) return e;
         if ((e = launch_gen(h, 1, h->b, M, 0, 0))) return e;
         return launch_gen(h, 2, h->rec, M, 0, 0);
+    case kArchFCEq8: {
+        // Eq. 8: sum_l alpha[j,l,k] h_j(t-k) = (sum_l A[k-1][l][j]) h_j(t-k): the
+        // per-lag column sums are formed once here (init, untimed) into alpha^T [Q][M]
+        if ((e = launch_gen(h, 0, h->W, M, 0, 0))) return e;
+        if ((e = launch_gen(h, 1, h->b, M, 0, 0))) return e;
+        const int L = h->fc_lags;
+        float* A = nullptr;
+        if ((e = cudaMalloc(&A, sizeof(float) * (size_t)L * M * M))) return e;
+        if ((e = launch_gen(h, 2, A, M, 0, 0))) { cudaFree(A); return e; }
+        const int64_t n = (int64_t)h->Q * M;
+        k_colsum_lags<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, h->stream>>>(A, M, L, h->Q, h->rec);
+        h->launches++;
+        e = cudaGetLastError();
+        cudaStreamSynchronize(h->stream);
+        cudaFree(A);
+        return e;
+    }
+    case kArchLSTMDiag: case kArchGRUDiag:   // W [S][G*M], u [G*M] (in rec), b [G*M]
+        for (int g = 0; g < h->G; ++g) {
+            if ((e = launch_gen(h, 3 * g, h->W, GM, (int64_t)g * M, 0))) return e;
+            if ((e = launch_gen(h, 3 * g + 1, h->rec, GM, (int64_t)g * M, 0))) return e;
+            if ((e = launch_gen(h, 3 * g + 2, h->b, GM, (int64_t)g * M, 0))) return e;
+        }
+        return cudaSuccess;
     case kArchLSTM: case kArchGRU:
         for (int g = 0; g < h->G; ++g) {
             if ((e = launch_gen(h, 3 * g, h->W, GM, (int64_t)g * M, 0))) return e;

@@ -17,7 +17,8 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ELMRNN_LIB") or os.path.join(_HERE, "libelmrnn.so")   # override: testing aid
 
-ARCHS = {"elman": 0, "jordan": 1, "narmax": 2, "fc": 3, "lstm": 4, "gru": 5}
+ARCHS = {"elman": 0, "jordan": 1, "narmax": 2, "fc": 3, "lstm": 4, "gru": 5,
+         "lstm_diag": 6, "gru_diag": 7, "fc_eq8": 8}   # paper-literal per-cell variants (elmrnn.h)
 STATUS = {0: "OK", 1: "WARN_RIDGE", -1: "ERR_ARG", -2: "ERR_SHAPE", -3: "ERR_UNDERDETERMINED",
           -4: "ERR_NONFINITE", -5: "ERR_UNSUPPORTED", -6: "ERR_CUDA", -7: "ERR_OOM"}
 

@@ -116,6 +116,10 @@ CONFIGS = {
     "C3fc": dict(arch="fc", series="sin4", N=1_000_000, Q=30, S=4, M=128, noise=0.0),
     "C3gru": dict(arch="gru", series="sin4", N=1_000_000, Q=30, S=4, M=128, noise=0.0),
     "C4": dict(arch="lstm", series="mg", N=4_000_000, Q=50, S=1, M=256, noise=0.01),
+    # paper-literal per-cell variants at the C3 shape
+    "C3lstm_diag": dict(arch="lstm_diag", series="sin4", N=1_000_000, Q=30, S=4, M=128, noise=0.0),
+    "C3gru_diag": dict(arch="gru_diag", series="sin4", N=1_000_000, Q=30, S=4, M=128, noise=0.0),
+    "C3fc_eq8": dict(arch="fc_eq8", series="sin4", N=1_000_000, Q=30, S=4, M=128, noise=0.0),
 }
 
 

@@ -60,7 +60,8 @@ def gpu_H(arch, S, M, Q, seed, X, Yfb=None, **o):
 @pytest.mark.parametrize("arch,M,Q,o", [
     ("elman", 20, 10, {}), ("jordan", 7, 5, {}), ("narmax", 9, 6, {"F": 3, "R": 2}), ("fc", 12, 4, {}),
     ("fc", 12, 4, {"fc_lags": 1, "weight_grid": 1}), ("lstm", 33, 3, {}), ("lstm", 16, 3, {"weight_grid": 1}),
-    ("gru", 40, 3, {"weight_grid": 2}), ("gru", 8, 2, {"rec_scale": 1})])
+    ("gru", 40, 3, {"weight_grid": 2}), ("gru", 8, 2, {"rec_scale": 1}),
+    ("lstm_diag", 21, 4, {}), ("gru_diag", 17, 3, {"rec_scale": 1}), ("fc_eq8", 12, 5, {"fc_lags": 3})])
 def test_weights_bitwise(arch, M, Q, o):
     S = 3
     e = E(arch, S, M, Q, 12345, **o)
@@ -93,6 +94,15 @@ GRID = [
     ("lstm", 301, 4, 50, 10, {}, False),
     ("lstm", 129, 1, 3, 1, {}, False),
     ("lstm", 64, 1, 32, 100, {"weight_grid": 1}, False),
+    # paper-literal per-cell variants
+    ("lstm_diag", 300, 4, 128, 30, {}, False),      # C3 shape
+    ("lstm_diag", 257, 1, 50, 100, {}, False),
+    ("lstm_diag", 99, 7, 3, 1, {}, False),           # S > 4: runtime-S loop
+    ("gru_diag", 300, 4, 128, 30, {}, False),
+    ("gru_diag", 129, 2, 33, 50, {"rec_scale": 1}, False),
+    ("fc_eq8", 300, 4, 128, 30, {}, False),
+    ("fc_eq8", 200, 1, 20, 12, {"fc_lags": 3, "act": 1}, False),
+    ("fc_eq8", 50, 1, 1, 9, {}, False),
 ]
 
 
@@ -222,7 +232,9 @@ def solve_tolerances(Hg, Ho, Y, b_ref, i_ref):
 SOLVE_CASES = [("elman", 1000, 1, 20, 10, "mg", 0.0), ("jordan", 5000, 1, 64, 20, "ar5", 0.0),
                ("narmax", 5000, 1, 64, 20, "ar5", 0.0), ("gru", 3000, 4, 128, 30, "sin4", 0.0),
                ("fc", 2000, 4, 128, 30, "sin4", 0.0), ("lstm", 8000, 1, 256, 50, "mg", 0.01),
-               ("lstm", 20000, 1, 511, 5, "mg", 0.01)]
+               ("lstm", 20000, 1, 511, 5, "mg", 0.01),
+               ("lstm_diag", 3000, 4, 128, 30, "sin4", 0.0), ("gru_diag", 3000, 4, 128, 30, "sin4", 0.0),
+               ("fc_eq8", 3000, 4, 128, 30, "sin4", 0.0)]
 
 
 @pytest.mark.parametrize("arch,N,S,M,Q,kind,noise", SOLVE_CASES)
