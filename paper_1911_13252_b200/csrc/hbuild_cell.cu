@@ -37,14 +37,37 @@ __global__ void __launch_bounds__(256) k_elman(const float* __restrict__ X, int6
     const T bj = __ldg(b + j);
     T h[QMAX];
     T last = 0;
+    T w4[4];   // W[:,j] for S <= 4 (larger S re-reads from L1)
+#pragma unroll
+    for (int s = 0; s < 4; ++s) w4[s] = s < S ? (T)__ldg(W + (int64_t)s * M + j) : (T)0;
 #pragma unroll
     for (int t = 0; t < QMAX; ++t) {
         if (t < Q) {
             T a = bj;
-            for (int s = 0; s < S; ++s)
-                a = fma((T)__ldg(W + (int64_t)s * M + j), (T)__ldg(xi + (int64_t)t * S + s), a);
+            if (S <= 4) {
 #pragma unroll
-            for (int k = 1; k <= t; ++k) a = fma(al[k - 1], h[t - k], a);
+                for (int s = 0; s < 4; ++s)
+                    if (s < S) a = fma(w4[s], (T)__ldg(xi + (int64_t)t * S + s), a);
+            } else {
+                for (int s = 0; s < S; ++s)
+                    a = fma((T)__ldg(W + (int64_t)s * M + j), (T)__ldg(xi + (int64_t)t * S + s), a);
+            }
+            if constexpr (QMAX <= 32) {
+                // lag sum in 4 independent partial sums (shortens the dependent chain 4x)
+                T p1 = 0, p2 = 0, p3 = 0;
+#pragma unroll
+                for (int k = 1; k <= t; ++k) {
+                    const T v = h[t - k];
+                    if ((k & 3) == 1) a = fma(al[k - 1], v, a);
+                    else if ((k & 3) == 2) p1 = fma(al[k - 1], v, p1);
+                    else if ((k & 3) == 3) p2 = fma(al[k - 1], v, p2);
+                    else p3 = fma(al[k - 1], v, p3);
+                }
+                a = (a + p1) + (p2 + p3);
+            } else {
+#pragma unroll
+                for (int k = 1; k <= t; ++k) a = fma(al[k - 1], h[t - k], a);
+            }
             h[t] = act_T(a, act);
             last = h[t];
         }
