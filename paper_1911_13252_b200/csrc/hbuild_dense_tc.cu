@@ -59,6 +59,7 @@ struct TcParams {
     const uint8_t* Uimg;   // [NCH][KS][hi|lo][16 KB] pre-swizzled images
     int S, Q;
     int two_pass;          // 1: U on the fp16 grid (weight_grid = 1), U_lo = 0 -> hi.hi + lo.hi only
+    int debug_no_u;        // ELMRNN_DEBUG_NO_U: skip U streaming after step 0 (timing experiment only)
     int64_t ntiles;
     float k_sig, k_tanh;   // -log2(e) 2^-sigma, 2 log2(e) 2^-sigma
     unsigned long long* trace;   // optional event trace of CTA 0 (ELMRNN_TRACE), else null
@@ -126,7 +127,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
     uint64_t* acc_full = bars + 2 * kTcStages;   // [2]
     uint64_t* acc_empty = acc_full + 2;          // [2]
     uint64_t* a_ready = acc_empty + 2;           // [KS]: K-slice ks of A = h(t-1) is in TMEM
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_ready + C::KS);
+    uint64_t* a_free = a_ready + C::KS;          // [KS]: the last chunk's MMAs no longer read A slice ks
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_free + C::KS);
     uint32_t* trace_cnt = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -140,6 +142,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
             ptx::mbar_init(acc_empty + i, kTcEpiWarps);
         }
         for (int i = 0; i < C::KS; ++i) ptx::mbar_init(a_ready + i, kTcEpiWarps);
+        for (int i = 0; i < C::KS; ++i) ptx::mbar_init(a_free + i, 1);
         *trace_cnt = 0;
         ptx::fence_mbar_init();
     }
@@ -163,8 +166,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
             for (int c = 0; c < C::NCH * C::KS; ++c) {
                 ptx::mbar_wait(empty + st, ph ^ 1);
                 if (ptx::elect_one()) {
-                    ptx::mbar_arrive_expect_tx(full + st, bytes);
-                    ptx::bulk_g2s(stages + st * kTcStageBytes, p.Uimg + (size_t)c * kTcStageBytes, bytes, full + st);
+                    if (p.debug_no_u && s > 0) {   // timing experiment only (results invalid)
+                        ptx::mbar_arrive(full + st);
+                    } else {
+                        ptx::mbar_arrive_expect_tx(full + st, bytes);
+                        ptx::bulk_g2s(stages + st * kTcStageBytes, p.Uimg + (size_t)c * kTcStageBytes, bytes,
+                                      full + st);
+                    }
                 }
                 __syncwarp();
                 if (++st == kTcStages) { st = 0; ph ^= 1; }
@@ -197,16 +205,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                     const uint64_t dbl = dbh + (uint64_t)(kTcSliceBytes >> 4);
                     const uint32_t tah = a_hi + ks * 32, tal = a_lo + ks * 32;
                     if (ptx::elect_one()) {
+                        // passes ordered so the two MMAs reading the same B_hi tile are adjacent
                         ptx::mma_f16_ts(d, tah, dbh, idesc, ks != 0);
-                        if (!two) ptx::mma_f16_ts(d, tah, dbl, idesc, 1);
                         ptx::mma_f16_ts(d, tal, dbh, idesc, 1);
+                        if (!two) ptx::mma_f16_ts(d, tah, dbl, idesc, 1);
 #pragma unroll
                         for (int kk = 1; kk < 4; ++kk) {
                             ptx::mma_f16_ts(d, tah + kk * 8, dbh + 2 * kk, idesc, 1);
-                            if (!two) ptx::mma_f16_ts(d, tah + kk * 8, dbl + 2 * kk, idesc, 1);
                             ptx::mma_f16_ts(d, tal + kk * 8, dbh + 2 * kk, idesc, 1);
+                            if (!two) ptx::mma_f16_ts(d, tah + kk * 8, dbl + 2 * kk, idesc, 1);
                         }
                         ptx::mma_commit(empty + st);                  // frees the U stage
+                        // last chunk of the step: A slice ks is free for h(t) once these MMAs retire
+                        if (n == C::NCH - 1 && ks < C::KS - 1) ptx::mma_commit(a_free + ks);
                         if (ks == C::KS - 1) ptx::mma_commit(acc_full + ach);   // chunk accumulator ready
                     }
                     __syncwarp();
@@ -226,7 +237,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
         const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
         const float kS = p.k_sig, kT = p.k_tanh;     // -log2e 2^-sigma, 2 log2e 2^-sigma
         float c[C::NCH * 8];                         // c(t) of neurons n*32 + 8u + 0..7
-        uint32_t ach = 0, aph = 0;
+        uint32_t ach = 0, aph = 0, afph = 0;
         uint32_t* my_stg = stg + (size_t)e * C::ITEMS * 32 + lane;   // [item][lane]
         {   // h(0) = 0 for the first tile
             const uint32_t z[4] = {0u, 0u, 0u, 0u};
@@ -275,6 +286,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                     xs[s] = (valid && s < p.S) ? __ldg(xrow + (int64_t)(t - 1) * p.S + s) : 0.0f;
 #pragma unroll
                 for (int n = 0; n < C::NCH; ++n) {
+                    if (n == C::NCH - 1) {
+                        // h(t) slices 0..KS-2 (chunks 0..NCH-3) are staged: move each into
+                        // the TMEM A operand as soon as the last chunk's MMAs have read the
+                        // old one, so step t+1's first MMAs overlap this chunk's epilogue
+                        for (int ks = 0; ks < C::KS - 1; ++ks) {
+                            ptx::mbar_wait(a_free + ks, afph);
+                            ptx::tc_fence_after();
+                            publish(ks, ks + 1, t == p.Q);
+                        }
+                        afph ^= 1;
+                    }
                     ptx::mbar_wait(acc_full + ach, aph);
                     ptx::tc_fence_after();
                     if (e == 0 && lane == 0) trace_ev(p, trace_cnt, 4, t, n);
@@ -285,15 +307,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(acc_empty + ach);   // accumulator drained
-                    // The last chunk's accumulator implies every MMA of step t is done:
-                    // release K-slices 0..KS-2 of h(t) now, so step t+1's first MMAs
-                    // overlap this chunk's epilogue (its own slice follows below).
-                    if (n == C::NCH - 1) publish(0, C::KS - 1, t == p.Q);
                     float hv[8];
                     // MUFU budget: 5 ex2 + 1.25 rcp per element.  The four gate
                     // denominators of a neuron share one reciprocal (1/a = bcd/(abcd)),
                     // as do the tanh(c) denominators of 4 neurons; exp2 arguments are
-                    // clamped to +-30 so the products stay finite (sigma(20.8) = 1 - 9e-10).
+                    // clamped at +30 so the products stay finite (sigma(20.8) = 1 - 9e-10;
+                    // a very negative argument gives d = 1 exactly, no clamp needed).
 #pragma unroll
                     for (int g4 = 0; g4 < 2; ++g4) {
                         float so[4], dc[4];
@@ -301,18 +320,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                         for (int nb = 0; nb < 4; ++nb) {
                             const int j = n * 32 + 8 * u + 4 * g4 + nb;
                             const float* w = p.wb + j * (4 * (SS + 1));   // [gate][b, W_0..W_{S-1}]
-                            float pre[4];
+                            // exp2 argument k_g (acc 2^-sigma + b + x W): k_g is folded into
+                            // W|b on the host, so it is FFMA(k 2^-sigma, acc, b') + x W'
+                            float arg[4];
 #pragma unroll
                             for (int g = 0; g < 4; ++g) {
-                                float v = a[g4][nb * 4 + g] + w[g * (SS + 1)];
+                                float v = fmaf(g == 1 ? kT : kS, a[g4][nb * 4 + g], w[g * (SS + 1)]);
 #pragma unroll
                                 for (int s = 0; s < SS; ++s) v = fmaf(xs[s], w[g * (SS + 1) + 1 + s], v);
-                                pre[g] = v;
+                                arg[g] = fminf(v, 30.0f);   // only large positive arguments can overflow
                             }
-                            const float d0 = 1.0f + ex2_approx(clamp30(kS * pre[0]));   // o
-                            const float d1 = 1.0f + ex2_approx(clamp30(kT * pre[1]));   // c~ (tanh)
-                            const float d2 = 1.0f + ex2_approx(clamp30(kS * pre[2]));   // lambda
-                            const float d3 = 1.0f + ex2_approx(clamp30(kS * pre[3]));   // in
+                            const float d0 = 1.0f + ex2_approx(arg[0]);   // o
+                            const float d1 = 1.0f + ex2_approx(arg[1]);   // c~ (tanh)
+                            const float d2 = 1.0f + ex2_approx(arg[2]);   // lambda
+                            const float d3 = 1.0f + ex2_approx(arg[3]);   // in
                             const float p01 = d0 * d1, p23 = d2 * d3;
                             const float rr = rcp_approx(p01 * p23);
                             const float r01 = rr * p23, r23 = rr * p01;
@@ -322,7 +343,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                             const int ci = n * 8 + 4 * g4 + nb;
                             const float cn = fmaf(sl, c[ci], si * tc);
                             c[ci] = cn;
-                            dc[nb] = 1.0f + ex2_approx(clamp30(2.8853900817779268f * cn));
+                            dc[nb] = 1.0f + ex2_approx(fminf(2.8853900817779268f * cn, 30.0f));
                         }
                         const float p01 = dc[0] * dc[1], p23 = dc[2] * dc[3];
                         const float rr = rcp_approx(p01 * p23);
@@ -399,6 +420,7 @@ cudaError_t launch_lstm_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, fl
     p.Uimg = static_cast<const uint8_t*>(h->tc_ops);
     p.S = h->S; p.Q = h->Q;
     p.two_pass = h->weight_grid == 1;
+    p.debug_no_u = std::getenv("ELMRNN_DEBUG_NO_U") != nullptr;
     p.ntiles = (N + kTcRows - 1) / kTcRows;
     p.k_sig = -1.4426950408889634f * h->tc_inv_scale;
     p.k_tanh = 2.8853900817779268f * h->tc_inv_scale;
@@ -469,12 +491,15 @@ cudaError_t tc_prepare(elmrnn* h) {
     if ((e = cudaMemcpyAsync(W.data(), h->W, sizeof(float) * S * GM, cudaMemcpyDeviceToHost, h->stream))) return e;
     if ((e = cudaMemcpyAsync(b.data(), h->b, sizeof(float) * GM, cudaMemcpyDeviceToHost, h->stream))) return e;
     if ((e = cudaStreamSynchronize(h->stream))) return e;
+    // [j][gate][b, W_0..W_{S-1}] x k_g with k_g = -log2(e) (sigmoid gates o, lambda, in)
+    // or 2 log2(e) (tanh gate c~): the epilogue's exp2 argument is k_g pre-activation
     h->tc_wb.assign((size_t)M * 4 * (SP + 1), 0.0f);
     for (int j = 0; j < M; ++j)
         for (int g = 0; g < 4; ++g) {
+            const double kg = g == 1 ? 2.8853900817779268 : -1.4426950408889634;
             float* d = h->tc_wb.data() + ((size_t)j * 4 + g) * (SP + 1);
-            d[0] = b[g * M + j] * scale;
-            for (int s2 = 0; s2 < S; ++s2) d[1 + s2] = W[(size_t)s2 * GM + g * M + j] * scale;
+            d[0] = (float)(kg * b[g * M + j]);
+            for (int s2 = 0; s2 < S; ++s2) d[1 + s2] = (float)(kg * W[(size_t)s2 * GM + g * M + j]);
         }
     int64_t total = (int64_t)(M / 32) * (M / 64) * 128 * 64;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);

@@ -241,15 +241,16 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                     for (int i = 0; i < 16; ++i) {
                         const int j = 64 * c + 16 * u + i;
                         const float* w = p.wb + j * (3 * (SS + 1));
-                        float pz = a[i >> 3][(i & 7) * 2] + w[0];
-                        float pr = a[i >> 3][(i & 7) * 2 + 1] + w[SS + 1];
+                        // exp2 arguments k_g pre-activation; k_g folded into W|b on the host
+                        float pz = fmaf(kS, a[i >> 3][(i & 7) * 2], w[0]);
+                        float pr = fmaf(kS, a[i >> 3][(i & 7) * 2 + 1], w[SS + 1]);
 #pragma unroll
                         for (int s = 0; s < SS; ++s) {
                             pz = fmaf(xs[s], w[1 + s], pz);
                             pr = fmaf(xs[s], w[SS + 2 + s], pr);
                         }
-                        const float dz = 1.0f + ex2_approx(clamp30g(kS * pz));
-                        const float dr = 1.0f + ex2_approx(clamp30g(kS * pr));
+                        const float dz = 1.0f + ex2_approx(fminf(pz, 30.0f));
+                        const float dr = 1.0f + ex2_approx(fminf(pr, 30.0f));
                         const float rr = rcp_approx(dz * dr);
                         my_z[(c * 16 + i) * 32] = dr * rr;            // z = 1/dz
                         rh[i] = (dz * rr) * h[c * 16 + i];            // r o h(t-1)
@@ -284,10 +285,10 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                         for (int k2 = 0; k2 < 2; ++k2) {
                             const int j = 64 * c + 16 * u + i + k2;
                             const float* w = p.wb + j * (3 * (SS + 1)) + 2 * (SS + 1);
-                            float pn = a2[c][i + k2] + w[0];
+                            float pn = fmaf(kT, a2[c][i + k2], w[0]);
 #pragma unroll
                             for (int s = 0; s < SS; ++s) pn = fmaf(xs[s], w[1 + s], pn);
-                            dn[k2] = 1.0f + ex2_approx(clamp30g(kT * pn));
+                            dn[k2] = 1.0f + ex2_approx(fminf(pn, 30.0f));
                         }
                         const float rr = rcp_approx(dn[0] * dn[1]);
                         const float n0 = fmaf(-2.0f, dn[1] * rr, 1.0f), n1 = fmaf(-2.0f, dn[0] * rr, 1.0f);
@@ -387,11 +388,13 @@ cudaError_t gru_tc_prepare(elmrnn* h) {
     if ((e = cudaMemcpyAsync(b.data(), h->b, sizeof(float) * GM, cudaMemcpyDeviceToHost, h->stream))) return e;
     if ((e = cudaStreamSynchronize(h->stream))) return e;
     h->tc_wb.assign((size_t)kGM * 3 * (SP + 1), 0.0f);
+    // x k_g: -log2(e) for the sigmoid gates z, r; 2 log2(e) for the tanh candidate f
     for (int j = 0; j < kGM; ++j)
         for (int g = 0; g < 3; ++g) {
+            const double kg = g == 2 ? 2.8853900817779268 : -1.4426950408889634;
             float* d = h->tc_wb.data() + ((size_t)j * 3 + g) * (SP + 1);
-            d[0] = b[g * kGM + j] * scale;
-            for (int s2 = 0; s2 < S; ++s2) d[1 + s2] = W[(size_t)s2 * GM + g * kGM + j] * scale;
+            d[0] = (float)(kg * b[g * kGM + j]);
+            for (int s2 = 0; s2 < S; ++s2) d[1 + s2] = (float)(kg * W[(size_t)s2 * GM + g * kGM + j]);
         }
     const int64_t total = (int64_t)kGChunks * kGKS * 128 * 64;
     k_pack_u_gru<<<(int)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, h->stream>>>(
