@@ -15,7 +15,8 @@
  *   Alg. 1 (S-RELM), P:214-223     : init -> H(t), t=1..Q -> beta = H(Q)^+ Y
  *   Eq. 5  Elman,  P:226-228       : self recurrence over Q lags
  *   Eq. 6  Jordan, P:229-231       : output feedback (teacher forced, reading R7)
- *   Eq. 7  NARMAX, P:232-234       : output + error feedback (e == 0, reading R8)
+ *   Eq. 7  NARMAX, P:232-234       : output + error feedback (e == 0, reading R8;
+ *                                    or a given e: SURVEY 8(f) row 4, reading R30)
  *   S2.2.4 fully connected, P:125-127 (prose reading R9: all neurons, Q lags)
  *   S2.2.5 LSTM, P:128-142 ; S2.2.6 GRU, P:144-150 (dense U, reading R10/R11)
  *   S4.2   QR solve, P:327-328     : H = QR, z = Q^T Y, R beta = z
@@ -239,7 +240,13 @@ static void orc_row_elman(const orc_net* n, const float* Xi, double* hist /*[Q+1
 /* Eq. 6 (Jordan) / Eq. 7 (NARMAX) under teacher forcing: full t-loop.
  * The feedback terms read the teacher signal, never h, so h_j(Q) depends
  * only on step Q (collapse identity; asserted by tests). */
-static double orc_tf_step(const orc_net* n, const float* Xi, const float* Yi, int t, int j) {
+/* e(tau) of reading R30: Ei[tau-1] when an error window is given, else 0 (R8);
+ * e(tau <= 0) = 0 like y (R13). */
+static double orc_e(const float* Ei, int tau) {
+    if (tau <= 0 || !Ei) return 0.0;
+    return (double)Ei[tau - 1];
+}
+static double orc_tf_step(const orc_net* n, const float* Xi, const float* Yi, const float* Ei, int t, int j) {
     double a = orc_wx_b(n->blk[0], n->blk[1], Xi, n->S, n->M, t, j);
     if (n->arch == ARCH_JORDAN) {
         const float* al = n->blk[2];
@@ -247,14 +254,14 @@ static double orc_tf_step(const orc_net* n, const float* Xi, const float* Yi, in
     } else {
         const float *W1 = n->blk[2], *W2 = n->blk[3];
         for (int l = 1; l <= n->F; ++l) a += (double)W1[(int64_t)j * n->F + (l - 1)] * orc_y(Xi, Yi, n->S, t - l);
-        for (int l = 1; l <= n->R; ++l) a += (double)W2[(int64_t)j * n->R + (l - 1)] * 0.0; /* e == 0 (R8) */
+        for (int l = 1; l <= n->R; ++l) a += (double)W2[(int64_t)j * n->R + (l - 1)] * orc_e(Ei, t - l);
     }
     return orc_g(a, n->act);
 }
-static void orc_row_tf(const orc_net* n, const float* Xi, const float* Yi, double* Hrow) {
+static void orc_row_tf(const orc_net* n, const float* Xi, const float* Yi, const float* Ei, double* Hrow) {
     for (int j = 0; j < n->M; ++j) {
         double h = 0.0;
-        for (int t = 1; t <= n->Q; ++t) h = orc_tf_step(n, Xi, Yi, t, j);
+        for (int t = 1; t <= n->Q; ++t) h = orc_tf_step(n, Xi, Yi, Ei, t, j);
         Hrow[j] = h;
     }
 }
@@ -388,9 +395,10 @@ static void orc_row_gru_diag(const orc_net* n, const float* Xi, double* Hrow) {
 /* Alg. 1 line 2: H(Q) for every sample row; rows are independent
  * (the parallel decomposition of P:250), so an OpenMP row split gives
  * bitwise-identical results for any thread count. */
-int orc_build_H(int arch, int S, int M, int Q, int F, int R, int act, int fc_lags,
-                const float* const* blocks, const float* X, int64_t ldx,
-                const float* Yfb, int64_t ldy, int64_t N, double* H, int64_t ldh, int threads) {
+int orc_build_H_ef(int arch, int S, int M, int Q, int F, int R, int act, int fc_lags,
+                   const float* const* blocks, const float* X, int64_t ldx,
+                   const float* Yfb, int64_t ldy, const float* Efb, int64_t lde,
+                   int64_t N, double* H, int64_t ldh, int threads) {
     if (arch < 0 || arch > ARCH_FC_EQ8 || S < 1 || M < 1 || Q < 1) return -1;
     orc_net net = { arch, S, M, Q, F, R, act, fc_lags, blocks };
     int64_t wlen = (int64_t)(Q + 1) * M + 8 * M + Q + 8;
@@ -406,10 +414,11 @@ int orc_build_H(int arch, int S, int M, int Q, int F, int R, int act, int fc_lag
         for (int64_t i = 0; i < N; ++i) {
             const float* Xi = X + i * ldx;
             const float* Yi = Yfb ? Yfb + i * ldy : NULL;
+            const float* Ei = (Efb && arch == ARCH_NARMAX) ? Efb + i * lde : NULL;
             double* Hrow = H + i * ldh;
             switch (arch) {
             case ARCH_ELMAN: orc_row_elman(&net, Xi, work, Hrow); break;
-            case ARCH_JORDAN: case ARCH_NARMAX: orc_row_tf(&net, Xi, Yi, Hrow); break;
+            case ARCH_JORDAN: case ARCH_NARMAX: orc_row_tf(&net, Xi, Yi, Ei, Hrow); break;
             case ARCH_FC: orc_row_fc(&net, Xi, work, Hrow); break;
             case ARCH_LSTM: orc_row_lstm(&net, Xi, work, Hrow); break;
             case ARCH_GRU: orc_row_gru(&net, Xi, work, Hrow); break;
@@ -421,6 +430,36 @@ int orc_build_H(int arch, int S, int M, int Q, int F, int R, int act, int fc_lag
         free(work);
     }
     return 0;
+}
+
+int orc_build_H(int arch, int S, int M, int Q, int F, int R, int act, int fc_lags,
+                const float* const* blocks, const float* X, int64_t ldx,
+                const float* Yfb, int64_t ldy, int64_t N, double* H, int64_t ldh, int threads) {
+    return orc_build_H_ef(arch, S, M, Q, F, R, act, fc_lags, blocks, X, ldx, Yfb, ldy, NULL, 0, N, H, ldh, threads);
+}
+
+/* NARMAX error feedback (Eq. 7, "e(t) = y(t) - yhat(t)" P:122;
+ * SURVEY 8(f) row 4; reading R30).  Rows are the consecutive stride-1 windows
+ * of one series (R22): window i's output y(tau) is the target of window
+ * k = i + tau - Q, so
+ *     e_i(tau) = Y[k] - yhat[k],  yhat[k] = sum_j H[k][j] beta[j]  (Eq. 4),
+ * and e_i(tau) = 0 when k < 0 (before the first window, like R13).
+ * Ef[i][tau-1] holds e_i(tau) for tau = 1..Q, stored as fp32 (the GPU's
+ * input type), rounded once from fp64. */
+void orc_error_windows(const double* H, int64_t ldh, const double* Y, int64_t N, int M, int Q,
+                       const double* beta, float* Ef, int64_t lde) {
+    for (int64_t i = 0; i < N; ++i) {
+        for (int tau = 1; tau <= Q; ++tau) {
+            int64_t k = i + tau - Q;
+            double e = 0.0;
+            if (k >= 0) {
+                double yhat = 0.0;
+                for (int j = 0; j < M; ++j) yhat += H[k * ldh + j] * beta[j];
+                e = Y[k] - yhat;
+            }
+            Ef[i * lde + (tau - 1)] = (float)e;
+        }
+    }
 }
 
 /* ------------------------------------------------------------------------ */

@@ -62,6 +62,10 @@ def lib():
         L.orc_num_blocks.restype = i32
         L.orc_build_H.argtypes = [i32] * 8 + [vp, vp, i64, vp, i64, i64, vp, i64, i32]
         L.orc_build_H.restype = i32
+        L.orc_build_H_ef.argtypes = [i32] * 8 + [vp, vp, i64, vp, i64, vp, i64, i64, vp, i64, i32]
+        L.orc_build_H_ef.restype = i32
+        L.orc_error_windows.argtypes = [vp, i64, vp, i64, i32, i32, vp, vp, i64]
+        L.orc_error_windows.restype = None
         L.orc_lstsq.argtypes = [vp, i64, vp, i64, i32, vp, vp, vp]
         L.orc_lstsq.restype = i32
         L.orc_solve_from_R.argtypes = [vp, i32, i64, vp, vp]
@@ -144,8 +148,10 @@ def gen_weights(net: Net, seed: int):
     return out
 
 
-def build_H(net: Net, blocks, X, Yfb=None, threads: int = 1) -> np.ndarray:
-    """fp64 H(Q) [N][M] for fp32 X [N][Q][S] (or [N][Q*S]) and optional Yfb [N][Q]."""
+def build_H(net: Net, blocks, X, Yfb=None, threads: int = 1, Ef=None) -> np.ndarray:
+    """fp64 H(Q) [N][M] for fp32 X [N][Q][S] (or [N][Q*S]), optional Yfb [N][Q]
+    and, for NARMAX, an optional error window Ef [N][Q] (e_i(tau) = Ef[i][tau-1],
+    reading R30; None: e == 0, reading R8)."""
     X = np.ascontiguousarray(X, dtype=np.float32)
     N = X.shape[0]
     X2 = X.reshape(N, -1)
@@ -158,11 +164,16 @@ def build_H(net: Net, blocks, X, Yfb=None, threads: int = 1) -> np.ndarray:
     if Yfb is not None:
         Yfb = np.ascontiguousarray(Yfb, dtype=np.float32).reshape(N, -1)
         ydata, ldy = Yfb.ctypes.data, Yfb.shape[1]
+    edata, lde = None, 0
+    if Ef is not None:
+        Ef = np.ascontiguousarray(Ef, dtype=np.float32).reshape(N, -1)
+        assert Ef.shape[1] >= net.Q
+        edata, lde = Ef.ctypes.data, Ef.shape[1]
     if N == 0:
         return H
-    rc = lib().orc_build_H(net.code, net.S, net.M, net.Q, net.F, net.R, net.act, net.fc_lags,
-                           ctypes.cast(ptrs, ctypes.c_void_p), X2.ctypes.data, X2.shape[1],
-                           ydata, ldy, N, H.ctypes.data, net.M, threads)
+    rc = lib().orc_build_H_ef(net.code, net.S, net.M, net.Q, net.F, net.R, net.act, net.fc_lags,
+                              ctypes.cast(ptrs, ctypes.c_void_p), X2.ctypes.data, X2.shape[1],
+                              ydata, ldy, edata, lde, N, H.ctypes.data, net.M, threads)
     assert rc == 0
     return H
 
@@ -195,6 +206,32 @@ def lstsq(H, Y):
                          ctypes.addressof(info), R.ctypes.data)
     return beta, SolveInfo(info.rho, info.rmse, info.rdiag_min_abs, info.rdiag_max_abs,
                            info.ridge_lambda, info.rank_flag, info.n_total, rc, R)
+
+
+def error_windows(H, Y, beta, Q: int) -> np.ndarray:
+    """NARMAX error-feedback windows (Eq. 7, P:122 e(t) = y(t) - yhat(t); reading
+    R30): Ef[i][tau-1] = Y[k] - H[k].beta with k = i + tau - Q (0 when k < 0),
+    fp32 [N][Q]."""
+    H = np.ascontiguousarray(H, dtype=np.float64)
+    N, M = H.shape
+    Y = np.ascontiguousarray(np.asarray(Y, dtype=np.float64).reshape(N))
+    beta = np.ascontiguousarray(beta, dtype=np.float64).reshape(M)
+    Ef = np.zeros((N, Q), dtype=np.float32)
+    lib().orc_error_windows(H.ctypes.data, M, Y.ctypes.data, N, M, Q, beta.ctypes.data, Ef.ctypes.data, Q)
+    return Ef
+
+
+def train_narmax_ef(net: Net, blocks, X, Y, Yfb=None, threads: int = 1):
+    """Two-pass NARMAX training with real error feedback:
+    pass 0 with e == 0 (R8) gives beta0; e = y - yhat(beta0) (R30); pass 1
+    rebuilds H with that e and re-solves.  Returns (H1, beta1, info1, beta0, info0)."""
+    assert net.arch == "narmax"
+    H0 = build_H(net, blocks, X, Yfb, threads=threads)
+    b0, i0 = lstsq(H0, Y)
+    Ef = error_windows(H0, Y, b0, net.Q)
+    H1 = build_H(net, blocks, X, Yfb, threads=threads, Ef=Ef)
+    b1, i1 = lstsq(H1, Y)
+    return H1, b1, i1, b0, i0
 
 
 def solve_from_R(R, M: int, n_total: int):
