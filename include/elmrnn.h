@@ -102,7 +102,8 @@ ELMRNN_API void elmrnn_opts_default(elmrnn_opts* opts);
  * the fixed random weights on the GPU with the counter-based generator of
  * DESIGN.md "Weights" (R1, R2).  arch: elmrnn_arch; d = S input dimension
  * (Table 1); M hidden neurons; Q window length / lags; seed: weight seed.
- * Errors: ARG, UNSUPPORTED, OOM, CUDA.  *out is NULL on error. */
+ * Errors: ARG, UNSUPPORTED (M > 1024; Elman/fc_eq8 with Q > 128; a forced
+ * tensor-core path the shape does not admit), OOM, CUDA.  *out is NULL on error. */
 ELMRNN_API elmrnn_status elmrnn_init(elmrnn_t* out, int arch, int d, int M, int Q, uint64_t seed);
 ELMRNN_API elmrnn_status elmrnn_init_ex(elmrnn_t* out, int arch, int d, int M, int Q, uint64_t seed,
                              const elmrnn_opts* opts);
@@ -121,6 +122,29 @@ ELMRNN_API elmrnn_status elmrnn_set_stream(elmrnn_t h, void* cuda_stream);
  * N == 0 is a no-op.  Errors: ARG, SHAPE, CUDA. */
 ELMRNN_API elmrnn_status elmrnn_build_H(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb,
                              int64_t ldy, int64_t N, float* H, int64_t ldh);
+
+/* Eq. 7 with real error feedback (reading R30):
+ * elmrnn_build_H plus, for NARMAX, the error terms sum_{l=1}^{R} W''[j][l] e(t-l).
+ *   Ef  dev fp32 [N][lde] error window, Ef[i][tau-1] = e_i(tau), or NULL (e == 0,
+ *       R8: identical to elmrnn_build_H); lde >= Q.  Typically the output of
+ *       elmrnn_error_windows for the previous pass's beta.
+ * Other arguments as elmrnn_build_H.  Errors: ARG (Ef given for another
+ * architecture), SHAPE, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_build_H_ef(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb,
+                                int64_t ldy, const float* Ef, int64_t lde, int64_t N, float* H,
+                                int64_t ldh);
+
+/* NARMAX error windows for the second pass ("e(t) = y(t) - yhat(t)",
+ * Eq. 4 for yhat; reading R30): with the rows of H being consecutive stride-1
+ * windows of one series (R22), window i's e(tau) is the residual of window
+ * k = i + tau - Q:
+ *     Ef[i][tau-1] = Y[k] - sum_j H[k][j] beta[j]   (k >= 0; else 0), tau = 1..Q,
+ * accumulated in fp64 and rounded once to fp32.
+ *   H dev fp32 [N][ldh] (pass-0 H), Y dev fp32 [N], beta dev fp64 [M],
+ *   Ef dev fp32 [N][lde] output, lde >= Q.  Uses an N-float library workspace.
+ * Asynchronous.  Errors: ARG, SHAPE, OOM, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_error_windows(elmrnn_t h, const float* H, int64_t ldh, const float* Y,
+                                   int64_t N, const double* beta, float* Ef, int64_t lde);
 
 /* S4.2: beta = argmin ||H beta - Y||_2 by fp64 Householder
  * tall-skinny QR of [H | Y] (the reflectors are applied to Y as the augmented

@@ -49,7 +49,7 @@ elmrnn_status elmrnn_init_ex(elmrnn_t* out, int arch, int d, int M, int Q, uint6
         return fail(nullptr, ELMRNN_ERR_ARG, "invalid option value");
     if ((arch == ELMRNN_ELMAN || arch == ELMRNN_FC_EQ8) && !elman_supported(Q))
         return fail(nullptr, ELMRNN_ERR_UNSUPPORTED, "Elman supports Q <= 128");
-    if (M > 1023) return fail(nullptr, ELMRNN_ERR_UNSUPPORTED, "M <= 1023 (TSQR: one thread per column of [H|Y])");
+    if (M > 1024) return fail(nullptr, ELMRNN_ERR_UNSUPPORTED, "M <= 1024 (the widest BASELINE config, C5)");
 
     elmrnn* h = new (std::nothrow) elmrnn();
     if (!h) return fail(nullptr, ELMRNN_ERR_OOM, "host allocation failed");
@@ -66,7 +66,7 @@ elmrnn_status elmrnn_init_ex(elmrnn_t* out, int arch, int d, int M, int Q, uint6
     const int64_t GM = (int64_t)h->G * M;
     switch (arch) {
     case ELMRNN_ELMAN: case ELMRNN_JORDAN: h->rec_len = (int64_t)Q * M; break;
-    case ELMRNN_NARMAX: h->rec_len = (int64_t)(o.F > 0 ? o.F : 1) * M; break;
+    case ELMRNN_NARMAX: h->rec_len = (int64_t)(o.F + o.R > 0 ? o.F + o.R : 1) * M; break;
     case ELMRNN_FC: h->rec_len = (int64_t)o.fc_lags * M * M; break;
     case ELMRNN_FC_EQ8: h->rec_len = (int64_t)Q * M; break;
     case ELMRNN_LSTM_DIAG: case ELMRNN_GRU_DIAG: h->rec_len = GM; break;
@@ -100,12 +100,12 @@ elmrnn_status elmrnn_set_stream(elmrnn_t h, void* s) {
 }
 
 static elmrnn_status build_impl(elmrnn* h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy, int64_t N,
-                                float* H, int64_t ldh) {
+                                float* H, int64_t ldh, const float* Ef = nullptr, int64_t lde = 0) {
     cudaError_t e;
     switch (h->arch) {
     case ELMRNN_ELMAN: case ELMRNN_FC_EQ8: e = launch_elman(h, X, ldx, N, H, ldh); break;
     case ELMRNN_LSTM_DIAG: case ELMRNN_GRU_DIAG: e = launch_diag_gated(h, X, ldx, N, H, ldh); break;
-    case ELMRNN_JORDAN: case ELMRNN_NARMAX: e = launch_teacher_forced(h, X, ldx, Yfb, ldy, N, H, ldh); break;
+    case ELMRNN_JORDAN: case ELMRNN_NARMAX: e = launch_teacher_forced(h, X, ldx, Yfb, ldy, N, H, ldh, Ef, lde); break;
     default:
         e = h->path == 2 ? launch_dense_tc(h, X, ldx, N, H, ldh) : launch_dense_fma(h, X, ldx, N, H, ldh);
         if (e == cudaErrorInvalidConfiguration)
@@ -128,6 +128,43 @@ elmrnn_status elmrnn_build_H(elmrnn_t h, const float* X, int64_t ldx, const floa
     if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(H)) & 3)
         return fail(h, ELMRNN_ERR_SHAPE, "pointers must be 4-byte aligned");
     return build_impl(h, X, ldx, Yfb, ldy, N, H, ldh);
+}
+
+elmrnn_status elmrnn_build_H_ef(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy,
+                                const float* Ef, int64_t lde, int64_t N, float* H, int64_t ldh) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (Ef && h->arch != ELMRNN_NARMAX) return fail(h, ELMRNN_ERR_ARG, "error feedback is a NARMAX input");
+    if (Ef && lde < h->Q) return fail(h, ELMRNN_ERR_SHAPE, "lde < Q");
+    if (Ef && (reinterpret_cast<uintptr_t>(Ef) & 3)) return fail(h, ELMRNN_ERR_SHAPE, "Ef must be 4-byte aligned");
+    if (N < 0) return fail(h, ELMRNN_ERR_ARG, "N < 0");
+    if (N == 0) return ELMRNN_OK;
+    if (!X || !H) return fail(h, ELMRNN_ERR_ARG, "X or H is NULL");
+    if (ldx < (int64_t)h->Q * h->S) return fail(h, ELMRNN_ERR_SHAPE, "ldx < Q*d");
+    if (ldh < h->M) return fail(h, ELMRNN_ERR_SHAPE, "ldh < M");
+    if (Yfb && ldy < h->Q) return fail(h, ELMRNN_ERR_SHAPE, "ldy < Q");
+    if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(H)) & 3)
+        return fail(h, ELMRNN_ERR_SHAPE, "pointers must be 4-byte aligned");
+    return build_impl(h, X, ldx, Yfb, ldy, N, H, ldh, Ef, lde);
+}
+
+elmrnn_status elmrnn_error_windows(elmrnn_t h, const float* H, int64_t ldh, const float* Y, int64_t N,
+                                   const double* beta, float* Ef, int64_t lde) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (N < 0) return fail(h, ELMRNN_ERR_ARG, "N < 0");
+    if (N == 0) return ELMRNN_OK;
+    if (!H || !Y || !beta || !Ef) return fail(h, ELMRNN_ERR_ARG, "NULL pointer");
+    if (ldh < h->M) return fail(h, ELMRNN_ERR_SHAPE, "ldh < M");
+    if (lde < h->Q) return fail(h, ELMRNN_ERR_SHAPE, "lde < Q");
+    cudaError_t e;
+    if (N > h->rws_rows) {
+        if (h->rws) cudaFree(h->rws);
+        h->rws = nullptr;
+        h->rws_rows = 0;
+        if ((e = cudaMalloc(&h->rws, sizeof(float) * N))) return cuda_fail(h, e, "error-window workspace");
+        h->rws_rows = N;
+    }
+    if ((e = launch_error_windows(h, H, ldh, Y, N, beta, Ef, lde))) return cuda_fail(h, e, "error_windows");
+    return ELMRNN_OK;
 }
 
 static elmrnn_status finish_solve(elmrnn* h, elmrnn_solve_info* info) {
@@ -237,7 +274,7 @@ const char* elmrnn_last_error(elmrnn_t h) { return h ? h->err.c_str() : g_init_e
 void elmrnn_destroy(elmrnn_t h) {
     if (!h) return;
     cudaFree(h->W); cudaFree(h->b); cudaFree(h->rec); cudaFree(h->tc_ops);
-    cudaFree(h->Rws); cudaFree(h->sdev); cudaFree(h->flag); cudaFree(h->Hws); cudaFree(h->scratch);
+    cudaFree(h->Rws); cudaFree(h->sdev); cudaFree(h->flag); cudaFree(h->Hws); cudaFree(h->rws); cudaFree(h->scratch);
     if (h->shost) cudaFreeHost(h->shost);
     delete h;
 }

@@ -40,7 +40,7 @@ struct elmrnn {
     // packed weights (device)
     float* W;             // [S][G*M]
     float* b;             // [G*M]
-    float* rec;           // Elman/Jordan alpha^T [Q][M]; NARMAX W'^T [F][M]; FC A [L][M][M];
+    float* rec;           // Elman/Jordan alpha^T [Q][M]; NARMAX W'^T [F][M] | W''^T [R][M]; FC A [L][M][M];
                           // LSTM/GRU U_cat [M][G*M] (U_cat[k][g*M+j] = U_g[k][j])
     int64_t rec_len;
     // tensor-core operands (device; only when path == 2)
@@ -55,6 +55,8 @@ struct elmrnn {
     int* flag;            // device non-finite flag
     elm::SolveDev* shost; // pinned host mirror
     float* Hws;           // predict scratch
+    float* rws;           // error-window scratch: residual per row (N floats)
+    int64_t rws_rows;
     int64_t Hws_rows;
     float* scratch;       // builder scratch (FC history ring)
     size_t scratch_bytes;
@@ -74,7 +76,9 @@ int num_blocks(int arch);
 cudaError_t launch_elman(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
 cudaError_t launch_diag_gated(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
 cudaError_t launch_teacher_forced(elmrnn* h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy,
-                                  int64_t N, float* H, int64_t ldh);
+                                  int64_t N, float* H, int64_t ldh, const float* Ef = nullptr, int64_t lde = 0);
+cudaError_t launch_error_windows(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t N,
+                                 const double* beta, float* Ef, int64_t lde);
 cudaError_t launch_dense_fma(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
 bool elman_supported(int Q);
 

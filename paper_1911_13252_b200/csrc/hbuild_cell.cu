@@ -188,14 +188,16 @@ cudaError_t launch_elman(elmrnn* h, const float* X, int64_t ldx, int64_t N, floa
 // teacher signal, never h, so H(Q) needs step Q only (one-step collapse):
 //   a_j = W[:,j].x(Q) + b_j + sum_{k=1}^{nlag} rec[k-1][j] * y(Q-k)
 // Jordan: rec = alpha^T, nlag = Q-1 (y(0) = 0).  NARMAX: rec = W'^T,
-// nlag = min(F, Q-1); the W'' terms multiply e == 0.
-// y(tau) = Yfb[i][tau-1], or X[i][tau][0] when Yfb == NULL.
+// nlag = min(F, Q-1); the W'' terms multiply e == 0 (R8) unless an error
+// window is given (R30): + sum_{l=1}^{nerr} W''^T[l-1][j] e(Q-l), nerr = min(R, Q-1).
+// y(tau) = Yfb[i][tau-1], or X[i][tau][0] when Yfb == NULL; e(tau) = Ef[i][tau-1].
 __global__ void __launch_bounds__(256) k_teacher_forced(const float* __restrict__ X, int64_t ldx,
                                                         const float* __restrict__ Yfb, int64_t ldy, int64_t N, int S,
                                                         int M, int Q, int nlag, int act,
                                                         const float* __restrict__ W, const float* __restrict__ b,
                                                         const float* __restrict__ recT, float* __restrict__ H,
-                                                        int64_t ldh) {
+                                                        int64_t ldh, const float* __restrict__ Ef, int64_t lde,
+                                                        int nerr, const float* __restrict__ recE) {
     int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (cell >= N * (int64_t)M) return;
     int64_t i = cell / M;
@@ -210,19 +212,27 @@ __global__ void __launch_bounds__(256) k_teacher_forced(const float* __restrict_
         for (int k = 1; k <= nlag; ++k)
             a = fmaf(__ldg(recT + (int64_t)(k - 1) * M + j), __ldg(xi + (int64_t)(Q - k) * S), a);
     }
+    if (Ef) {
+        const float* ei = Ef + i * lde;
+        for (int l = 1; l <= nerr; ++l) a = fmaf(__ldg(recE + (int64_t)(l - 1) * M + j), __ldg(ei + (Q - l - 1)), a);
+    }
     H[i * ldh + j] = act_g(a, act);
 }
 
 cudaError_t launch_teacher_forced(elmrnn* h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy, int64_t N,
-                                  float* H, int64_t ldh) {
+                                  float* H, int64_t ldh, const float* Ef, int64_t lde) {
     int64_t cells = N * (int64_t)h->M;
     int threads = 256;
     int64_t blocks = (cells + threads - 1) / threads;
     if (blocks > INT32_MAX) return cudaErrorInvalidConfiguration;
     int nlag = h->Q - 1;
     if (h->arch == kArchNarmax) nlag = h->F < h->Q - 1 ? h->F : h->Q - 1;
+    const bool ef = Ef && h->arch == kArchNarmax;
+    const int nerr = ef ? (h->R < h->Q - 1 ? h->R : h->Q - 1) : 0;
     k_teacher_forced<<<(unsigned)blocks, threads, 0, h->stream>>>(X, ldx, Yfb, ldy, N, h->S, h->M, h->Q, nlag,
-                                                                  h->act, h->W, h->b, h->rec, H, ldh);
+                                                                  h->act, h->W, h->b, h->rec, H, ldh,
+                                                                  ef ? Ef : nullptr, lde, nerr,
+                                                                  h->rec + (size_t)h->F * h->M);
     h->launches++;
     return cudaGetLastError();
 }

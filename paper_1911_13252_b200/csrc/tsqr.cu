@@ -612,6 +612,85 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
     }
 }
 
+// ---- wide solve (n = M+1 > 1024: more columns than threads in a CTA) ---------------------
+// Same steps as k_tsqr_solve, with each thread owning the columns j = tid,
+// tid + nt, ...; the ridge rows sqrt(lambda)(I|0) are written to slab 1 and
+// folded into slab 0 by k_tsqr_merge_wy (a zero slab folds as the identity:
+// every reflector has s2 = 0, g = 0), then k_solve_wide_finish re-normalises
+// the signs and back-substitutes.  Reading R18/R19 as in k_tsqr_solve.
+__device__ void wide_sign_normalise(double* __restrict__ R, int n, double* zs) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) zs[j] = R[(size_t)j * n + j] < 0.0 ? -1.0 : 1.0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+        for (int k = 0; k <= j; ++k) R[(size_t)k * n + j] *= zs[k];
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024, 1)
+    k_solve_wide_prep(double* __restrict__ R, double* __restrict__ Rridge, double* __restrict__ Rorig, int M,
+                      SolveDev* __restrict__ out) {
+    extern __shared__ __align__(16) double zs[];
+    __shared__ double red[32];
+    const int n = M + 1;
+    wide_sign_normalise(R, n, zs);
+    double dmn = INFINITY, dmx = 0.0, f2 = 0.0;
+    for (int j = threadIdx.x; j < M; j += blockDim.x) {
+        const double d = fabs(R[(size_t)j * n + j]);
+        dmn = fmin(dmn, d);
+        dmx = fmax(dmx, d);
+        for (int k = 0; k <= j; ++k) f2 += R[(size_t)k * n + j] * R[(size_t)k * n + j];
+    }
+    const double dmin = block_min(dmn, red), dmax = block_max(dmx, red), fro2 = block_sum(f2, red);
+    const bool ridge = !(dmin > DBL_EPSILON * (double)M * dmax);
+    const double lambda = ridge ? 1e-8 * fro2 / (double)M : 0.0;
+    const double sl = sqrt(lambda);
+    for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) {
+        Rorig[e] = R[e];
+        const int64_t k = e / n, j = e % n;
+        Rridge[e] = (k == j && k < M) ? sl : 0.0;
+    }
+    if (threadIdx.x == 0) {
+        out->dmin = dmin;
+        out->dmax = dmax;
+        out->lambda = lambda;
+        out->rank_flag = ridge ? 1 : 0;
+    }
+}
+
+__global__ void __launch_bounds__(1024, 1)
+    k_solve_wide_finish(double* __restrict__ R, const double* __restrict__ Rorig, int M, long long n_total,
+                        const int* __restrict__ flag, double* __restrict__ beta, SolveDev* __restrict__ out) {
+    extern __shared__ __align__(16) double zs[];
+    __shared__ double red[32];
+    __shared__ double bk;
+    const int n = M + 1;
+    wide_sign_normalise(R, n, zs);
+    for (int j = threadIdx.x; j < M; j += blockDim.x) zs[j] = R[(size_t)j * n + M];
+    __syncthreads();
+    for (int k = M - 1; k >= 0; --k) {
+        if (threadIdx.x == 0) bk = zs[k] / R[(size_t)k * n + k];
+        __syncthreads();
+        for (int j = threadIdx.x; j < k; j += blockDim.x) zs[j] -= R[(size_t)j * n + k] * bk;
+        if (threadIdx.x == 0) zs[k] = bk;
+        __syncthreads();
+    }
+    double s2 = 0.0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        double s = 0.0;
+        for (int c = j; c < M; ++c) s += Rorig[(size_t)j * n + c] * zs[c];
+        s -= Rorig[(size_t)j * n + M];
+        s2 += s * s;
+        if (j < M) beta[j] = zs[j];
+    }
+    const double rho2 = block_sum(s2, red);
+    if (threadIdx.x == 0) {
+        out->rho = sqrt(rho2);
+        out->rmse = sqrt(rho2) / sqrt((double)n_total);
+        out->nonfinite = *flag;
+        out->n_total = n_total;
+    }
+}
+
 // ---- 2D register-tiled fold (fold2d) ------------------------------------------------------
 // Thread t = (column group cg = t / 4, row group rg = t % 4) holds TR rows
 // (rg*TR ..) of the TC tile columns TC*cg .. TC*cg+TC-1: a tile of 4*TR rows.
@@ -926,8 +1005,12 @@ __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, in
         s2 += __shfl_xor_sync(F, s2, 16);
         double g = 0.0, u0 = 0.0;
         if (cp == (i >> 1)) {
-            if (s2 != 0.0) {
-                const double t = fma(x0, x0, s2);
+            // t <= 1e-280 is the H = I case of make_reflector (|beta u0| lies in [t, 2t]);
+            // testing t itself also keeps subnormal t away from rsqrt.approx.ftz,
+            // which flushes it to 0 (rs = inf, NaN reflector).  Subnormal t occurs
+            // in deep noise cascades of rank-deficient partial R (16-row tiles, n > 512).
+            const double t = fma(x0, x0, s2);
+            if (t > 1e-280) {
                 const double rs = rsqrt_nr(t);
                 const double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * (t * rs);
                 const double uu = x0 - beta;
@@ -1316,12 +1399,15 @@ static bool use_2d(int n) {
 }
 static int threads_2d(int n) { return (4 * ((n + kTC2 - 1) / kTC2) + 31) / 32 * 32; }
 
+// n = M+1 above this takes the WY leaf/merge and the wide solve (columns > threads).
+constexpr int kWideN = 1024;
 // Blocked compact-WY leaf + merge (wy_fold).  ELMRNN_TSQR_WY=0/1 overrides the default.
 // Measured (B200, profiles/): M = 256 WY 113 ms vs 147 ms per-column fold at
 // C4; M <= 128 the per-column fold is faster (C3 10.4 vs 11.8 ms).
 static bool use_wy(int n) {
-    if (const char* e = std::getenv("ELMRNN_TSQR_WY")) return std::atoi(e) != 0 && n <= 1024;
-    return n > 192 && n <= 1024;
+    if (n > kWideN) return true;   // the only leaf/merge for more columns than CTA threads
+    if (const char* e = std::getenv("ELMRNN_TSQR_WY")) return std::atoi(e) != 0;
+    return n > 192;
 }
 static int wy_rows(int n) {
     if (const char* e = std::getenv("ELMRNN_TSQR_WY_ROWS")) {   // testing aid
@@ -1470,7 +1556,7 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
     const Var v = pick_var(n);
     const int64_t slabs = tsqr_leaf_slabs(h, N);
     cudaError_t e;
-    if ((e = ensure_solve_ws(h, slabs))) return e;
+    if ((e = ensure_solve_ws(h, n > kWideN && slabs < 2 ? 2 : slabs))) return e;   // wide solve: slab 1 = ridge rows
     if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream))) return e;
     const int rows_tile = use_wy(n) ? wy_rows(n) : use_2d(n) ? kRG * kTR2 : var_rows(v);
     int64_t rows = (N + slabs - 1) / slabs;
@@ -1520,7 +1606,7 @@ cudaError_t tsqr_pack(elmrnn* h, double* Rpk) {
 cudaError_t tsqr_merge_packed(elmrnn* h, const double* Rpk_all, int P) {
     const int n = h->M + 1;
     cudaError_t e;
-    if ((e = ensure_solve_ws(h, P))) return e;
+    if ((e = ensure_solve_ws(h, n > kWideN && P < 2 ? 2 : P))) return e;
     if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream))) return e;
     int64_t total = (int64_t)P * n * n;
     int blocks = (int)((total + 255) / 256);
@@ -1536,6 +1622,24 @@ cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta) {
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
     double* Rorig = h->Rws + (size_t)(h->Rws_slabs - 1) * n * n;
+    if (n > kWideN) {
+        const size_t zsm = ((n + 1) & ~1) * sizeof(double);
+        k_solve_wide_prep<<<1, 1024, zsm, h->stream>>>(h->Rws, h->Rws + (size_t)n * n, Rorig, h->M, h->sdev);
+        h->launches++;
+        cudaError_t e = wy_dispatch(n, [&](auto rows) {
+            constexpr int RW = decltype(rows)::value;
+            const size_t sm = wy_smem_bytes(RW, n);
+            cudaFuncSetAttribute(k_tsqr_merge_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_tsqr_merge_wy<RW><<<1, wy_threads(n), sm, h->stream>>>(h->Rws, 2, 1, n);
+            h->launches++;
+            return cudaGetLastError();
+        });
+        if (e) return e;
+        k_solve_wide_finish<<<1, 1024, zsm, h->stream>>>(h->Rws, Rorig, h->M, (long long)n_total, h->flag, beta,
+                                                          h->sdev);
+        h->launches++;
+        return cudaGetLastError();
+    }
     const size_t smem = ((n + 1) & ~1) * sizeof(double) + var_smem(v, n);
     return dispatch(v, [&](auto tr, auto p, auto b) {
         k_tsqr_solve<decltype(tr)::value, decltype(p)::value, decltype(b)::value><<<1, threads, smem, h->stream>>>(
@@ -1565,4 +1669,42 @@ cudaError_t launch_predict_gemv(elmrnn* h, const float* H, int64_t ldh, int64_t 
     return cudaGetLastError();
 }
 
+}  // namespace elm
+
+namespace elm {
+// ---- NARMAX error feedback (Eq. 7, e(t) = y(t) - yhat(t) P:122; reading R30) ----
+// r_k = Y_k - H_k . beta (Eq. 4, fp64 accumulation, rounded once), then
+// Ef[i][tau-1] = r_{i+tau-Q} (0 when i+tau-Q < 0): rows are consecutive
+// stride-1 windows of one series (R22).
+__global__ void k_residual(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t N, int M,
+                           const double* __restrict__ beta, float* __restrict__ r) {
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= N) return;
+    double s = 0.0;
+    for (int j = lane; j < M; j += 32) s += (double)H[row * ldh + j] * beta[j];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) r[row] = (float)((double)Y[row] - s);
+}
+
+__global__ void k_error_windows(const float* __restrict__ r, int64_t N, int Q, float* __restrict__ Ef, int64_t lde) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N * Q; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / Q;
+        const int tau = (int)(e - i * Q) + 1;
+        const int64_t k = i + tau - Q;
+        Ef[i * lde + tau - 1] = k >= 0 ? r[k] : 0.0f;
+    }
+}
+
+cudaError_t launch_error_windows(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t N,
+                                 const double* beta, float* Ef, int64_t lde) {
+    const int64_t blocks = (N * 32 + 255) / 256;
+    if (blocks > INT32_MAX) return cudaErrorInvalidConfiguration;
+    k_residual<<<(unsigned)blocks, 256, 0, h->stream>>>(H, ldh, Y, N, h->M, beta, h->rws);
+    h->launches++;
+    const int64_t b2 = std::min<int64_t>((N * h->Q + 255) / 256, (int64_t)h->sm_count * 16);
+    k_error_windows<<<(unsigned)b2, 256, 0, h->stream>>>(h->rws, N, h->Q, Ef, lde);
+    h->launches++;
+    return cudaGetLastError();
+}
 }  // namespace elm

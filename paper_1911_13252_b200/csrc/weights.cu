@@ -163,7 +163,7 @@ static cudaError_t launch_gen(elmrnn* h, int id, float* dst, int64_t ld, int64_t
 // Packed layouts:
 //   W   [S][G*M]   (gate g in columns g*M .. g*M+M-1)
 //   b   [G*M]
-//   rec Elman/Jordan alpha^T [Q][M]; NARMAX W'^T [F][M]; FC A [L*M][M];
+//   rec Elman/Jordan alpha^T [Q][M]; NARMAX W'^T [F][M] then W''^T [R][M]; FC A [L*M][M];
 //       LSTM/GRU U_cat [M][G*M]; diagonal LSTM/GRU u [G*M];
 //       FC by Eq. 8: alpha^T [Q][M] with alpha[k][j] = sum_l A[k][l][j]
 cudaError_t gen_weights(elmrnn* h) {
@@ -177,7 +177,9 @@ cudaError_t gen_weights(elmrnn* h) {
     case kArchNarmax:
         if ((e = launch_gen(h, 0, h->W, M, 0, 0))) return e;
         if ((e = launch_gen(h, 1, h->b, M, 0, 0))) return e;
-        return launch_gen(h, 2, h->rec, M, 0, 1);  // W'' multiplies e == 0 (R8): not stored
+        if ((e = launch_gen(h, 2, h->rec, M, 0, 1))) return e;
+        // W''^T [R][M] after W'^T: read only when an error window is given (R30)
+        return launch_gen(h, 3, h->rec + (size_t)h->F * M, M, 0, 1);
     case kArchFC:
         if ((e = launch_gen(h, 0, h->W, M, 0, 0))) return e;
         if ((e = launch_gen(h, 1, h->b, M, 0, 0))) return e;

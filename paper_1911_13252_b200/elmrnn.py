@@ -23,6 +23,7 @@ STATUS = {0: "OK", 1: "WARN_RIDGE", -1: "ERR_ARG", -2: "ERR_SHAPE", -3: "ERR_UND
           -4: "ERR_NONFINITE", -5: "ERR_UNSUPPORTED", -6: "ERR_CUDA", -7: "ERR_OOM"}
 
 EXPORTED = ("elmrnn_opts_default", "elmrnn_init", "elmrnn_init_ex", "elmrnn_set_stream", "elmrnn_build_H",
+            "elmrnn_build_H_ef", "elmrnn_error_windows",
             "elmrnn_solve_beta", "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_packed_r_len",
             "elmrnn_predict", "elmrnn_get_weights", "elmrnn_weight_block_len", "elmrnn_path",
             "elmrnn_launch_count", "elmrnn_last_error", "elmrnn_destroy")
@@ -74,6 +75,8 @@ def lib() -> ctypes.CDLL:
         L.elmrnn_init_ex.argtypes = [vp, i32, i32, i32, i32, u64, vp]
         L.elmrnn_set_stream.argtypes = [vp, vp]
         L.elmrnn_build_H.argtypes = [vp, vp, i64, vp, i64, i64, vp, i64]
+        L.elmrnn_build_H_ef.argtypes = [vp, vp, i64, vp, i64, vp, i64, i64, vp, i64]
+        L.elmrnn_error_windows.argtypes = [vp, vp, i64, vp, i64, vp, vp, i64]
         L.elmrnn_solve_beta.argtypes = [vp, vp, i64, vp, i64, vp, vp]
         L.elmrnn_solve_local.argtypes = [vp, vp, i64, vp, i64, vp]
         L.elmrnn_solve_merge.argtypes = [vp, vp, i32, i64, vp, vp]
@@ -90,7 +93,8 @@ def lib() -> ctypes.CDLL:
         L.elmrnn_last_error.restype = ctypes.c_char_p
         L.elmrnn_destroy.argtypes = [vp]
         L.elmrnn_destroy.restype = None
-        for f in ("elmrnn_init", "elmrnn_init_ex", "elmrnn_set_stream", "elmrnn_build_H", "elmrnn_solve_beta",
+        for f in ("elmrnn_init", "elmrnn_init_ex", "elmrnn_set_stream", "elmrnn_build_H", "elmrnn_build_H_ef",
+                  "elmrnn_error_windows", "elmrnn_solve_beta",
                   "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_predict", "elmrnn_get_weights",
                   "elmrnn_path"):
             getattr(L, f).restype = i32
@@ -174,8 +178,10 @@ class ELMRNN:
         return lib().elmrnn_packed_r_len(self._h)
 
     # -- API
-    def build_H(self, X: torch.Tensor, Yfb: torch.Tensor | None = None, H: torch.Tensor | None = None):
-        """elmrnn_build_H: X [N][Q][d] (or [N][ldx]) fp32 CUDA -> H [N][M] fp32."""
+    def build_H(self, X: torch.Tensor, Yfb: torch.Tensor | None = None, H: torch.Tensor | None = None,
+                Ef: torch.Tensor | None = None):
+        """elmrnn_build_H (elmrnn_build_H_ef when a NARMAX error window Ef [N][Q] is
+        given): X [N][Q][d] (or [N][ldx]) fp32 CUDA -> H [N][M] fp32."""
         _dev_check(X, "X", torch.float32)
         N = X.shape[0]
         ldx, _ = _rows(X, "X") if N else (self.Q * self.d, 0)
@@ -188,8 +194,30 @@ class ELMRNN:
         _dev_check(H, "H", torch.float32)
         ldh, _ = _rows(H, "H") if N else (self.M, 0)
         self._stream()
-        self._check(lib().elmrnn_build_H(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, N, _ptr(H), ldh))
+        if Ef is None:
+            self._check(lib().elmrnn_build_H(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, N, _ptr(H), ldh))
+        else:
+            _dev_check(Ef, "Ef", torch.float32)
+            lde = _rows(Ef, "Ef")[0] if N else self.Q
+            self._check(lib().elmrnn_build_H_ef(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, _ptr(Ef), lde, N,
+                                                _ptr(H), ldh))
         return H
+
+    def error_windows(self, H: torch.Tensor, Y: torch.Tensor, beta: torch.Tensor, Ef: torch.Tensor | None = None):
+        """elmrnn_error_windows: NARMAX error window Ef [N][Q] fp32 from the
+        residuals Y - H beta of consecutive windows (reading R30)."""
+        _dev_check(H, "H", torch.float32)
+        _dev_check(Y, "Y", torch.float32)
+        _dev_check(beta, "beta", torch.float64)
+        N = H.shape[0]
+        if Ef is None:
+            Ef = torch.empty((N, self.Q), dtype=torch.float32, device=H.device)
+        _dev_check(Ef, "Ef", torch.float32)
+        ldh = _rows(H, "H")[0] if N else self.M
+        lde = _rows(Ef, "Ef")[0] if N else self.Q
+        self._stream()
+        self._check(lib().elmrnn_error_windows(self._h, _ptr(H), ldh, _ptr(Y), N, _ptr(beta), _ptr(Ef), lde))
+        return Ef
 
     def build_H_from_host(self, Xh: torch.Tensor, Xd: torch.Tensor, H: torch.Tensor, chunks: int = 8,
                           copy_stream: torch.cuda.Stream | None = None):
@@ -278,6 +306,18 @@ class ELMRNN:
         H = self.build_H(X, Yfb)
         beta, info = self.solve_beta(H, Y)
         return H, beta, info
+
+    def train_narmax_ef(self, X, Y, Yfb=None):
+        """NARMAX with real error feedback (reading R30): pass 0
+        with e == 0, e = y - yhat(beta0) as error windows, pass 1 rebuilds H with
+        them and re-solves.  Returns (H1, beta1, info1, beta0, info0)."""
+        if self.arch != "narmax":
+            raise ValueError("error feedback is a NARMAX method")
+        H0, b0, i0 = self.train(X, Y, Yfb)
+        Ef = self.error_windows(H0, Y, b0)
+        H1 = self.build_H(X, Yfb, H0, Ef=Ef)
+        b1, i1 = self.solve_beta(H1, Y)
+        return H1, b1, i1, b0, i0
 
     @staticmethod
     def _info(i: _Info, st: int) -> SolveInfo:

@@ -207,7 +207,7 @@ def test_empty_and_errors():
     with pytest.raises(ElmrnnError, match="ERR_ARG"):
         E("lstm", 0, 8, 4, 1)
     with pytest.raises(ElmrnnError, match="ERR_UNSUPPORTED"):
-        E("lstm", 1, 1024, 4, 1)
+        E("lstm", 1, 1025, 4, 1)
 
 
 # ------------------------------------------------------------------------- solve parity
@@ -313,6 +313,23 @@ def test_tsqr_wy_and_fold_agree(M, N, monkeypatch):
         assert np.abs(np.abs(R) - Rn).max() <= 1e-12 * scale, wy
 
 
+@pytest.mark.parametrize("rows,M,N", [("16", 511, 600), ("16", 300, 3001), ("32", 1000, 1500)])
+def test_tsqr_wy_deep_noise_cascade(rows, M, N, monkeypatch):
+    """A leaf that folds many short tiles before reaching full rank drives the
+    noise rows of its partial R into subnormals (DESIGN 6.3); the WY panel must
+    treat t = x0^2 + |x|^2 <= 1e-280 as H = I (else rsqrt.approx.ftz gives NaN)."""
+    monkeypatch.setenv("ELMRNN_TSQR_WY", "1")
+    monkeypatch.setenv("ELMRNN_TSQR_WY_ROWS", rows)
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    H = torch.rand(N, M, device="cuda", generator=g) - 0.5
+    Y = torch.rand(N, device="cuda", generator=g) - 0.5
+    Rn = np.abs(np.linalg.qr(np.column_stack([H.double().cpu().numpy(), Y.double().cpu().numpy()]), mode="r"))
+    e = E("lstm", 1, M, 4, 1, force_path=1)
+    R = _packed_to_R(e.solve_local(H, Y).cpu().numpy(), M + 1)
+    assert np.isfinite(R).all()
+    assert np.abs(np.abs(R) - Rn).max() <= 1e-12 * Rn.max()
+
+
 def test_ridge_and_nonfinite():
     from paper_1911_13252_b200 import ElmrnnError
     e = E("elman", 1, 4, 3, 1)
@@ -387,3 +404,151 @@ def test_full_config_sampled(cfg):
     assert float(g.abs().max()) <= 1e-8 * max(1.0, float((H64.T @ Yd.double()).abs().max()))
     rmse = float(r.norm()) / np.sqrt(c["N"])
     assert info.rmse == pytest.approx(rmse, rel=1e-6)
+
+
+# ------------------------------------------------------------------------- C5 sweep (BASELINE configs[4])
+# LSTM/GRU, M in {32, 128, 512, 1024}, Q in {10, 50, 100}, univariate MG+noise.
+# N per case keeps the oracle (8 M^2 Q fp64 flop per LSTM sample) to seconds
+# while spanning several tiles of the chosen builder plus a ragged tail
+# (FMA tiles are 8-64 rows, tensor-core tiles 128).
+def _c5_rows(M, Q):
+    return {32: 300, 128: 300, 512: 45, 1024: 21}[M] if Q <= 10 else {32: 200, 128: 140, 512: 21, 1024: 11}[M]
+
+
+C5_GRID = [(a, M, Q) for a in ("lstm", "gru") for M in (32, 128, 512, 1024) for Q in (10, 50, 100)]
+
+
+@pytest.mark.parametrize("arch,M,Q", C5_GRID)
+def test_c5_sweep_H_parity(arch, M, Q):
+    N = _c5_rows(M, Q)
+    s = sy.series("mg", N + Q + 1, seed=M + Q, noise=0.01)
+    X, Y, _ = sy.windows(s[:, :1], N, Q)
+    e, Hg = gpu_H(arch, 1, M, Q, 3, X)
+    net = orc.Net(arch, S=1, M=M, Q=Q)
+    Ho = orc.build_H(net, orc.gen_weights(net, 3), X, threads=8)
+    err = np.abs(Hg - Ho).max()
+    assert err <= H_TOL, f"path {e.path}: max |dH| = {err:.3e}"
+
+
+@pytest.mark.parametrize("M,N", [(1024, 3001), (1000, 1201), (1024, 1025)])
+def test_tsqr_wide_matches_lapack(M, N):
+    """n = M+1 > 1024 columns (more than a CTA's threads): WY leaf/merge and
+    the wide solve.  R of [H | Y] against numpy's Householder QR (LAPACK
+    geqrf) up to row signs, beta against the oracle's lstsq of the same H."""
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    H = torch.rand(N, M, device="cuda", generator=g) - 0.5
+    Y = torch.rand(N, device="cuda", generator=g) - 0.5
+    n = M + 1
+    Hn, Yn = H.double().cpu().numpy(), Y.double().cpu().numpy()
+    Rn = np.abs(np.linalg.qr(np.column_stack([Hn, Yn]), mode="r"))
+    e = E("lstm", 1, M, 4, 1)
+    R = _packed_to_R(e.solve_local(H, Y).cpu().numpy(), n)
+    assert np.abs(np.abs(R) - Rn).max() <= 1e-12 * Rn.max()
+    beta, info = e.solve_beta(H, Y)
+    b_ref, i_ref = orc.lstsq(Hn, Yn)
+    cond = np.linalg.cond(i_ref.R[:M, :M])
+    assert np.linalg.norm(beta.cpu().numpy() - b_ref) / np.linalg.norm(b_ref) <= 1e-12 * cond
+    assert info.rmse == pytest.approx(i_ref.rmse, rel=1e-10 * cond)
+    assert info.status == 0 and info.n_total == N
+    # virtual ranks: solve_local x 3 + solve_merge equals the single solve
+    cuts = np.linspace(0, N, 4).astype(int)
+    parts = [e.solve_local(H[a:b], Y[a:b]).clone() for a, b in zip(cuts[:-1], cuts[1:])]
+    b3, _ = e.solve_merge(torch.stack(parts), 3, N)
+    assert float((b3 - beta).norm() / beta.norm()) <= 1e-12 * cond
+
+
+def test_tsqr_wide_ridge():
+    """Rank-deficient H at n > 1024: the wide solve takes the ridge path (R19)
+    like the oracle (duplicated columns)."""
+    M, N = 1024, 2000
+    g = torch.Generator(device="cuda").manual_seed(5)
+    H = torch.rand(N, M, device="cuda", generator=g) - 0.5
+    H[:, 700:] = H[:, :M - 700]
+    Y = torch.rand(N, device="cuda", generator=g) - 0.5
+    e = E("gru", 1, M, 4, 1)
+    beta, info = e.solve_beta(H, Y)
+    b_ref, i_ref = orc.lstsq(H.double().cpu().numpy(), Y.double().cpu().numpy())
+    assert info.status == 1 and info.rank_flag == 1 and i_ref.status == 1
+    assert info.ridge_lambda == pytest.approx(i_ref.ridge_lambda, rel=1e-10)
+    assert info.rmse == pytest.approx(i_ref.rmse, rel=1e-6)
+    np.testing.assert_allclose(beta.cpu().numpy(), b_ref, rtol=1e-5, atol=1e-6 * np.abs(b_ref).max())
+
+
+@pytest.mark.parametrize("arch", ["lstm", "gru"])
+def test_c5_m1024_train_sampled(arch):
+    """C5 widest shape end to end (M = 1024, Q = 10, N = 4096 rows on one GPU):
+    sampled H rows against the oracle; beta and the RMSE against the oracle's
+    Householder lstsq of the same fp32 H (n = 1025: WY leaf + wide solve)."""
+    N, M, Q = 4096, 1024, 10
+    s = sy.series("mg", N + Q + 1, seed=1, noise=0.01)
+    X, Y, _ = sy.windows(s[:, :1], N, Q)
+    e = E(arch, 1, M, Q, 1)
+    Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+    H, beta, info = e.train(Xd, Yd)
+    rows = np.array([0, 1, 777, 2049, N - 1])
+    net = orc.Net(arch, S=1, M=M, Q=Q)
+    Ho = orc.build_H(net, orc.gen_weights(net, 1), X[rows], threads=8)
+    assert np.abs(H[torch.from_numpy(rows).cuda()].cpu().numpy() - Ho).max() <= H_TOL
+    # solver isolation at n = 1025: the oracle's Householder lstsq of the same fp32 H
+    b_iso, i_iso = orc.lstsq(H.double().cpu().numpy(), Y.astype(np.float64))
+    assert info.status == i_iso.status
+    cond = np.linalg.cond(i_iso.R[:M, :M])
+    rel = np.linalg.norm(beta.cpu().numpy() - b_iso) / np.linalg.norm(b_iso)
+    print(f"{arch} M=1024: cond(R)={cond:.2e} status={info.status} rel dbeta={rel:.2e}")
+    assert rel <= (1e-4 if info.status else max(1e-10, 1e-12 * cond))
+    assert info.rmse == pytest.approx(i_iso.rmse, rel=1e-6)
+
+
+# ------------------------------------------------------------------------- NARMAX error feedback (8(f) row 4)
+@pytest.mark.parametrize("N,S,M,Q,o", [(1000, 1, 64, 20, {}), (333, 4, 37, 10, {"F": 3, "R": 7, "act": 1}),
+                                       (100, 1, 5, 1, {}), (257, 2, 16, 12, {"F": 0, "R": 12})])
+def test_narmax_error_window_build_parity(N, S, M, Q, o):
+    """elmrnn_build_H_ef against the oracle's Eq.-7 t-loop on the same error window."""
+    X, Y, Yfb = inputs(N, Q, S, seed=N, kind="ar5")
+    Ef = np.random.default_rng(N).standard_normal((N, Q)).astype(np.float32)
+    e = E("narmax", S, M, Q, 6, **o)
+    Hg = e.build_H(torch.from_numpy(X).cuda(), torch.from_numpy(Yfb).cuda(),
+                   Ef=torch.from_numpy(Ef).cuda()).cpu().numpy().astype(np.float64)
+    net = oracle_net("narmax", S, M, Q, **o)
+    Ho = orc.build_H(net, orc.gen_weights(net, 6), X, Yfb, threads=8, Ef=Ef)
+    assert np.abs(Hg - Ho).max() <= H_TOL
+    # Ef = 0 is exactly the one-pass build
+    H0 = e.build_H(torch.from_numpy(X).cuda(), torch.from_numpy(Yfb).cuda()).cpu().numpy()
+    Hz = e.build_H(torch.from_numpy(X).cuda(), torch.from_numpy(Yfb).cuda(),
+                   Ef=torch.zeros(N, Q, device="cuda")).cpu().numpy()
+    np.testing.assert_array_equal(H0, Hz)
+
+
+def test_narmax_error_windows_parity():
+    """elmrnn_error_windows against the oracle's definition on the same fp32 H and beta."""
+    N, M, Q = 5000, 64, 20
+    g = torch.Generator(device="cuda").manual_seed(3)
+    H = torch.rand(N, M, device="cuda", generator=g)
+    Y = torch.randn(N, device="cuda", generator=g)
+    beta = torch.randn(M, device="cuda", dtype=torch.float64, generator=g)
+    e = E("narmax", 1, M, Q, 1)
+    Ef = e.error_windows(H, Y, beta).cpu().numpy()
+    ref = orc.error_windows(H.double().cpu().numpy(), Y.double().cpu().numpy(), beta.cpu().numpy(), Q)
+    scale = np.abs(ref).max()
+    assert np.abs(Ef - ref).max() <= 4e-7 * scale
+    assert (Ef[:Q][np.arange(Q)[:, None] + np.arange(Q)[None, :] < Q - 1] == 0).all()   # k < 0 entries
+
+
+def test_narmax_two_pass_train_parity():
+    """Two-pass NARMAX training end to end (C2 shape, 20k rows) against the oracle's two-pass method."""
+    N, M, Q = 20000, 64, 20
+    s = sy.series("ar5", N + Q + 1, seed=4)
+    X, Y, Yfb = sy.windows(s[:, :1], N, Q)
+    e = E("narmax", 1, M, Q, 1)
+    Xd, Yd, Yfbd = (torch.from_numpy(a).cuda() for a in (X, Y, Yfb))
+    H1, b1, i1, b0, i0 = e.train_narmax_ef(Xd, Yd, Yfbd)
+    net = orc.Net("narmax", S=1, M=M, Q=Q)
+    Ho1, bo1, io1, bo0, io0 = orc.train_narmax_ef(net, orc.gen_weights(net, 1), X, Y, Yfb, threads=8)
+    Hg1 = H1.cpu().numpy().astype(np.float64)
+    assert np.abs(Hg1 - Ho1).max() <= H_TOL
+    tol_b, tol_r, floor, ratio = solve_tolerances(Hg1, Ho1, Y, bo1, io1)
+    rel = np.linalg.norm(b1.cpu().numpy() - bo1) / np.linalg.norm(bo1)
+    print(f"narmax-ef: rmse pass0 {i0.rmse:.6f} pass1 {i1.rmse:.6f}; rel dbeta {rel:.2e} (tol {tol_b:.2e})")
+    assert rel <= tol_b
+    assert abs(i1.rmse - io1.rmse) / io1.rmse <= tol_r
+    assert abs(i0.rmse - io0.rmse) / io0.rmse <= 1e-4
