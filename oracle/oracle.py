@@ -12,6 +12,10 @@ Paper: El Zini, Rizk, Awad, arXiv 1911.13252 ("P:n" = PAPER.md line n).
   * ``lstsq``    -- S4.2: Householder QR of [H | Y], z = Q^T Y,
     back substitution; rank check + ridge fallback (R19).
   * ``predict``  -- Eq. 4, no output bias (R16).
+  * ``error_windows`` / ``train_narmax_ef`` -- Eq. 7 with e = y - yhat (P:122),
+    two passes (reading R30).
+  * ``test_rmse`` / ``forecast`` -- held-out RMSE and the free-running
+    recursive forecast (reading R31).
 """
 from __future__ import annotations
 
@@ -268,3 +272,28 @@ def rng_u64(z: int) -> int:
 
 def max_threads() -> int:
     return lib().orc_max_threads()
+
+
+def test_rmse(net: Net, blocks, X, Y, beta, Yfb=None, threads: int = 1) -> float:
+    """Held-out RMSE (SPEC "rmse_test"): sqrt(mean((yhat - y)^2))
+    with yhat = H(Q) beta (Eq. 4) on the evaluation windows."""
+    yhat = predict(build_H(net, blocks, X, Yfb, threads=threads), beta)
+    d = yhat - np.asarray(Y, dtype=np.float64).reshape(-1)
+    return float(np.sqrt(np.mean(d * d)))
+
+
+def forecast(net: Net, blocks, X, beta, K: int, threads: int = 1) -> np.ndarray:
+    """Free-running (recursive) K-step forecast (SPEC "recursive
+    self-feedback mode"; reading R31).  Univariate autoregressive windows (d = 1):
+    window w_0 = X[i] (s[i..i+Q-1]); step k predicts yhat_k = H(w_k) beta (Eq. 4;
+    Jordan/NARMAX feedback y(tau) = w_k[tau], the Yfb = NULL convention, R7), then
+    w_{k+1} = (w_k[1:], fp32(yhat_k)): the prediction replaces the next observation.
+    Returns fp64 [N][K]."""
+    assert net.S == 1
+    W = np.ascontiguousarray(np.asarray(X, dtype=np.float32).reshape(X.shape[0], -1)[:, :net.Q])
+    out = np.zeros((W.shape[0], K), dtype=np.float64)
+    for k in range(K):
+        yhat = predict(build_H(net, blocks, W, None, threads=threads), beta)
+        out[:, k] = yhat
+        W = np.ascontiguousarray(np.concatenate([W[:, 1:], yhat.astype(np.float32)[:, None]], axis=1))
+    return out
