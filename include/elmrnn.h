@@ -184,6 +184,28 @@ ELMRNN_API int64_t elmrnn_packed_r_len(elmrnn_t h);
 ELMRNN_API elmrnn_status elmrnn_predict(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb,
                              int64_t ldy, int64_t N, const double* beta, float* Yhat);
 
+/* Free-running (recursive) K-step forecast (reading R31):
+ * for univariate autoregressive windows (d = 1), w_0 = X[i][0..Q-1]; step k
+ * computes yhat_k = H(w_k) . beta (Eq. 4; Jordan/NARMAX feed back
+ * y(tau) = w_k[tau], the Yfb == NULL convention of elmrnn_build_H) and shifts
+ * the prediction in as the next observation: w_{k+1} = (w_k[1:], fp32(yhat_k)).
+ *   X dev fp32 [N][ldx], ldx >= Q; beta dev fp64 [M];
+ *   Yhat dev fp32 [N][ldyh] output, Yhat[i][k] = yhat_k of window i, ldyh >= K.
+ * Runs K (build_H, predict-and-shift) rounds on the handle's stream with a
+ * library workspace of N*(Q+1) + N*M floats.  N == 0 or K == 0 is a no-op.
+ * Errors: ARG, SHAPE, UNSUPPORTED (d != 1, Q > 128), OOM, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_forecast(elmrnn_t h, const float* X, int64_t ldx, int64_t N,
+                              const double* beta, int K, float* Yhat, int64_t ldyh);
+
+/* Held-out RMSE (SPEC "rmse_test"): sqrt(mean_i (yhat_i - Y_i)^2)
+ * with yhat = elmrnn_predict(X, Yfb, beta) on evaluation windows; fp64
+ * accumulation in one CTA (fixed order).  X, Yfb as elmrnn_build_H; Y dev fp32
+ * [N]; rmse host fp64 (the call synchronises the stream).
+ * Errors: ARG (N < 1), SHAPE, OOM, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_test_rmse(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb,
+                               int64_t ldy, const float* Y, int64_t N, const double* beta,
+                               double* rmse);
+
 /* Parity hook: copy logical weight block block_id (DESIGN.md "Weights" block
  * map, row-major logical layout) to host_dst (count floats, must equal the
  * block's length).  Synchronous.  Errors: ARG, CUDA. */

@@ -221,6 +221,16 @@ int64_t elmrnn_packed_r_len(elmrnn_t h) {
     return (int64_t)(h->M + 1) * (h->M + 2) / 2;
 }
 
+static cudaError_t ensure_hws(elmrnn* h, int64_t N) {
+    if (N <= h->Hws_rows) return cudaSuccess;
+    if (h->Hws) cudaFree(h->Hws);
+    h->Hws = nullptr;
+    h->Hws_rows = 0;
+    cudaError_t e = cudaMalloc(&h->Hws, sizeof(float) * N * h->M);
+    if (!e) h->Hws_rows = N;
+    return e;
+}
+
 elmrnn_status elmrnn_predict(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy, int64_t N,
                              const double* beta, float* Yhat) {
     if (!h) return ELMRNN_ERR_ARG;
@@ -230,16 +240,68 @@ elmrnn_status elmrnn_predict(elmrnn_t h, const float* X, int64_t ldx, const floa
     if (ldx < (int64_t)h->Q * h->S) return fail(h, ELMRNN_ERR_SHAPE, "ldx < Q*d");
     if (Yfb && ldy < h->Q) return fail(h, ELMRNN_ERR_SHAPE, "ldy < Q");
     cudaError_t e;
-    if (N > h->Hws_rows) {
-        if (h->Hws) cudaFree(h->Hws);
-        h->Hws = nullptr;
-        h->Hws_rows = 0;
-        if ((e = cudaMalloc(&h->Hws, sizeof(float) * N * h->M))) return cuda_fail(h, e, "predict workspace");
-        h->Hws_rows = N;
-    }
+    if ((e = ensure_hws(h, N))) return cuda_fail(h, e, "predict workspace");
     elmrnn_status st = build_impl(h, X, ldx, Yfb, ldy, N, h->Hws, h->M);
     if (st != ELMRNN_OK) return st;
     if ((e = launch_predict_gemv(h, h->Hws, h->M, N, beta, Yhat))) return cuda_fail(h, e, "predict");
+    return ELMRNN_OK;
+}
+
+static int64_t forecast_ldw(const elmrnn* h) { return (h->Q + 3) & ~3; }   // 16-B aligned window rows
+
+elmrnn_status elmrnn_forecast(elmrnn_t h, const float* X, int64_t ldx, int64_t N, const double* beta, int K,
+                              float* Yhat, int64_t ldyh) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (h->S != 1) return fail(h, ELMRNN_ERR_UNSUPPORTED, "free-running forecast needs a univariate window (d = 1)");
+    if (h->Q > 128) return fail(h, ELMRNN_ERR_UNSUPPORTED, "forecast supports Q <= 128");
+    if (N < 0 || K < 0) return fail(h, ELMRNN_ERR_ARG, "N < 0 or K < 0");
+    if (N == 0 || K == 0) return ELMRNN_OK;
+    if (!X || !beta || !Yhat) return fail(h, ELMRNN_ERR_ARG, "NULL pointer");
+    if (ldx < h->Q) return fail(h, ELMRNN_ERR_SHAPE, "ldx < Q");
+    if (ldyh < K) return fail(h, ELMRNN_ERR_SHAPE, "ldyh < K");
+    cudaError_t e;
+    const int64_t ldw = forecast_ldw(h);
+    if (N > h->fws_rows) {
+        if (h->fws) cudaFree(h->fws);
+        h->fws = nullptr;
+        h->fws_rows = 0;
+        if ((e = cudaMalloc(&h->fws, sizeof(float) * N * (ldw + 1)))) return cuda_fail(h, e, "forecast workspace");
+        h->fws_rows = N;
+    }
+    if ((e = ensure_hws(h, N))) return cuda_fail(h, e, "forecast workspace");
+    if ((e = launch_window_init(h, X, ldx, N, h->fws, ldw))) return cuda_fail(h, e, "forecast");
+    for (int k = 0; k < K; ++k) {
+        elmrnn_status st = build_impl(h, h->fws, ldw, nullptr, 0, N, h->Hws, h->M);
+        if (st != ELMRNN_OK) return st;
+        if ((e = launch_predict_shift(h, h->Hws, h->M, N, beta, h->fws, ldw, Yhat + k, ldyh)))
+            return cuda_fail(h, e, "forecast");
+    }
+    return ELMRNN_OK;
+}
+
+elmrnn_status elmrnn_test_rmse(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy,
+                               const float* Y, int64_t N, const double* beta, double* rmse) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (N < 1) return fail(h, ELMRNN_ERR_ARG, "N < 1");
+    if (!X || !Y || !beta || !rmse) return fail(h, ELMRNN_ERR_ARG, "NULL pointer");
+    if (ldx < (int64_t)h->Q * h->S) return fail(h, ELMRNN_ERR_SHAPE, "ldx < Q*d");
+    if (Yfb && ldy < h->Q) return fail(h, ELMRNN_ERR_SHAPE, "ldy < Q");
+    cudaError_t e;
+    if (N > h->fws_rows) {
+        if (h->fws) cudaFree(h->fws);
+        h->fws = nullptr;
+        h->fws_rows = 0;
+        if ((e = cudaMalloc(&h->fws, sizeof(float) * N * (forecast_ldw(h) + 1)))) return cuda_fail(h, e, "workspace");
+        h->fws_rows = N;
+    }
+    if (!h->dscr && (e = cudaMalloc(&h->dscr, sizeof(double)))) return cuda_fail(h, e, "workspace");
+    float* yhat = h->fws + (size_t)N * forecast_ldw(h);
+    elmrnn_status st = elmrnn_predict(h, X, ldx, Yfb, ldy, N, beta, yhat);
+    if (st != ELMRNN_OK) return st;
+    if ((e = launch_rmse(h, yhat, Y, N, h->dscr))) return cuda_fail(h, e, "test_rmse");
+    if ((e = cudaMemcpyAsync(rmse, h->dscr, sizeof(double), cudaMemcpyDeviceToHost, h->stream)) ||
+        (e = cudaStreamSynchronize(h->stream)))
+        return cuda_fail(h, e, "test_rmse");
     return ELMRNN_OK;
 }
 
@@ -274,7 +336,7 @@ const char* elmrnn_last_error(elmrnn_t h) { return h ? h->err.c_str() : g_init_e
 void elmrnn_destroy(elmrnn_t h) {
     if (!h) return;
     cudaFree(h->W); cudaFree(h->b); cudaFree(h->rec); cudaFree(h->tc_ops);
-    cudaFree(h->Rws); cudaFree(h->sdev); cudaFree(h->flag); cudaFree(h->Hws); cudaFree(h->rws); cudaFree(h->scratch);
+    cudaFree(h->Rws); cudaFree(h->sdev); cudaFree(h->flag); cudaFree(h->Hws); cudaFree(h->rws); cudaFree(h->fws); cudaFree(h->dscr); cudaFree(h->scratch);
     if (h->shost) cudaFreeHost(h->shost);
     delete h;
 }

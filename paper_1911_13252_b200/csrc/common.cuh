@@ -57,6 +57,9 @@ struct elmrnn {
     float* Hws;           // predict scratch
     float* rws;           // error-window scratch: residual per row (N floats)
     int64_t rws_rows;
+    float* fws;           // forecast window buffer [N][ldw] + predict output [N]
+    int64_t fws_rows;
+    double* dscr;         // device scalar (held-out RMSE)
     int64_t Hws_rows;
     float* scratch;       // builder scratch (FC history ring)
     size_t scratch_bytes;
@@ -77,6 +80,10 @@ cudaError_t launch_elman(elmrnn* h, const float* X, int64_t ldx, int64_t N, floa
 cudaError_t launch_diag_gated(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
 cudaError_t launch_teacher_forced(elmrnn* h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy,
                                   int64_t N, float* H, int64_t ldh, const float* Ef = nullptr, int64_t lde = 0);
+cudaError_t launch_window_init(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* w, int64_t ldw);
+cudaError_t launch_predict_shift(elmrnn* h, const float* H, int64_t ldh, int64_t N, const double* beta, float* w,
+                                 int64_t ldw, float* yout, int64_t ldyo);
+cudaError_t launch_rmse(elmrnn* h, const float* yhat, const float* y, int64_t N, double* out);
 cudaError_t launch_error_windows(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t N,
                                  const double* beta, float* Ef, int64_t lde);
 cudaError_t launch_dense_fma(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);

@@ -1670,41 +1670,3 @@ cudaError_t launch_predict_gemv(elmrnn* h, const float* H, int64_t ldh, int64_t 
 }
 
 }  // namespace elm
-
-namespace elm {
-// ---- NARMAX error feedback (Eq. 7, e(t) = y(t) - yhat(t) P:122; reading R30) ----
-// r_k = Y_k - H_k . beta (Eq. 4, fp64 accumulation, rounded once), then
-// Ef[i][tau-1] = r_{i+tau-Q} (0 when i+tau-Q < 0): rows are consecutive
-// stride-1 windows of one series (R22).
-__global__ void k_residual(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t N, int M,
-                           const double* __restrict__ beta, float* __restrict__ r) {
-    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (row >= N) return;
-    double s = 0.0;
-    for (int j = lane; j < M; j += 32) s += (double)H[row * ldh + j] * beta[j];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) r[row] = (float)((double)Y[row] - s);
-}
-
-__global__ void k_error_windows(const float* __restrict__ r, int64_t N, int Q, float* __restrict__ Ef, int64_t lde) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N * Q; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = e / Q;
-        const int tau = (int)(e - i * Q) + 1;
-        const int64_t k = i + tau - Q;
-        Ef[i * lde + tau - 1] = k >= 0 ? r[k] : 0.0f;
-    }
-}
-
-cudaError_t launch_error_windows(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t N,
-                                 const double* beta, float* Ef, int64_t lde) {
-    const int64_t blocks = (N * 32 + 255) / 256;
-    if (blocks > INT32_MAX) return cudaErrorInvalidConfiguration;
-    k_residual<<<(unsigned)blocks, 256, 0, h->stream>>>(H, ldh, Y, N, h->M, beta, h->rws);
-    h->launches++;
-    const int64_t b2 = std::min<int64_t>((N * h->Q + 255) / 256, (int64_t)h->sm_count * 16);
-    k_error_windows<<<(unsigned)b2, 256, 0, h->stream>>>(h->rws, N, h->Q, Ef, lde);
-    h->launches++;
-    return cudaGetLastError();
-}
-}  // namespace elm

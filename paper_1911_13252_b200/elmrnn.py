@@ -23,7 +23,7 @@ STATUS = {0: "OK", 1: "WARN_RIDGE", -1: "ERR_ARG", -2: "ERR_SHAPE", -3: "ERR_UND
           -4: "ERR_NONFINITE", -5: "ERR_UNSUPPORTED", -6: "ERR_CUDA", -7: "ERR_OOM"}
 
 EXPORTED = ("elmrnn_opts_default", "elmrnn_init", "elmrnn_init_ex", "elmrnn_set_stream", "elmrnn_build_H",
-            "elmrnn_build_H_ef", "elmrnn_error_windows",
+            "elmrnn_build_H_ef", "elmrnn_error_windows", "elmrnn_forecast", "elmrnn_test_rmse",
             "elmrnn_solve_beta", "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_packed_r_len",
             "elmrnn_predict", "elmrnn_get_weights", "elmrnn_weight_block_len", "elmrnn_path",
             "elmrnn_launch_count", "elmrnn_last_error", "elmrnn_destroy")
@@ -77,6 +77,8 @@ def lib() -> ctypes.CDLL:
         L.elmrnn_build_H.argtypes = [vp, vp, i64, vp, i64, i64, vp, i64]
         L.elmrnn_build_H_ef.argtypes = [vp, vp, i64, vp, i64, vp, i64, i64, vp, i64]
         L.elmrnn_error_windows.argtypes = [vp, vp, i64, vp, i64, vp, vp, i64]
+        L.elmrnn_forecast.argtypes = [vp, vp, i64, i64, vp, i32, vp, i64]
+        L.elmrnn_test_rmse.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, vp]
         L.elmrnn_solve_beta.argtypes = [vp, vp, i64, vp, i64, vp, vp]
         L.elmrnn_solve_local.argtypes = [vp, vp, i64, vp, i64, vp]
         L.elmrnn_solve_merge.argtypes = [vp, vp, i32, i64, vp, vp]
@@ -94,7 +96,7 @@ def lib() -> ctypes.CDLL:
         L.elmrnn_destroy.argtypes = [vp]
         L.elmrnn_destroy.restype = None
         for f in ("elmrnn_init", "elmrnn_init_ex", "elmrnn_set_stream", "elmrnn_build_H", "elmrnn_build_H_ef",
-                  "elmrnn_error_windows", "elmrnn_solve_beta",
+                  "elmrnn_error_windows", "elmrnn_forecast", "elmrnn_test_rmse", "elmrnn_solve_beta",
                   "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_predict", "elmrnn_get_weights",
                   "elmrnn_path"):
             getattr(L, f).restype = i32
@@ -290,6 +292,31 @@ class ELMRNN:
         self._stream()
         self._check(lib().elmrnn_predict(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, N, _ptr(beta), _ptr(out)))
         return out
+
+    def forecast(self, X: torch.Tensor, beta: torch.Tensor, K: int):
+        """elmrnn_forecast: free-running K-step forecast of univariate windows -> fp32 [N][K]."""
+        _dev_check(X, "X", torch.float32)
+        _dev_check(beta, "beta", torch.float64)
+        N = X.shape[0]
+        ldx = _rows(X, "X")[0] if N else self.Q
+        out = torch.empty((N, K), dtype=torch.float32, device=X.device)
+        self._stream()
+        self._check(lib().elmrnn_forecast(self._h, _ptr(X), ldx, N, _ptr(beta), K, _ptr(out), max(K, 1)))
+        return out
+
+    def test_rmse(self, X: torch.Tensor, Y: torch.Tensor, beta: torch.Tensor, Yfb: torch.Tensor | None = None) -> float:
+        """elmrnn_test_rmse: held-out RMSE of beta on evaluation windows."""
+        _dev_check(X, "X", torch.float32)
+        _dev_check(Y, "Y", torch.float32)
+        _dev_check(beta, "beta", torch.float64)
+        N = X.shape[0]
+        ldx = _rows(X, "X")[0] if N else self.Q * self.d
+        ldy = _rows(Yfb, "Yfb")[0] if Yfb is not None else 0
+        r = ctypes.c_double()
+        self._stream()
+        self._check(lib().elmrnn_test_rmse(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, _ptr(Y), N, _ptr(beta),
+                                           ctypes.byref(r)))
+        return r.value
 
     def get_weights(self, block_id: int):
         """elmrnn_get_weights: logical weight block as a flat float32 CPU tensor."""

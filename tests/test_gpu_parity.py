@@ -552,3 +552,61 @@ def test_narmax_two_pass_train_parity():
     assert rel <= tol_b
     assert abs(i1.rmse - io1.rmse) / io1.rmse <= tol_r
     assert abs(i0.rmse - io0.rmse) / io0.rmse <= 1e-4
+
+
+# ------------------------------------------------------------------------- forecasting (8(f) row 3)
+FC_ARCHS = [("elman", 20, 10), ("jordan", 64, 20), ("narmax", 64, 20), ("fc", 50, 10), ("lstm", 32, 10),
+            ("lstm", 128, 30), ("gru", 128, 30), ("gru", 40, 12), ("lstm_diag", 33, 10), ("gru_diag", 33, 10),
+            ("fc_eq8", 20, 12)]
+
+
+@pytest.mark.parametrize("arch,M,Q", FC_ARCHS)
+def test_forecast_per_step_parity(arch, M, Q):
+    """Each forecast step k against the oracle's Eq. 4 on the window the GPU
+    itself fed back (w_k = X shifted by the GPU's own fp32 predictions), so
+    the check does not compound; then the whole trajectory against the
+    oracle's forecast for a contractive beta."""
+    N, K = 300, 6
+    X, Y, _ = inputs(N, Q, 1, seed=M + Q)
+    beta = np.random.default_rng(M).standard_normal(M) / M
+    e = E(arch, 1, M, Q, 8)
+    bd = torch.from_numpy(beta).cuda()
+    Yh = e.forecast(torch.from_numpy(X).cuda(), bd, K).cpu().numpy()
+    net = orc.Net(arch, S=1, M=M, Q=Q)
+    bl = orc.gen_weights(net, 8)
+    tol = 1e-5 * max(1.0, np.abs(beta).sum())
+    W = X[:, :, 0].copy()
+    for k in range(K):
+        ref = orc.predict(orc.build_H(net, bl, W[:, :, None], threads=8), beta)
+        assert np.abs(Yh[:, k] - ref).max() <= tol, k
+        W = np.concatenate([W[:, 1:], Yh[:, k:k + 1]], axis=1)
+    full = orc.forecast(net, bl, X, beta, K, threads=8)
+    assert np.abs(Yh - full).max() <= 10 * tol
+
+
+def test_forecast_errors_and_empty():
+    from paper_1911_13252_b200 import ElmrnnError
+    e = E("gru", 2, 8, 4, 1)
+    with pytest.raises(ElmrnnError, match="UNSUPPORTED"):
+        e.forecast(torch.zeros(5, 4, 2, device="cuda"), torch.zeros(8, dtype=torch.float64, device="cuda"), 3)
+    e1 = E("gru", 1, 8, 4, 1)
+    assert e1.forecast(torch.zeros(0, 4, 1, device="cuda"), torch.zeros(8, dtype=torch.float64, device="cuda"),
+                       3).shape == (0, 3)
+
+
+@pytest.mark.parametrize("arch,M,Q,S", [("gru", 32, 10, 1), ("lstm", 256, 20, 1), ("narmax", 64, 20, 1),
+                                        ("fc", 128, 10, 4)])
+def test_test_rmse_parity(arch, M, Q, S):
+    """Held-out RMSE of a beta trained on the first windows, evaluated on later ones."""
+    Ntr, Nte = 3000, 1000
+    kind = "sin4" if S == 4 else ("ar5" if arch == "narmax" else "mg")
+    s = sy.series(kind, Ntr + Nte + Q + 1, seed=9)
+    X, Y, _ = sy.windows(s[:, :S], Ntr + Nte, Q)
+    e = E(arch, S, M, Q, 2)
+    Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+    _, beta, _ = e.train(Xd[:Ntr], Yd[:Ntr])
+    r = e.test_rmse(Xd[Ntr:], Yd[Ntr:], beta)
+    b = beta.cpu().numpy()
+    net = orc.Net(arch, S=S, M=M, Q=Q)
+    ref = orc.test_rmse(net, orc.gen_weights(net, 2), X[Ntr:], Y[Ntr:], b, threads=8)
+    assert abs(r - ref) <= 1e-5 * max(1.0, np.abs(b).sum()), (r, ref)
