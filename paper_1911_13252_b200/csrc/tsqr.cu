@@ -966,6 +966,12 @@ __device__ __forceinline__ double rcp_nr(double d) {
     return fma(r, e, r);
 }
 
+// Panel factorisation by one warp.  Lane = (row group rg, column pair cp):
+// rows rg, rg+4, ... of panel columns 2cp, 2cp+1 in registers.  Per column i
+// the critical path is ONE shuffle round (v = column i from its owner lanes)
+// and ONE 2-level butterfly that reduces |v|^2 and both dot products v^T a
+// together; every lane then forms the reflector itself from identical bits
+// (commutative butterfly sums), so g, u0 and beta need no broadcast.
 template <int ROWS>
 __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, int nbp, double* Rd, double* cgv,
                                       double* cuv) {
@@ -981,7 +987,9 @@ __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, in
     }
     // R entries of row i are read one column ahead: row i+1 is untouched until reflector i+1
     double x0n = Rd[0], rd0n = Rd[c0], rd1n = Rd[c1];
-#pragma unroll
+    // two columns per loop body (the column parity selects a0 / a1 at compile
+    // time); a full 16-column unroll overflows the instruction cache
+#pragma unroll 2
     for (int i = 0; i < kNBW; ++i) {
         if (i >= nbp) break;
         constexpr unsigned F = 0xffffffffu;
@@ -992,67 +1000,57 @@ __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, in
             rd0n = Rd[(i + 1) * kNBW + c0];
             rd1n = Rd[(i + 1) * kNBW + c1];
         }
-        // ---- reflector of panel column i (owner lanes cp == i/2; all 4 compute it)
-        double s2a = 0.0, s2b = 0.0;
+        double v[RPL];
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) v[r] = __shfl_sync(F, (i & 1) ? a1[r] : a0[r], src);
+        double s2a = 0.0, s2b = 0.0, w0 = 0.0, w0b = 0.0, w1 = 0.0, w1b = 0.0;
 #pragma unroll
         for (int r = 0; r < RPL; r += 2) {
-            const double x = (i & 1) ? a1[r] : a0[r], y = (i & 1) ? a1[r + 1] : a0[r + 1];
-            s2a = fma(x, x, s2a);
-            s2b = fma(y, y, s2b);
+            s2a = fma(v[r], v[r], s2a);
+            s2b = fma(v[r + 1], v[r + 1], s2b);
+            w0 = fma(v[r], a0[r], w0);
+            w0b = fma(v[r + 1], a0[r + 1], w0b);
+            w1 = fma(v[r], a1[r], w1);
+            w1b = fma(v[r + 1], a1[r + 1], w1b);
         }
         double s2 = s2a + s2b;
+        w0 += w0b;
+        w1 += w1b;
         s2 += __shfl_xor_sync(F, s2, 8);
+        w0 += __shfl_xor_sync(F, w0, 8);
+        w1 += __shfl_xor_sync(F, w1, 8);
         s2 += __shfl_xor_sync(F, s2, 16);
-        double g = 0.0, u0 = 0.0;
-        if (cp == (i >> 1)) {
-            // t <= 1e-280 is the H = I case of make_reflector (|beta u0| lies in [t, 2t]);
-            // testing t itself also keeps subnormal t away from rsqrt.approx.ftz,
-            // which flushes it to 0 (rs = inf, NaN reflector).  Subnormal t occurs
-            // in deep noise cascades of rank-deficient partial R (16-row tiles, n > 512).
-            const double t = fma(x0, x0, s2);
-            if (t > 1e-280) {
-                const double rs = rsqrt_nr(t);
-                const double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * (t * rs);
-                const double uu = x0 - beta;
-                if (fabs(beta * uu) > 1e-280) {   // see make_reflector
-                    u0 = uu;
-                    g = -rs * rs * rcp_nr(1.0 + fabs(x0) * rs);   // = 1 / (beta u0)
-                    if (rg == 0) Rd[i * kNBW + i] = beta;
-                }
+        w0 += __shfl_xor_sync(F, w0, 16);
+        w1 += __shfl_xor_sync(F, w1, 16);
+        // ---- reflector of panel column i (make_reflector semantics): s2 == 0 or
+        // t <= 1e-280 is H = I (|beta u0| lies in [t, 2t]); testing t also keeps a
+        // subnormal t away from rsqrt.approx.ftz, which would flush it to 0 (NaN
+        // reflector) -- it occurs in deep noise cascades of rank-deficient partial R
+        double g = 0.0, u0 = 0.0, beta = 0.0;
+        const double t = fma(x0, x0, s2);
+        if (s2 != 0.0 && t > 1e-280) {
+            const double rs = rsqrt_nr(t);
+            beta = -(x0 >= 0.0 ? 1.0 : -1.0) * (t * rs);
+            const double uu = x0 - beta;
+            if (fabs(beta * uu) > 1e-280) {
+                u0 = uu;
+                g = -rs * rs * rcp_nr(1.0 + fabs(x0) * rs);   // = 1 / (beta u0)
             }
+        }
+        if (cp == (i >> 1)) {
 #pragma unroll
-            for (int r = 0; r < RPL; ++r) C[(size_t)(rg + 4 * r) * LDC + p + i] = (i & 1) ? a1[r] : a0[r];
+            for (int r = 0; r < RPL; ++r) C[(size_t)(rg + 4 * r) * LDC + p + i] = v[r];
             if (rg == 0) {
                 cgv[i] = g;
                 cuv[i] = u0;
+                if (g != 0.0) Rd[i * kNBW + i] = beta;
             }
         }
-        g = __shfl_sync(F, g, i >> 1);
-        u0 = __shfl_sync(F, u0, i >> 1);
         if (g != 0.0 && i + 1 < nbp) {
-            // ---- apply H_i to the panel columns right of i; v by shuffle from the owner
-            double v[RPL];
-#pragma unroll
-            for (int r = 0; r < RPL; ++r) v[r] = __shfl_sync(F, (i & 1) ? a1[r] : a0[r], src);
+            // ---- apply H_i to the panel columns right of i: W_j = u0 R[i][j] + v^T a_j
             const bool l0 = c0 > i && c0 < nbp, l1 = c1 > i && c1 < nbp;
-            double w0 = (rg == 0 && l0) ? u0 * rd0 : 0.0;
-            double w1 = (rg == 0 && l1) ? u0 * rd1 : 0.0;
-            double w0b = 0.0, w1b = 0.0;
-#pragma unroll
-            for (int r = 0; r < RPL; r += 2) {
-                w0 = fma(v[r], a0[r], w0);
-                w1 = fma(v[r], a1[r], w1);
-                w0b = fma(v[r + 1], a0[r + 1], w0b);
-                w1b = fma(v[r + 1], a1[r + 1], w1b);
-            }
-            w0 += w0b;
-            w1 += w1b;
-            w0 += __shfl_xor_sync(F, w0, 8);
-            w1 += __shfl_xor_sync(F, w1, 8);
-            w0 += __shfl_xor_sync(F, w0, 16);
-            w1 += __shfl_xor_sync(F, w1, 16);
-            const double f0 = l0 ? g * w0 : 0.0;
-            const double f1 = l1 ? g * w1 : 0.0;
+            const double f0 = l0 ? g * fma(u0, rd0, w0) : 0.0;
+            const double f1 = l1 ? g * fma(u0, rd1, w1) : 0.0;
 #pragma unroll
             for (int r = 0; r < RPL; ++r) {
                 a0[r] = fma(f0, v[r], a0[r]);
@@ -1309,14 +1307,49 @@ __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
     const int64_t r1 = min(N, r0 + rows_per_cta);
     bool bad = false;
     const int pw = wy_panel_warp(sm_slot);
+    // 16-B vector loads of H when rows allow it, issued in batches of 8 per
+    // thread so the tile load is not a chain of dependent HBM round trips
+    const bool vec = (M % 4 == 0) && (ldh % 4 == 0) && ((reinterpret_cast<uintptr_t>(H) & 15) == 0);
+    const int M4 = M / 4, tail = LDC - M;
     for (int64_t base = r0; base < r1; base += ROWS) {
-        for (int r = 0; r < ROWS; ++r) {
-            const int64_t row = base + r;
-            for (int c = tid; c < LDC; c += nt) {
-                float x = 0.0f;
-                if (row < r1 && c < n) x = c < M ? __ldg(H + row * ldh + c) : __ldg(Y + row);
+        if (vec) {
+            constexpr int B = 8;
+            for (int e0 = tid; e0 < ROWS * M4; e0 += nt * B) {
+                float4 v[B];
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const int e = e0 + b * nt, r = e / M4, q = e - r * M4;
+                    v[b] = (e < ROWS * M4 && base + r < r1)
+                               ? __ldg(reinterpret_cast<const float4*>(H + (base + r) * ldh) + q)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const int e = e0 + b * nt, r = e / M4, q = e - r * M4;
+                    if (e < ROWS * M4) {
+                        bad |= !(isfinite(v[b].x) && isfinite(v[b].y) && isfinite(v[b].z) && isfinite(v[b].w));
+                        double2* d = reinterpret_cast<double2*>(C + (size_t)r * LDC + 4 * q);
+                        d[0] = make_double2(v[b].x, v[b].y);
+                        d[1] = make_double2(v[b].z, v[b].w);
+                    }
+                }
+            }
+            for (int e = tid; e < ROWS * tail; e += nt) {   // Y column, zero padding
+                const int r = e / tail, c = M + (e - r * tail);
+                const int64_t row = base + r;
+                const float x = (c == M && row < r1) ? __ldg(Y + row) : 0.0f;
                 bad |= !isfinite(x);
                 C[(size_t)r * LDC + c] = (double)x;
+            }
+        } else {
+            for (int r = 0; r < ROWS; ++r) {
+                const int64_t row = base + r;
+                for (int c = tid; c < LDC; c += nt) {
+                    float x = 0.0f;
+                    if (row < r1 && c < n) x = c < M ? __ldg(H + row * ldh + c) : __ldg(Y + row);
+                    bad |= !isfinite(x);
+                    C[(size_t)r * LDC + c] = (double)x;
+                }
             }
         }
         __syncthreads();
@@ -1417,6 +1450,17 @@ static int wy_rows(int n) {
     // 32-row tiles, 2-3 CTAs per SM (their panels overlap each other's trailing updates)
     return wy_smem_bytes(32, n) <= 220 * 1024 ? 32 : 16;
 }
+// Leaf dynamic shared memory: the tile + coefficients, optionally padded so
+// that at most ELMRNN_TSQR_WY_CTAS CTAs share an SM (testing aid: fewer
+// co-resident CTAs means less contention on each latency-bound panel warp).
+static size_t wy_leaf_smem(int rows, int n) {
+    size_t sm = wy_smem_bytes(rows, n);
+    if (const char* e = std::getenv("ELMRNN_TSQR_WY_CTAS")) {
+        const int c = std::atoi(e);
+        if (c >= 1) sm = std::max(sm, (size_t)(227 * 1024 / c - 1024 * c));
+    }
+    return std::min(sm, (size_t)227 * 1024);
+}
 static int wy_threads(int n) {
     int w = n <= 320 ? 4 : std::min(8, ((n + 1) / 2 + 31) / 32);
     if (const char* e = std::getenv("ELMRNN_TSQR_WY_WARPS")) w = std::max(1, std::min(8, std::atoi(e)));   // testing aid
@@ -1446,7 +1490,7 @@ int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
     const int threads = var_threads(v, n);
     int per_sm = use_wy(n) ? wy_dispatch(n, [&](auto rows) {
         constexpr int RW = decltype(rows)::value;
-        const size_t sm = wy_smem_bytes(RW, n);
+        const size_t sm = wy_leaf_smem(RW, n);
         cudaFuncSetAttribute(k_tsqr_leaf_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         int ps = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_tsqr_leaf_wy<RW>, wy_threads(n), sm);
@@ -1565,7 +1609,7 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
     if (use_wy(n)) {
         e = wy_dispatch(n, [&](auto rws) {
             constexpr int RW = decltype(rws)::value;
-            const size_t sm = wy_smem_bytes(RW, n);
+            const size_t sm = wy_leaf_smem(RW, n);
             cudaFuncSetAttribute(k_tsqr_leaf_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             int* slot = reinterpret_cast<int*>(h->sdev + 1);   // per-SM arrival counters (ensure_solve_ws)
             cudaMemsetAsync(slot, 0, 1024 * sizeof(int), h->stream);
