@@ -96,6 +96,9 @@ cudaError_t launch_dense_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, f
 bool gru_tc_supported(const elmrnn* h);
 cudaError_t gru_tc_prepare(elmrnn* h);
 cudaError_t launch_gru_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
+bool lstm_wide_supported(const elmrnn* h);
+size_t lstm_wide_wb_offset(const elmrnn* h);
+cudaError_t launch_lstm_wide(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
 bool fc_tc_supported(const elmrnn* h);
 cudaError_t fc_tc_prepare(elmrnn* h);
 cudaError_t launch_fc_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);

@@ -467,6 +467,7 @@ bool tc_supported(const elmrnn* h) {
     if (h->arch == kArchGRU) return gru_tc_supported(h);
     if (h->arch == kArchFC) return fc_tc_supported(h);
     if (h->arch != kArchLSTM) return false;
+    if (lstm_wide_supported(h)) return true;   // 256 < M <= 1024: hbuild_lstm_wide.cu
     if (h->M != 128 && h->M != 256) return false;
     if (h->S > 4) return false;
     return (tc_padded_s(h->S) + 1) * 4 * h->M <= kTcWbMax;
@@ -476,7 +477,9 @@ cudaError_t tc_prepare(elmrnn* h) {
     if (h->arch == kArchGRU) return gru_tc_prepare(h);
     if (h->arch == kArchFC) return fc_tc_prepare(h);
     const int M = h->M;
+    const bool wide = lstm_wide_supported(h);
     size_t bytes = (size_t)(M / 32) * (M / 64) * kTcStageBytes;
+    if (wide) bytes += sizeof(float) * (size_t)M * 4 * (tc_padded_s(h->S) + 1);   // W | b in global memory
     cudaError_t e;
     if ((e = cudaMalloc(&h->tc_ops, bytes))) return e;
     h->tc_ops_bytes = bytes;
@@ -501,6 +504,10 @@ cudaError_t tc_prepare(elmrnn* h) {
             d[0] = (float)(kg * b[g * M + j]);
             for (int s2 = 0; s2 < S; ++s2) d[1 + s2] = (float)(kg * W[(size_t)s2 * GM + g * M + j]);
         }
+    if (wide &&
+        (e = cudaMemcpyAsync(static_cast<uint8_t*>(h->tc_ops) + lstm_wide_wb_offset(h), h->tc_wb.data(),
+                             sizeof(float) * h->tc_wb.size(), cudaMemcpyHostToDevice, h->stream)))
+        return e;
     int64_t total = (int64_t)(M / 32) * (M / 64) * 128 * 64;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
     k_pack_u<<<blocks, 256, 0, h->stream>>>(h->rec, M, scale, static_cast<uint8_t*>(h->tc_ops));
@@ -523,6 +530,7 @@ cudaError_t launch_dense_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, f
     if (h->arch == kArchFC) return launch_fc_tc(h, X, ldx, N, H, ldh);
     if (h->M == 256) return launch_m<256>(h, X, ldx, N, H, ldh);
     if (h->M == 128) return launch_m<128>(h, X, ldx, N, H, ldh);
+    if (lstm_wide_supported(h)) return launch_lstm_wide(h, X, ldx, N, H, ldh);
     return cudaErrorNotSupported;
 }
 
