@@ -97,6 +97,9 @@ bool gru_tc_supported(const elmrnn* h);
 cudaError_t gru_tc_prepare(elmrnn* h);
 cudaError_t launch_gru_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
 bool lstm_wide_supported(const elmrnn* h);
+bool gru_wide_supported(const elmrnn* h);
+cudaError_t gru_wide_prepare(elmrnn* h);
+cudaError_t launch_gru_wide(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
 size_t lstm_wide_wb_offset(const elmrnn* h);
 cudaError_t launch_lstm_wide(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
 bool fc_tc_supported(const elmrnn* h);

@@ -464,7 +464,7 @@ cudaError_t launch_lstm_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, fl
 static int tc_padded_s(int S) { return S <= 1 ? 1 : (S <= 2 ? 2 : 4); }
 
 bool tc_supported(const elmrnn* h) {
-    if (h->arch == kArchGRU) return gru_tc_supported(h);
+    if (h->arch == kArchGRU) return gru_tc_supported(h) || gru_wide_supported(h);
     if (h->arch == kArchFC) return fc_tc_supported(h);
     if (h->arch != kArchLSTM) return false;
     if (lstm_wide_supported(h)) return true;   // 256 < M <= 1024: hbuild_lstm_wide.cu
@@ -474,7 +474,7 @@ bool tc_supported(const elmrnn* h) {
 }
 
 cudaError_t tc_prepare(elmrnn* h) {
-    if (h->arch == kArchGRU) return gru_tc_prepare(h);
+    if (h->arch == kArchGRU) return gru_tc_supported(h) ? gru_tc_prepare(h) : gru_wide_prepare(h);
     if (h->arch == kArchFC) return fc_tc_prepare(h);
     const int M = h->M;
     const bool wide = lstm_wide_supported(h);
@@ -526,7 +526,8 @@ static cudaError_t launch_m(elmrnn* h, const float* X, int64_t ldx, int64_t N, f
 }
 
 cudaError_t launch_dense_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh) {
-    if (h->arch == kArchGRU) return launch_gru_tc(h, X, ldx, N, H, ldh);
+    if (h->arch == kArchGRU)
+        return gru_tc_supported(h) ? launch_gru_tc(h, X, ldx, N, H, ldh) : launch_gru_wide(h, X, ldx, N, H, ldh);
     if (h->arch == kArchFC) return launch_fc_tc(h, X, ldx, N, H, ldh);
     if (h->M == 256) return launch_m<256>(h, X, ldx, N, H, ldh);
     if (h->M == 128) return launch_m<128>(h, X, ldx, N, H, ldh);

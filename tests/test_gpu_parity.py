@@ -432,30 +432,35 @@ def test_c5_sweep_H_parity(arch, M, Q):
 
 # tcgen05 LSTM builder for wide layers (hbuild_lstm_wide.cu, 256 < M <= 1024):
 # several 128-row tiles, ragged tail, more tiles than... S = 1, 2, 3 (padded to 4)
-WIDE_CASES = [(512, 300, 10, 1), (1024, 260, 3, 1), (384, 333, 7, 2), (640, 129, 5, 3), (512, 1000, 2, 1)]
+WIDE_CASES = [("lstm", 512, 300, 10, 1), ("lstm", 1024, 260, 3, 1), ("lstm", 384, 333, 7, 2),
+              ("lstm", 640, 129, 5, 3), ("lstm", 512, 1000, 2, 1),
+              # GRU (hbuild_gru_wide.cu, 128 < M <= 1024, M % 128 == 0): both phases streamed
+              ("gru", 256, 300, 10, 1), ("gru", 1024, 260, 3, 1), ("gru", 384, 333, 7, 2), ("gru", 640, 129, 5, 3),
+              ("gru", 512, 1000, 2, 4), ("gru", 256, 129, 1, 1)]
 
 
-@pytest.mark.parametrize("M,N,Q,S", WIDE_CASES)
-def test_lstm_wide_tc_parity(M, N, Q, S):
+@pytest.mark.parametrize("arch,M,N,Q,S", WIDE_CASES)
+def test_wide_tc_parity(arch, M, N, Q, S):
     X, Y, _ = inputs(N, Q, S, seed=M + Q)
-    e, Hg = gpu_H("lstm", S, M, Q, 4, X)
+    e, Hg = gpu_H(arch, S, M, Q, 4, X)
     assert e.path == 2
-    net = orc.Net("lstm", S=S, M=M, Q=Q)
+    net = orc.Net(arch, S=S, M=M, Q=Q)
     Ho = orc.build_H(net, orc.gen_weights(net, 4), X, threads=8)
     err = np.abs(Hg - Ho).max()
     assert err <= H_TOL, f"max |dH| = {err:.3e}"
 
 
-def test_lstm_wide_tc_two_pass_and_many_tiles():
+@pytest.mark.parametrize("arch", ["lstm", "gru"])
+def test_wide_tc_two_pass_and_many_tiles(arch):
     """fp16-grid weights (2-pass MMA) and more tiles than SMs (persistent CTAs
     loop over tiles: the history slots and c state are reused across tiles)."""
     M, Q, S = 512, 4, 1
     N = 128 * 148 + 77
     X, Y, _ = inputs(N, Q, S, seed=5)
-    e, Hg = gpu_H("lstm", S, M, Q, 4, X, weight_grid=1)
+    e, Hg = gpu_H(arch, S, M, Q, 4, X, weight_grid=1)
     assert e.path == 2
     rows = np.r_[0:130, N - 300:N]
-    net = orc.Net("lstm", S=S, M=M, Q=Q, weight_grid=1)
+    net = orc.Net(arch, S=S, M=M, Q=Q, weight_grid=1)
     Ho = orc.build_H(net, orc.gen_weights(net, 4), X[rows], threads=8)
     assert np.abs(Hg[rows] - Ho).max() <= H_TOL
 
