@@ -297,3 +297,14 @@ def forecast(net: Net, blocks, X, beta, K: int, threads: int = 1) -> np.ndarray:
         out[:, k] = yhat
         W = np.ascontiguousarray(np.concatenate([W[:, 1:], yhat.astype(np.float32)[:, None]], axis=1))
     return out
+
+
+def lstsq_multi(H, Y):
+    """Multi-output least squares (the paper's future work P:655):
+    the P outputs are independent problems beta_p = argmin ||H beta - Y[:, p]||, each
+    solved by the single-output Householder lstsq above.  Returns (B [P][M], [SolveInfo])."""
+    Y = np.asarray(Y, dtype=np.float64)
+    if Y.ndim == 1:
+        Y = Y[:, None]
+    out = [lstsq(H, Y[:, p]) for p in range(Y.shape[1])]
+    return np.stack([b for b, _ in out]), [i for _, i in out]

@@ -1445,7 +1445,8 @@ static bool use_wy(int n) {
 static int wy_rows(int n) {
     if (const char* e = std::getenv("ELMRNN_TSQR_WY_ROWS")) {   // testing aid
         const int r = std::atoi(e);
-        if ((r == 96 || r == 64 || r == 32 || r == 24 || r == 16) && wy_smem_bytes(r, n) <= 220 * 1024) return r;
+        if ((r == 96 || r == 64 || r == 32 || r == 24 || r == 16 || r == 8) && wy_smem_bytes(r, n) <= 220 * 1024)
+            return r;
     }
     // 32-row tiles, 2-3 CTAs per SM (their panels overlap each other's trailing updates)
     return wy_smem_bytes(32, n) <= 220 * 1024 ? 32 : 16;
@@ -1473,6 +1474,7 @@ static auto wy_dispatch(int n, F&& f) {
     case 64: return f(std::integral_constant<int, 64>{});
     case 32: return f(std::integral_constant<int, 32>{});
     case 24: return f(std::integral_constant<int, 24>{});
+    case 8: return f(std::integral_constant<int, 8>{});
     default: return f(std::integral_constant<int, 16>{});
     }
 }
@@ -1481,7 +1483,8 @@ template <class F>
 static auto wy_dispatch_merge(int n, F&& f) {
     if (wy_smem_bytes(96, n) <= 220 * 1024) return f(std::integral_constant<int, 96>{});
     if (wy_smem_bytes(64, n) <= 220 * 1024) return f(std::integral_constant<int, 64>{});
-    return wy_dispatch(n, f);
+    if (wy_smem_bytes(32, n) <= 220 * 1024) return f(std::integral_constant<int, 32>{});
+    return f(std::integral_constant<int, 16>{});
 }
 
 int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
@@ -1670,7 +1673,7 @@ cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta) {
         const size_t zsm = ((n + 1) & ~1) * sizeof(double);
         k_solve_wide_prep<<<1, 1024, zsm, h->stream>>>(h->Rws, h->Rws + (size_t)n * n, Rorig, h->M, h->sdev);
         h->launches++;
-        cudaError_t e = wy_dispatch(n, [&](auto rows) {
+        cudaError_t e = wy_dispatch_merge(n, [&](auto rows) {
             constexpr int RW = decltype(rows)::value;
             const size_t sm = wy_smem_bytes(RW, n);
             cudaFuncSetAttribute(k_tsqr_merge_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

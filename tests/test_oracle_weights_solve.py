@@ -188,3 +188,18 @@ def test_predict_is_H_beta():
     rng = np.random.default_rng(0)
     H = rng.standard_normal((17, 5)); b = rng.standard_normal(5)
     np.testing.assert_allclose(orc.predict(H, b), H @ b, rtol=1e-14, atol=1e-14)
+
+
+def test_lstsq_multi_is_per_output_lstsq_and_numpy():
+    """Multi-output least squares = P independent problems: each column against
+    numpy's lstsq (LAPACK SVD) and the single-output Householder lstsq."""
+    rng = np.random.default_rng(17)
+    H = rng.standard_normal((120, 9))
+    Y = rng.standard_normal((120, 3))
+    B, infos = orc.lstsq_multi(H, Y)
+    ref = np.linalg.lstsq(H, Y, rcond=None)[0].T
+    np.testing.assert_allclose(B, ref, rtol=1e-10, atol=1e-12)
+    for p in range(3):
+        b1, i1 = orc.lstsq(H, Y[:, p])
+        np.testing.assert_array_equal(B[p], b1)
+        assert infos[p].rmse == pytest.approx(np.sqrt(np.mean((H @ ref[p] - Y[:, p]) ** 2)), rel=1e-10)
