@@ -159,6 +159,21 @@ ELMRNN_API elmrnn_status elmrnn_error_windows(elmrnn_t h, const float* H, int64_
 ELMRNN_API elmrnn_status elmrnn_solve_beta(elmrnn_t h, const float* H, int64_t ldh, const float* Y,
                                 int64_t N, double* beta, elmrnn_solve_info* info);
 
+/* Multi-output least squares (the paper's future work,
+ * P:655): B = argmin ||H B - Y||_F for P outputs at once, by one fp64
+ * Householder TSQR of [H | Y_1 .. Y_P] (the reflectors are applied to all P
+ * augmented columns, z = Q^T Y), then P back substitutions with the same R.
+ * Each output's beta equals elmrnn_solve_beta on that column (up to rounding).
+ *   H dev fp32 [N][ldh]; Y dev fp32 [N][ldy], ldy >= P; beta dev fp64 [P][M]
+ *   (output p at beta + p*M); rmse host fp64 [P] or NULL (synchronises);
+ *   info as elmrnn_solve_beta, describing output 0 (the rank check and ridge
+ *   are properties of H and shared by all outputs).
+ * Errors: ARG, SHAPE, UNDERDETERMINED (N < M), UNSUPPORTED (M + P > 1536),
+ * NONFINITE, OOM, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_solve_beta_multi(elmrnn_t h, const float* H, int64_t ldh, const float* Y,
+                                      int64_t ldy, int P, int64_t N, double* beta, double* rmse,
+                                      elmrnn_solve_info* info);
+
 /* Row-sharded solve, step 1 (one per rank / row block): factor the local
  * [H | Y] (N rows) into its (M+1)x(M+1) upper-triangular R, written packed
  * row-major (row k holds R[k][k..M]) to Rpk dev fp64 [elmrnn_packed_r_len(h)].

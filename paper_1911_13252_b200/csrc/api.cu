@@ -5,6 +5,8 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
+#include <cmath>
 
 #include "common.cuh"
 
@@ -57,6 +59,7 @@ elmrnn_status elmrnn_init_ex(elmrnn_t* out, int arch, int d, int M, int Q, uint6
     h->fc_lags = o.fc_lags; h->rec_scale = o.rec_scale; h->weight_grid = o.weight_grid;
     h->force_path = o.force_path; h->seed = seed; h->G = gates_of(arch); h->stream = nullptr;
     h->path = 1;
+    h->nrhs = 1;
     cudaError_t e;
     if ((e = cudaGetDevice(&h->device))) { elmrnn_destroy(h); return cuda_fail(nullptr, e, "cudaGetDevice"); }
     if ((e = cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device))) {
@@ -190,9 +193,45 @@ elmrnn_status elmrnn_solve_beta(elmrnn_t h, const float* H, int64_t ldh, const f
     if (ldh < h->M) return fail(h, ELMRNN_ERR_SHAPE, "ldh < M");
     if (N < h->M) return fail(h, ELMRNN_ERR_UNDERDETERMINED, "N < M");
     cudaError_t e;
-    if ((e = tsqr_factor(h, H, ldh, Y, N))) return cuda_fail(h, e, "tsqr_factor");
+    if ((e = tsqr_factor(h, H, ldh, Y, 1, N))) return cuda_fail(h, e, "tsqr_factor");
     if ((e = tsqr_solve(h, N, beta))) return cuda_fail(h, e, "tsqr_solve");
     return finish_solve(h, info);
+}
+
+elmrnn_status elmrnn_solve_beta_multi(elmrnn_t h, const float* H, int64_t ldh, const float* Y, int64_t ldy, int P,
+                                      int64_t N, double* beta, double* rmse, elmrnn_solve_info* info) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (!H || !Y || !beta || P < 1) return fail(h, ELMRNN_ERR_ARG, "NULL pointer or P < 1");
+    if (ldh < h->M) return fail(h, ELMRNN_ERR_SHAPE, "ldh < M");
+    if (ldy < P) return fail(h, ELMRNN_ERR_SHAPE, "ldy < P");
+    if (h->M + P > 1536) return fail(h, ELMRNN_ERR_UNSUPPORTED, "M + P <= 1536 (one 16-row WY tile in shared memory)");
+    if (N < h->M) return fail(h, ELMRNN_ERR_UNDERDETERMINED, "N < M");
+    cudaError_t e;
+    if (P > h->rho_multi_len) {
+        if (h->rho_multi) cudaFree(h->rho_multi);
+        h->rho_multi = nullptr;
+        h->rho_multi_len = 0;
+        if ((e = cudaMalloc(&h->rho_multi, sizeof(double) * P))) return cuda_fail(h, e, "workspace");
+        h->rho_multi_len = P;
+    }
+    struct Nrhs { elmrnn* h; ~Nrhs() { h->nrhs = 1; } } guard{h};
+    h->nrhs = P;
+    if ((e = tsqr_factor(h, H, ldh, Y, ldy, N))) return cuda_fail(h, e, "tsqr_factor");
+    if ((e = tsqr_solve(h, N, beta))) return cuda_fail(h, e, "tsqr_solve");
+    elmrnn_solve_info tmp;
+    elmrnn_solve_info* ip = info ? info : (rmse ? &tmp : nullptr);
+    const elmrnn_status st = finish_solve(h, ip);
+    if (st < 0 || !rmse) return st;
+    if (P == 1) {   // a single output may take the per-column-fold solve, which reports through info
+        rmse[0] = ip->rmse;
+        return st;
+    }
+    std::vector<double> rho(P);
+    if ((e = cudaMemcpyAsync(rho.data(), h->rho_multi, sizeof(double) * P, cudaMemcpyDeviceToHost, h->stream)) ||
+        (e = cudaStreamSynchronize(h->stream)))
+        return cuda_fail(h, e, "solve");
+    for (int p = 0; p < P; ++p) rmse[p] = rho[p] / std::sqrt((double)N);
+    return st;
 }
 
 elmrnn_status elmrnn_solve_local(elmrnn_t h, const float* H, int64_t ldh, const float* Y, int64_t N, double* Rpk) {
@@ -200,7 +239,7 @@ elmrnn_status elmrnn_solve_local(elmrnn_t h, const float* H, int64_t ldh, const 
     if (!Rpk || N < 0 || (N > 0 && (!H || !Y))) return fail(h, ELMRNN_ERR_ARG, "bad argument");
     if (ldh < h->M) return fail(h, ELMRNN_ERR_SHAPE, "ldh < M");
     cudaError_t e;
-    if ((e = tsqr_factor(h, H, ldh, Y, N))) return cuda_fail(h, e, "tsqr_factor");
+    if ((e = tsqr_factor(h, H, ldh, Y, 1, N))) return cuda_fail(h, e, "tsqr_factor");
     if ((e = tsqr_pack(h, Rpk))) return cuda_fail(h, e, "tsqr_pack");
     return ELMRNN_OK;
 }
@@ -336,7 +375,7 @@ const char* elmrnn_last_error(elmrnn_t h) { return h ? h->err.c_str() : g_init_e
 void elmrnn_destroy(elmrnn_t h) {
     if (!h) return;
     cudaFree(h->W); cudaFree(h->b); cudaFree(h->rec); cudaFree(h->tc_ops);
-    cudaFree(h->Rws); cudaFree(h->sdev); cudaFree(h->flag); cudaFree(h->Hws); cudaFree(h->rws); cudaFree(h->fws); cudaFree(h->dscr); cudaFree(h->scratch);
+    cudaFree(h->Rws); cudaFree(h->sdev); cudaFree(h->flag); cudaFree(h->Hws); cudaFree(h->rho_multi); cudaFree(h->rws); cudaFree(h->fws); cudaFree(h->dscr); cudaFree(h->scratch);
     if (h->shost) cudaFreeHost(h->shost);
     delete h;
 }

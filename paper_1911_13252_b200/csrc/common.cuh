@@ -49,8 +49,12 @@ struct elmrnn {
     float tc_inv_scale;       // 2^-sigma of the scaled fp16 U images
     std::vector<float> tc_wb; // host copy of W | b (kernel parameter block)
     // solve workspace (device)
-    double* Rws;          // slabs of (M+1)^2 doubles
+    double* Rws;          // slabs of n^2 doubles, n = M + nrhs
     int64_t Rws_slabs;
+    int Rws_n;            // n the slabs were allocated for
+    int nrhs;             // outputs in the current solve (1; P inside elmrnn_solve_beta_multi)
+    double* rho_multi;    // device [P] per-output residual norms (multi-output solve)
+    int rho_multi_len;
     elm::SolveDev* sdev;  // device diagnostics
     int* flag;            // device non-finite flag
     elm::SolveDev* shost; // pinned host mirror
@@ -108,7 +112,7 @@ cudaError_t launch_fc_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, floa
 
 // ---- TSQR (tsqr.cu) ------------------------------------------------------------
 // Fold [H | Y] rows into per-CTA R slabs and reduce them to slab 0 (full storage).
-cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t N);
+cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t ldy, int64_t N);
 cudaError_t tsqr_pack(elmrnn* h, double* Rpk);
 cudaError_t tsqr_merge_packed(elmrnn* h, const double* Rpk_all, int P);
 cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta);

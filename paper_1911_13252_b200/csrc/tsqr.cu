@@ -627,11 +627,10 @@ __device__ void wide_sign_normalise(double* __restrict__ R, int n, double* zs) {
 }
 
 __global__ void __launch_bounds__(1024, 1)
-    k_solve_wide_prep(double* __restrict__ R, double* __restrict__ Rridge, double* __restrict__ Rorig, int M,
+    k_solve_wide_prep(double* __restrict__ R, double* __restrict__ Rridge, double* __restrict__ Rorig, int M, int n,
                       SolveDev* __restrict__ out) {
     extern __shared__ __align__(16) double zs[];
     __shared__ double red[32];
-    const int n = M + 1;
     wide_sign_normalise(R, n, zs);
     double dmn = INFINITY, dmx = 0.0, f2 = 0.0;
     for (int j = threadIdx.x; j < M; j += blockDim.x) {
@@ -657,35 +656,45 @@ __global__ void __launch_bounds__(1024, 1)
     }
 }
 
+// P = n - M outputs: beta[p*M + j]; rho of output p to rho_multi[p] (when non-null), output 0
+// also to out->rho / out->rmse.
 __global__ void __launch_bounds__(1024, 1)
-    k_solve_wide_finish(double* __restrict__ R, const double* __restrict__ Rorig, int M, long long n_total,
-                        const int* __restrict__ flag, double* __restrict__ beta, SolveDev* __restrict__ out) {
+    k_solve_wide_finish(double* __restrict__ R, const double* __restrict__ Rorig, int M, int n, long long n_total,
+                        const int* __restrict__ flag, double* __restrict__ beta, SolveDev* __restrict__ out,
+                        double* __restrict__ rho_multi) {
     extern __shared__ __align__(16) double zs[];
     __shared__ double red[32];
     __shared__ double bk;
-    const int n = M + 1;
     wide_sign_normalise(R, n, zs);
-    for (int j = threadIdx.x; j < M; j += blockDim.x) zs[j] = R[(size_t)j * n + M];
-    __syncthreads();
-    for (int k = M - 1; k >= 0; --k) {
-        if (threadIdx.x == 0) bk = zs[k] / R[(size_t)k * n + k];
+    for (int p = 0; p < n - M; ++p) {
+        const int col = M + p;
+        for (int j = threadIdx.x; j < M; j += blockDim.x) zs[j] = R[(size_t)j * n + col];
         __syncthreads();
-        for (int j = threadIdx.x; j < k; j += blockDim.x) zs[j] -= R[(size_t)j * n + k] * bk;
-        if (threadIdx.x == 0) zs[k] = bk;
-        __syncthreads();
+        for (int k = M - 1; k >= 0; --k) {
+            if (threadIdx.x == 0) bk = zs[k] / R[(size_t)k * n + k];
+            __syncthreads();
+            for (int j = threadIdx.x; j < k; j += blockDim.x) zs[j] -= R[(size_t)j * n + k] * bk;
+            if (threadIdx.x == 0) zs[k] = bk;
+            __syncthreads();
+        }
+        double s2 = 0.0;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+            double s = 0.0;
+            for (int c = j; c < M; ++c) s += Rorig[(size_t)j * n + c] * zs[c];
+            s -= Rorig[(size_t)j * n + col];
+            s2 += s * s;
+            if (j < M) beta[(size_t)p * M + j] = zs[j];
+        }
+        const double rho2 = block_sum(s2, red);   // ends with a barrier: zs may be reused
+        if (threadIdx.x == 0) {
+            if (rho_multi) rho_multi[p] = sqrt(rho2);
+            if (p == 0) {
+                out->rho = sqrt(rho2);
+                out->rmse = sqrt(rho2) / sqrt((double)n_total);
+            }
+        }
     }
-    double s2 = 0.0;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        double s = 0.0;
-        for (int c = j; c < M; ++c) s += Rorig[(size_t)j * n + c] * zs[c];
-        s -= Rorig[(size_t)j * n + M];
-        s2 += s * s;
-        if (j < M) beta[j] = zs[j];
-    }
-    const double rho2 = block_sum(s2, red);
     if (threadIdx.x == 0) {
-        out->rho = sqrt(rho2);
-        out->rmse = sqrt(rho2) / sqrt((double)n_total);
         out->nonfinite = *flag;
         out->n_total = n_total;
     }
@@ -1292,10 +1301,12 @@ __device__ __forceinline__ int wy_panel_warp(int* sm_slot) {
 
 template <int ROWS>
 __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
-    k_tsqr_leaf_wy(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t N, int M,
-                   double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag, int* sm_slot) {
+    k_tsqr_leaf_wy(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t ldy, int P,
+                   int64_t N, int M, double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag,
+                   int* sm_slot) {
     extern __shared__ __align__(16) double wsm[];
-    const int n = M + 1, LDC = wy_ldc(n), tid = threadIdx.x, nt = blockDim.x;
+    // columns [0, M) of the tile are H, [M, M + P) the P outputs Y[row][0..P-1] (row stride ldy)
+    const int n = M + P, LDC = wy_ldc(n), tid = threadIdx.x, nt = blockDim.x;
     double* C = wsm;
     double* Gs = C + (size_t)ROWS * LDC;     // [2][16][16]
     double* Rd = Gs + 2 * kNBW * kNBW;       // [16][16]
@@ -1334,10 +1345,10 @@ __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
                     }
                 }
             }
-            for (int e = tid; e < ROWS * tail; e += nt) {   // Y column, zero padding
+            for (int e = tid; e < ROWS * tail; e += nt) {   // Y columns, zero padding
                 const int r = e / tail, c = M + (e - r * tail);
                 const int64_t row = base + r;
-                const float x = (c == M && row < r1) ? __ldg(Y + row) : 0.0f;
+                const float x = (c < n && row < r1) ? __ldg(Y + row * ldy + (c - M)) : 0.0f;
                 bad |= !isfinite(x);
                 C[(size_t)r * LDC + c] = (double)x;
             }
@@ -1346,7 +1357,7 @@ __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
                 const int64_t row = base + r;
                 for (int c = tid; c < LDC; c += nt) {
                     float x = 0.0f;
-                    if (row < r1 && c < n) x = c < M ? __ldg(H + row * ldh + c) : __ldg(Y + row);
+                    if (row < r1 && c < n) x = c < M ? __ldg(H + row * ldh + c) : __ldg(Y + row * ldy + (c - M));
                     bad |= !isfinite(x);
                     C[(size_t)r * LDC + c] = (double)x;
                 }
@@ -1442,6 +1453,9 @@ static bool use_wy(int n) {
     if (const char* e = std::getenv("ELMRNN_TSQR_WY")) return std::atoi(e) != 0;
     return n > 192;
 }
+// multi-output [H | Y_1..Y_P] (P > 1) always takes the WY leaf/merge and the wide solve
+static bool use_wy_h(const elmrnn* h) { return h->nrhs > 1 || use_wy(h->M + h->nrhs); }
+static bool wide_solve(const elmrnn* h) { return h->nrhs > 1 || h->M + h->nrhs > kWideN; }
 static int wy_rows(int n) {
     if (const char* e = std::getenv("ELMRNN_TSQR_WY_ROWS")) {   // testing aid
         const int r = std::atoi(e);
@@ -1488,10 +1502,10 @@ static auto wy_dispatch_merge(int n, F&& f) {
 }
 
 int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
-    const int n = h->M + 1;
+    const int n = h->M + h->nrhs;
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
-    int per_sm = use_wy(n) ? wy_dispatch(n, [&](auto rows) {
+    int per_sm = use_wy_h(h) ? wy_dispatch(n, [&](auto rows) {
         constexpr int RW = decltype(rows)::value;
         const size_t sm = wy_leaf_smem(RW, n);
         cudaFuncSetAttribute(k_tsqr_leaf_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1514,13 +1528,14 @@ int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
 
 cudaError_t ensure_solve_ws(elmrnn* h, int64_t slabs) {
     cudaError_t e;
-    const int n = h->M + 1;
-    if (slabs + 1 > h->Rws_slabs) {   // +1: Rorig copy for the final solve
+    const int n = h->M + h->nrhs;
+    if (slabs + 1 > h->Rws_slabs || n != h->Rws_n) {   // +1: Rorig copy for the final solve
         if (h->Rws) cudaFree(h->Rws);
         h->Rws = nullptr;
         h->Rws_slabs = 0;
         if ((e = cudaMalloc(&h->Rws, (size_t)(slabs + 1) * n * n * sizeof(double)))) return e;
         h->Rws_slabs = slabs + 1;
+        h->Rws_n = n;
     }
     if (!h->sdev) {   // SolveDev + 1024 ints of per-SM counters (k_tsqr_leaf_wy)
         if ((e = cudaMalloc(&h->sdev, sizeof(SolveDev) + 1024 * sizeof(int)))) return e;
@@ -1531,12 +1546,12 @@ cudaError_t ensure_solve_ws(elmrnn* h, int64_t slabs) {
 }
 
 static cudaError_t tree(elmrnn* h, int64_t slabs) {
-    const int n = h->M + 1;
+    const int n = h->M + h->nrhs;
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
     const char* lv = std::getenv("ELMRNN_TSQR_LEVELS");   // testing aid: stop the tree early
     const int64_t max_stride = lv ? ((int64_t)1 << std::atoi(lv)) : slabs;
-    if (use_wy(n)) {
+    if (use_wy_h(h)) {
         // merges are latency-bound (one CTA per pair, few pairs at the top of the
         // tree): the tallest tile that fits means the fewest panel steps per fold
         return wy_dispatch_merge(n, [&](auto rows) {
@@ -1597,27 +1612,27 @@ static void qr_trace_dump(unsigned long long* buf) {
     }
 }
 
-cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t N) {
+cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t ldy, int64_t N) {
     struct TraceGuard { unsigned long long* b = qr_trace_setup(); ~TraceGuard() { qr_trace_dump(b); } } tg;
-    const int n = h->M + 1;
+    const int n = h->M + h->nrhs;
     const Var v = pick_var(n);
     const int64_t slabs = tsqr_leaf_slabs(h, N);
     cudaError_t e;
-    if ((e = ensure_solve_ws(h, n > kWideN && slabs < 2 ? 2 : slabs))) return e;   // wide solve: slab 1 = ridge rows
+    if ((e = ensure_solve_ws(h, wide_solve(h) && slabs < 2 ? 2 : slabs))) return e;   // wide solve: slab 1 = ridge rows
     if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream))) return e;
-    const int rows_tile = use_wy(n) ? wy_rows(n) : use_2d(n) ? kRG * kTR2 : var_rows(v);
+    const int rows_tile = use_wy_h(h) ? wy_rows(n) : use_2d(n) ? kRG * kTR2 : var_rows(v);
     int64_t rows = (N + slabs - 1) / slabs;
     rows = (rows + rows_tile - 1) / rows_tile * rows_tile;
     const int threads = var_threads(v, n);
-    if (use_wy(n)) {
+    if (use_wy_h(h)) {
         e = wy_dispatch(n, [&](auto rws) {
             constexpr int RW = decltype(rws)::value;
             const size_t sm = wy_leaf_smem(RW, n);
             cudaFuncSetAttribute(k_tsqr_leaf_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             int* slot = reinterpret_cast<int*>(h->sdev + 1);   // per-SM arrival counters (ensure_solve_ws)
             cudaMemsetAsync(slot, 0, 1024 * sizeof(int), h->stream);
-            k_tsqr_leaf_wy<RW><<<(unsigned)slabs, wy_threads(n), sm, h->stream>>>(H, ldh, Y, N, h->M, h->Rws, rows,
-                                                                                 h->flag, slot);
+            k_tsqr_leaf_wy<RW><<<(unsigned)slabs, wy_threads(n), sm, h->stream>>>(
+                H, ldh, Y, ldy, h->nrhs, N, h->M, h->Rws, rows, h->flag, slot);
             h->launches++;
             return cudaGetLastError();
         });
@@ -1641,7 +1656,7 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
 }
 
 cudaError_t tsqr_pack(elmrnn* h, double* Rpk) {
-    const int n = h->M + 1;
+    const int n = h->M + h->nrhs;
     int64_t len = (int64_t)n * (n + 1) / 2;
     int blocks = (int)((len + 255) / 256);
     if (blocks > 1024) blocks = 1024;
@@ -1651,9 +1666,9 @@ cudaError_t tsqr_pack(elmrnn* h, double* Rpk) {
 }
 
 cudaError_t tsqr_merge_packed(elmrnn* h, const double* Rpk_all, int P) {
-    const int n = h->M + 1;
+    const int n = h->M + h->nrhs;
     cudaError_t e;
-    if ((e = ensure_solve_ws(h, n > kWideN && P < 2 ? 2 : P))) return e;
+    if ((e = ensure_solve_ws(h, wide_solve(h) && P < 2 ? 2 : P))) return e;
     if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream))) return e;
     int64_t total = (int64_t)P * n * n;
     int blocks = (int)((total + 255) / 256);
@@ -1665,13 +1680,13 @@ cudaError_t tsqr_merge_packed(elmrnn* h, const double* Rpk_all, int P) {
 }
 
 cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta) {
-    const int n = h->M + 1;
+    const int n = h->M + h->nrhs;
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
     double* Rorig = h->Rws + (size_t)(h->Rws_slabs - 1) * n * n;
-    if (n > kWideN) {
+    if (wide_solve(h)) {
         const size_t zsm = ((n + 1) & ~1) * sizeof(double);
-        k_solve_wide_prep<<<1, 1024, zsm, h->stream>>>(h->Rws, h->Rws + (size_t)n * n, Rorig, h->M, h->sdev);
+        k_solve_wide_prep<<<1, 1024, zsm, h->stream>>>(h->Rws, h->Rws + (size_t)n * n, Rorig, h->M, n, h->sdev);
         h->launches++;
         cudaError_t e = wy_dispatch_merge(n, [&](auto rows) {
             constexpr int RW = decltype(rows)::value;
@@ -1682,8 +1697,8 @@ cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta) {
             return cudaGetLastError();
         });
         if (e) return e;
-        k_solve_wide_finish<<<1, 1024, zsm, h->stream>>>(h->Rws, Rorig, h->M, (long long)n_total, h->flag, beta,
-                                                          h->sdev);
+        k_solve_wide_finish<<<1, 1024, zsm, h->stream>>>(h->Rws, Rorig, h->M, n, (long long)n_total, h->flag, beta,
+                                                          h->sdev, h->nrhs > 1 ? h->rho_multi : nullptr);
         h->launches++;
         return cudaGetLastError();
     }

@@ -24,6 +24,7 @@ STATUS = {0: "OK", 1: "WARN_RIDGE", -1: "ERR_ARG", -2: "ERR_SHAPE", -3: "ERR_UND
 
 EXPORTED = ("elmrnn_opts_default", "elmrnn_init", "elmrnn_init_ex", "elmrnn_set_stream", "elmrnn_build_H",
             "elmrnn_build_H_ef", "elmrnn_error_windows", "elmrnn_forecast", "elmrnn_test_rmse",
+            "elmrnn_solve_beta_multi",
             "elmrnn_solve_beta", "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_packed_r_len",
             "elmrnn_predict", "elmrnn_get_weights", "elmrnn_weight_block_len", "elmrnn_path",
             "elmrnn_launch_count", "elmrnn_last_error", "elmrnn_destroy")
@@ -80,6 +81,7 @@ def lib() -> ctypes.CDLL:
         L.elmrnn_forecast.argtypes = [vp, vp, i64, i64, vp, i32, vp, i64]
         L.elmrnn_test_rmse.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, vp]
         L.elmrnn_solve_beta.argtypes = [vp, vp, i64, vp, i64, vp, vp]
+        L.elmrnn_solve_beta_multi.argtypes = [vp, vp, i64, vp, i64, i32, i64, vp, vp, vp]
         L.elmrnn_solve_local.argtypes = [vp, vp, i64, vp, i64, vp]
         L.elmrnn_solve_merge.argtypes = [vp, vp, i32, i64, vp, vp]
         L.elmrnn_packed_r_len.argtypes = [vp]
@@ -97,6 +99,7 @@ def lib() -> ctypes.CDLL:
         L.elmrnn_destroy.restype = None
         for f in ("elmrnn_init", "elmrnn_init_ex", "elmrnn_set_stream", "elmrnn_build_H", "elmrnn_build_H_ef",
                   "elmrnn_error_windows", "elmrnn_forecast", "elmrnn_test_rmse", "elmrnn_solve_beta",
+                  "elmrnn_solve_beta_multi",
                   "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_predict", "elmrnn_get_weights",
                   "elmrnn_path"):
             getattr(L, f).restype = i32
@@ -256,6 +259,25 @@ class ELMRNN:
         st = self._check(lib().elmrnn_solve_beta(self._h, _ptr(H), ldh, _ptr(Y), N, _ptr(beta),
                                                  ctypes.byref(inf) if info else None))
         return beta, (self._info(inf, st) if info else None)
+
+    def solve_beta_multi(self, H: torch.Tensor, Y: torch.Tensor):
+        """elmrnn_solve_beta_multi: Y [N][P] -> (B fp64 [P][M], rmse list [P], SolveInfo of output 0)."""
+        _dev_check(H, "H", torch.float32)
+        _dev_check(Y, "Y", torch.float32)
+        N = H.shape[0]
+        Y2 = Y.reshape(N, -1)
+        P = Y2.shape[1]
+        ldh, _ = _rows(H, "H")
+        ldy = Y2.stride(0) if N > 1 else P
+        if Y2.stride(1) != 1:
+            raise ValueError("Y must have unit inner stride")
+        B = torch.empty((P, self.M), dtype=torch.float64, device=H.device)
+        rm = (ctypes.c_double * P)()
+        inf = _Info()
+        self._stream()
+        st = self._check(lib().elmrnn_solve_beta_multi(self._h, _ptr(H), ldh, _ptr(Y2), ldy, P, N, _ptr(B), rm,
+                                                       ctypes.byref(inf)))
+        return B, list(rm), self._info(inf, st)
 
     def solve_local(self, H: torch.Tensor, Y: torch.Tensor, Rpk: torch.Tensor | None = None):
         """elmrnn_solve_local -> packed R fp64 [(M+1)(M+2)/2]."""

@@ -645,3 +645,54 @@ def test_test_rmse_parity(arch, M, Q, S):
     net = orc.Net(arch, S=S, M=M, Q=Q)
     ref = orc.test_rmse(net, orc.gen_weights(net, 2), X[Ntr:], Y[Ntr:], b, threads=8)
     assert abs(r - ref) <= 1e-5 * max(1.0, np.abs(b).sum()), (r, ref)
+
+
+# ------------------------------------------------------------------------- multi-output Y (8(f) row 3)
+@pytest.mark.parametrize("M,N,P", [(64, 5000, 3), (20, 1000, 1), (256, 20011, 2), (1024, 3001, 4), (129, 777, 5)])
+def test_solve_beta_multi_parity(M, N, P):
+    """One TSQR of [H | Y_1..Y_P] against the oracle's P independent Householder
+    solves of the same fp32 H, and against elmrnn_solve_beta column by column."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + P)
+    H = torch.rand(N, M, device="cuda", generator=g) - 0.5
+    Y = torch.rand(N, P, device="cuda", generator=g) - 0.5
+    e = E("lstm", 1, M, 4, 1, force_path=1)
+    B, rmse, info = e.solve_beta_multi(H, Y)
+    Bo, io = orc.lstsq_multi(H.double().cpu().numpy(), Y.double().cpu().numpy())
+    cond = np.linalg.cond(io[0].R[:M, :M])
+    tol = 1e-12 * max(1.0, cond)
+    for p in range(P):
+        rel = np.linalg.norm(B[p].cpu().numpy() - Bo[p]) / np.linalg.norm(Bo[p])
+        assert rel <= tol, (p, rel, cond)
+        assert rmse[p] == pytest.approx(io[p].rmse, rel=tol)
+        b1, i1 = e.solve_beta(H, Y[:, p].contiguous())
+        assert float((b1 - B[p]).norm() / b1.norm()) <= tol
+    assert info.status == 0 and info.rmse == pytest.approx(rmse[0], rel=1e-14)
+
+
+def test_solve_beta_multi_ridge_and_trained():
+    """Rank-deficient H: the ridge path (R19) is shared by all outputs; and a real
+    GRU H with two targets (y(t+1) and y(t+2))."""
+    M, N = 32, 600
+    g = torch.Generator(device="cuda").manual_seed(3)
+    H = torch.rand(N, M, device="cuda", generator=g)
+    H[:, 20:] = H[:, :12]
+    Y = torch.rand(N, 2, device="cuda", generator=g)
+    e = E("gru", 1, M, 4, 1)
+    B, rmse, info = e.solve_beta_multi(H, Y)
+    Bo, io = orc.lstsq_multi(H.double().cpu().numpy(), Y.double().cpu().numpy())
+    assert info.status == 1 and io[0].status == 1
+    for p in range(2):
+        np.testing.assert_allclose(B[p].cpu().numpy(), Bo[p], rtol=1e-5, atol=1e-6 * np.abs(Bo[p]).max())
+        assert rmse[p] == pytest.approx(io[p].rmse, rel=1e-6)
+    Q, S, M2, N2 = 10, 1, 64, 3000
+    s = sy.series("mg", N2 + Q + 2, seed=4)
+    X, Y1, _ = sy.windows(s[:, :1], N2, Q)
+    Y2 = s[Q + 1: Q + 1 + N2, 0].astype(np.float32)
+    e2 = E("gru", S, M2, Q, 2)
+    Hg = e2.build_H(torch.from_numpy(X).cuda())
+    Yd = torch.from_numpy(np.stack([Y1, Y2], axis=1)).cuda()
+    B2, rm2, _ = e2.solve_beta_multi(Hg, Yd)
+    Bo2, io2 = orc.lstsq_multi(Hg.double().cpu().numpy(), Yd.double().cpu().numpy())
+    cond = np.linalg.cond(io2[0].R[:M2, :M2])
+    for p in range(2):
+        assert np.linalg.norm(B2[p].cpu().numpy() - Bo2[p]) / np.linalg.norm(Bo2[p]) <= 1e-12 * cond
