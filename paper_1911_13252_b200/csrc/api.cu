@@ -375,7 +375,7 @@ const char* elmrnn_last_error(elmrnn_t h) { return h ? h->err.c_str() : g_init_e
 void elmrnn_destroy(elmrnn_t h) {
     if (!h) return;
     cudaFree(h->W); cudaFree(h->b); cudaFree(h->rec); cudaFree(h->tc_ops);
-    cudaFree(h->Rws); cudaFree(h->sdev); cudaFree(h->flag); cudaFree(h->Hws); cudaFree(h->rho_multi); cudaFree(h->rws); cudaFree(h->fws); cudaFree(h->dscr); cudaFree(h->scratch);
+    cudaFree(h->Rws); cudaFree(h->sdev); cudaFree(h->flag); cudaFree(h->Hws); cudaFree(h->prog); cudaFree(h->rho_multi); cudaFree(h->rws); cudaFree(h->fws); cudaFree(h->dscr); cudaFree(h->scratch);
     if (h->shost) cudaFreeHost(h->shost);
     delete h;
 }

@@ -54,6 +54,8 @@ struct elmrnn {
     int Rws_n;            // n the slabs were allocated for
     int nrhs;             // outputs in the current solve (1; P inside elmrnn_solve_beta_multi)
     double* rho_multi;    // device [P] per-output residual norms (multi-output solve)
+    int* prog;            // pipelined-merge progress counters [pairs][128]
+    int64_t prog_pairs;
     int rho_multi_len;
     elm::SolveDev* sdev;  // device diagnostics
     int* flag;            // device non-finite flag

@@ -945,6 +945,14 @@ __device__ __forceinline__ void named_bar_arrive(int id, int count) {
 
 // Shared-memory load the compiler may not hoist (keeps the 16 u0 / G values
 // out of registers across the trailing loops).
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ double lds_nohoist(const double* p) {
     double v;
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
@@ -1105,7 +1113,7 @@ __device__ __forceinline__ void wy_trailing(double* __restrict__ C, int LDC, int
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int j = j0 + 2 * tig + e;
-                rr[mt][e] = (j0 < jend && j < n) ? R[(size_t)(p + 8 * mt + gid) * n + j] : 0.0;
+                rr[mt][e] = (j0 < jend && j < n) ? __ldcg(R + (size_t)(p + 8 * mt + gid) * n + j) : 0.0;
             }
     };
     double rn[2][2];
@@ -1206,7 +1214,7 @@ __device__ __forceinline__ void rd_load(const double* __restrict__ R, int n, int
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
         const int e = lane + 32 * t, i = e / kNBW, c = e % kNBW;
-        rr[t] = (p < n && i < nbp && c < nbp && c >= i) ? R[(size_t)(p + i) * n + p + c] : 0.0;
+        rr[t] = (p < n && i < nbp && c < nbp && c >= i) ? __ldcg(R + (size_t)(p + i) * n + p + c) : 0.0;
     }
 }
 __device__ __forceinline__ void rd_put(double* Rd, const double (&rr)[8]) {
@@ -1229,12 +1237,33 @@ __device__ __forceinline__ void wy_panel_rd(double* C, int LDC, int n, int p, do
 
 template <int ROWS>
 __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* __restrict__ R, double* Gs,
-                        double* Rd, double* cgv, double* cuv, int pw) {
+                        double* Rd, double* cgv, double* cuv, int pw, const int* pred_prog = nullptr,
+                        int* my_prog = nullptr) {
     const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int tw = warp < pw ? warp : warp - 1;
     const bool lane0 = (threadIdx.x & 31) == 0 && warp == pw;
+    // Pipelined merge (k_tsqr_merge_wy_par): the fold of the previous row chunk into
+    // the same R publishes the number of panel steps it has completed; step p of
+    // this fold touches R rows p .. p+47 (trailing rows, look-ahead panel, diagonal
+    // prefetch), which the predecessor no longer writes once it has completed
+    // panel step p/16 + 2.
+    const int npan = (n + kNBW - 1) / kNBW;
+    auto wait_pred = [&](int need) {
+        if (!pred_prog) return;
+        need = min(need, npan);
+        if (threadIdx.x == 0)
+            while (ld_acquire_gpu(pred_prog) < need) __nanosleep(64);
+        __syncthreads();
+    };
+    auto publish = [&](int v) {
+        if (my_prog && threadIdx.x == 0) {
+            __threadfence();
+            st_release_gpu(my_prog, v);
+        }
+    };
     int p = k0, buf = 0;
     double rdn[8];   // panel warp: next panel's R diagonal block
+    wait_pred(k0 / kNBW + 2);
     if (warp == pw) {
         rd_load(R, n, p, rdn);
         rd_put(Rd, rdn);
@@ -1247,6 +1276,7 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
     for (;;) {
         const int pe = p + min(kNBW, n - p);
         if (pe >= n) break;   // no trailing columns (so below nbp == kNBW)
+        wait_pred(p / kNBW + 3);
         if (lane0) qr_ev(0, p);
         const int nbn = min(kNBW, n - pe);
         double *G0 = Gs + buf * kNBW * kNBW, *g0 = cgv + buf * kNBW, *u0 = cuv + buf * kNBW;
@@ -1272,12 +1302,14 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
         }
         __syncthreads();
         if (lane0) qr_ev(2, p);
+        publish(p / kNBW + 1);
         p = pe;
         buf ^= 1;
         wy_gram<ROWS>(C, LDC, p, min(kNBW, n - p), Gs + buf * kNBW * kNBW);
         __syncthreads();
         if (lane0) qr_ev(3, p - kNBW);
     }
+    publish(npan);
 }
 
 // Panel warp of this CTA: co-resident CTAs (typically blocks b, b+148, ...)
@@ -1390,6 +1422,41 @@ __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1) k_tsqr_merge_wy(doubl
         }
         __syncthreads();
         wy_fold<ROWS>(C, LDC, n, s * ROWS, Ra, Gs, Rd, cgv, cuv, (int)(blockIdx.x % (blockDim.x >> 5)));
+    }
+}
+
+// Pipelined merge: P CTAs share one pair (R_a <- qr_r([R_a; R_b])); CTA pc folds
+// the ROWS-row chunks s = pc, pc + P, ... of R_b in order, each fold waiting on
+// the progress counter of chunk s - 1 (a wavefront one to three panel steps
+// apart) instead of for the whole previous chunk.  All CTAs of the grid must be
+// co-resident: launched cooperatively.  prog: [pairs][kMaxChunks] zeroed ints.
+constexpr int kMaxChunks = 128;
+template <int ROWS>
+__global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
+    k_tsqr_merge_wy_par(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n, int P, int* prog) {
+    extern __shared__ __align__(16) double wsm[];
+    const int64_t m = blockIdx.x / P;
+    const int pc = (int)(blockIdx.x % P);
+    const int64_t c = m * 2 * stride, partner = c + stride;
+    if (partner >= slabs) return;
+    const int LDC = wy_ldc(n), tid = threadIdx.x, nt = blockDim.x;
+    double* C = wsm;
+    double* Gs = C + (size_t)ROWS * LDC;     // [2][16][16]
+    double* Rd = Gs + 2 * kNBW * kNBW;       // [16][16]
+    double* cgv = Rd + kNBW * kNBW;          // [2][16]
+    double* cuv = cgv + 2 * kNBW;            // [2][16]
+    double* Ra = Rws + (size_t)c * n * n;
+    const double* Rb = Rws + (size_t)partner * n * n;
+    int* pg = prog + m * kMaxChunks;
+    for (int s = pc; s * ROWS < n; s += P) {
+        for (int r = 0; r < ROWS; ++r) {
+            const int row = s * ROWS + r;
+            for (int cc = tid; cc < LDC; cc += nt)
+                C[(size_t)r * LDC + cc] = (row < n && cc < n && cc >= row) ? Rb[(size_t)row * n + cc] : 0.0;
+        }
+        __syncthreads();
+        wy_fold<ROWS>(C, LDC, n, s * ROWS, Ra, Gs, Rd, cgv, cuv, (int)(blockIdx.x % (blockDim.x >> 5)),
+                      s > 0 ? pg + s - 1 : nullptr, pg + s);
     }
 }
 
@@ -1537,6 +1604,14 @@ cudaError_t ensure_solve_ws(elmrnn* h, int64_t slabs) {
         h->Rws_slabs = slabs + 1;
         h->Rws_n = n;
     }
+    if ((slabs + 1) / 2 > h->prog_pairs) {   // progress counters of the pipelined merge
+        if (h->prog) cudaFree(h->prog);
+        h->prog = nullptr;
+        h->prog_pairs = 0;
+        const int64_t pairs = (slabs + 1) / 2;
+        if ((e = cudaMalloc(&h->prog, sizeof(int) * pairs * kMaxChunks))) return e;
+        h->prog_pairs = pairs;
+    }
     if (!h->sdev) {   // SolveDev + 1024 ints of per-SM counters (k_tsqr_leaf_wy)
         if ((e = cudaMalloc(&h->sdev, sizeof(SolveDev) + 1024 * sizeof(int)))) return e;
         if ((e = cudaMalloc(&h->flag, sizeof(int)))) return e;
@@ -1552,15 +1627,38 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
     const char* lv = std::getenv("ELMRNN_TSQR_LEVELS");   // testing aid: stop the tree early
     const int64_t max_stride = lv ? ((int64_t)1 << std::atoi(lv)) : slabs;
     if (use_wy_h(h)) {
-        // merges are latency-bound (one CTA per pair, few pairs at the top of the
-        // tree): the tallest tile that fits means the fewest panel steps per fold
+        // merges are latency-bound (few pairs at the top of the tree): the
+        // tallest tile that fits means the fewest panel steps per fold, and the
+        // SMs a level leaves idle pipeline each pair's row chunks
+        // (k_tsqr_merge_wy_par; ELMRNN_TSQR_PAR=0 disables, testing aid)
+        const char* pe = std::getenv("ELMRNN_TSQR_PAR");
+        const bool par_ok = !(pe && std::atoi(pe) == 0);
         return wy_dispatch_merge(n, [&](auto rows) {
             constexpr int RW = decltype(rows)::value;
             const size_t sm = wy_smem_bytes(RW, n);
             cudaFuncSetAttribute(k_tsqr_merge_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            cudaFuncSetAttribute(k_tsqr_merge_wy_par<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tsqr_merge_wy_par<RW>, wy_threads(n), sm);
+            const int64_t resident = (int64_t)occ * h->sm_count;
+            const int nch = (n + RW - 1) / RW;
             for (int64_t stride = 1; stride < slabs && stride < max_stride; stride *= 2) {
                 int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
-                k_tsqr_merge_wy<RW><<<(unsigned)pairs, wy_threads(n), sm, h->stream>>>(h->Rws, slabs, stride, n);
+                int P = (int)std::min<int64_t>(nch, resident / std::max<int64_t>(pairs, 1));
+                if (par_ok && P >= 2 && nch <= kMaxChunks && pairs <= h->prog_pairs) {
+                    cudaError_t e = cudaMemsetAsync(h->prog, 0, sizeof(int) * pairs * kMaxChunks, h->stream);
+                    if (e) return e;
+                    double* rws = h->Rws;
+                    int64_t sl = slabs, sd = stride;
+                    int nn = n;
+                    int* pg = h->prog;
+                    void* args[] = {&rws, &sl, &sd, &nn, &P, &pg};
+                    e = cudaLaunchCooperativeKernel((const void*)k_tsqr_merge_wy_par<RW>, dim3((unsigned)(pairs * P)),
+                                                    dim3(wy_threads(n)), args, sm, h->stream);
+                    if (e) return e;
+                } else {
+                    k_tsqr_merge_wy<RW><<<(unsigned)pairs, wy_threads(n), sm, h->stream>>>(h->Rws, slabs, stride, n);
+                }
                 h->launches++;
             }
             return cudaGetLastError();
