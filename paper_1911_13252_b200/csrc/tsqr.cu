@@ -991,7 +991,7 @@ __device__ __forceinline__ double rcp_nr(double d) {
 // (commutative butterfly sums), so g, u0 and beta need no broadcast.
 template <int ROWS>
 __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, int nbp, double* Rd, double* cgv,
-                                      double* cuv) {
+                                      double* cuv, double* Gp) {
     constexpr int RPL = ROWS / 4;   // rows per lane: rows rg, rg+4, ... (interleaved: no bank conflicts)
     const int lane = threadIdx.x & 31, rg = lane >> 3, cp = lane & 7;
     const int c0 = 2 * cp, c1 = c0 + 1;
@@ -1002,6 +1002,10 @@ __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, in
         a0[r] = c0 < nbp ? row[c0] : 0.0;
         a1[r] = c1 < nbp ? row[c1] : 0.0;
     }
+    // Gram matrix G = striu(V^T V) of this panel for the trailing update: zero here,
+    // strict-upper entries filled below from the butterfly sums (see w0 / w1)
+#pragma unroll
+    for (int t = 0; t < kNBW * kNBW / 32; ++t) Gp[lane + 32 * t] = 0.0;
     // R entries of row i are read one column ahead: row i+1 is untouched until reflector i+1
     double x0n = Rd[0], rd0n = Rd[c0], rd1n = Rd[c1];
     // two columns per loop body (the column parity selects a0 / a1 at compile
@@ -1039,6 +1043,11 @@ __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, in
         s2 += __shfl_xor_sync(F, s2, 16);
         w0 += __shfl_xor_sync(F, w0, 16);
         w1 += __shfl_xor_sync(F, w1, 16);
+        // columns c < i hold their final reflector vectors, so w = v_c . v_i = G[c][i]
+        if (rg == 0) {
+            if (c0 < i) Gp[c0 * kNBW + i] = w0;
+            if (c1 < i) Gp[c1 * kNBW + i] = w1;
+        }
         // ---- reflector of panel column i (make_reflector semantics): s2 == 0 or
         // t <= 1e-280 is H = I (|beta u0| lies in [t, 2t]); testing t also keeps a
         // subnormal t away from rsqrt.approx.ftz, which would flush it to 0 (NaN
@@ -1191,20 +1200,9 @@ __device__ __forceinline__ void wy_trailing(double* __restrict__ C, int LDC, int
 // with one-panel look-ahead: while warps 1.. apply panel p's block reflector to
 // columns beyond panel p+1, warp 0 applies it to panel p+1's 16 columns and
 // factors panel p+1 -- the latency-bound panel chain overlaps the FMA-bound
-// trailing update.  Coefficients / G are double-buffered by panel parity.
-template <int ROWS>
-__device__ __forceinline__ void wy_gram(const double* C, int LDC, int p, int nbp, double* Gs) {
-    for (int e = threadIdx.x; e < kNBW * kNBW; e += blockDim.x) {
-        const int a = e / kNBW, b = e % kNBW;
-        double acc = 0.0, acc2 = 0.0;
-        if (a < b && b < nbp)
-            for (int r = 0; r < ROWS; r += 2) {
-                acc = fma(C[(size_t)r * LDC + p + a], C[(size_t)r * LDC + p + b], acc);
-                acc2 = fma(C[(size_t)(r + 1) * LDC + p + a], C[(size_t)(r + 1) * LDC + p + b], acc2);
-            }
-        Gs[e] = acc + acc2;
-    }
-}
+// trailing update.  Coefficients and G = striu(V^T V) (written by the panel
+// warp from its butterfly sums) are double-buffered by panel parity.  (wy_fold
+// follows the R diagonal-block helpers below.)
 
 // R diagonal block of panel p (16 x 16, upper part) <-> registers / shared memory.
 // The panel warp reads the NEXT panel's block one step early (its R rows are
@@ -1226,9 +1224,9 @@ __device__ __forceinline__ void rd_put(double* Rd, const double (&rr)[8]) {
 
 template <int ROWS>
 __device__ __forceinline__ void wy_panel_rd(double* C, int LDC, int n, int p, double* __restrict__ R, double* Rd,
-                                            double* cgv, double* cuv) {
+                                            double* cgv, double* cuv, double* Gp) {
     const int lane = threadIdx.x & 31, nbp = min(kNBW, n - p);
-    wy_panel<ROWS>(C, LDC, p, nbp, Rd, cgv, cuv);
+    wy_panel<ROWS>(C, LDC, p, nbp, Rd, cgv, cuv, Gp);
     for (int e = lane; e < kNBW * kNBW; e += 32) {
         const int i = e / kNBW, c = e % kNBW;
         if (i < nbp && c < nbp && c >= i) R[(size_t)(p + i) * n + p + c] = Rd[e];
@@ -1268,10 +1266,8 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
         rd_load(R, n, p, rdn);
         rd_put(Rd, rdn);
         rd_load(R, n, p + kNBW, rdn);
-        wy_panel_rd<ROWS>(C, LDC, n, p, R, Rd, cgv, cuv);
+        wy_panel_rd<ROWS>(C, LDC, n, p, R, Rd, cgv, cuv, Gs);
     }
-    __syncthreads();
-    wy_gram<ROWS>(C, LDC, p, min(kNBW, n - p), Gs);
     __syncthreads();
     for (;;) {
         const int pe = p + min(kNBW, n - p);
@@ -1285,14 +1281,16 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
             __syncwarp();
             rd_put(Rd, rdn);
             rd_load(R, n, pe + kNBW, rdn);
-            wy_panel_rd<ROWS>(C, LDC, n, pe, R, Rd, cgv + (buf ^ 1) * kNBW, cuv + (buf ^ 1) * kNBW);
+            wy_panel_rd<ROWS>(C, LDC, n, pe, R, Rd, cgv + (buf ^ 1) * kNBW, cuv + (buf ^ 1) * kNBW,
+                              Gs + (buf ^ 1) * kNBW * kNBW);
         } else if (warp == pw) {
             // look-ahead: wait until panel p+1's columns carry panel p's update, factor it
             rd_put(Rd, rdn);
             rd_load(R, n, pe + kNBW, rdn);
             named_bar_sync(1, nw * 32);
             if (lane0) qr_ev(1, p);
-            wy_panel_rd<ROWS>(C, LDC, n, pe, R, Rd, cgv + (buf ^ 1) * kNBW, cuv + (buf ^ 1) * kNBW);
+            wy_panel_rd<ROWS>(C, LDC, n, pe, R, Rd, cgv + (buf ^ 1) * kNBW, cuv + (buf ^ 1) * kNBW,
+                              Gs + (buf ^ 1) * kNBW * kNBW);
             if (lane0) qr_ev(5, p);
         } else {
             wy_trailing<ROWS>(C, LDC, n, p, pe, pe + nbn, tw, nw - 1, R, G0, g0, u0);   // panel p+1's columns first
@@ -1304,10 +1302,7 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
         if (lane0) qr_ev(2, p);
         publish(p / kNBW + 1);
         p = pe;
-        buf ^= 1;
-        wy_gram<ROWS>(C, LDC, p, min(kNBW, n - p), Gs + buf * kNBW * kNBW);
-        __syncthreads();
-        if (lane0) qr_ev(3, p - kNBW);
+        buf ^= 1;   // the panel warp wrote G of the new panel p with its reflectors
     }
     publish(npan);
 }
