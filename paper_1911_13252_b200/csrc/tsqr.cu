@@ -1008,6 +1008,7 @@ __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, in
     for (int t = 0; t < kNBW * kNBW / 32; ++t) Gp[lane + 32 * t] = 0.0;
     // R entries of row i are read one column ahead: row i+1 is untouched until reflector i+1
     double x0n = Rd[0], rd0n = Rd[c0], rd1n = Rd[c1];
+    double my_g = 0.0, my_u0 = 0.0, my_beta = 0.0;
     // two columns per loop body (the column parity selects a0 / a1 at compile
     // time); a full 16-column unroll overflows the instruction cache
 #pragma unroll 2
@@ -1063,14 +1064,12 @@ __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, in
                 g = -rs * rs * rcp_nr(1.0 + fabs(x0) * rs);   // = 1 / (beta u0)
             }
         }
-        if (cp == (i >> 1)) {
-#pragma unroll
-            for (int r = 0; r < RPL; ++r) C[(size_t)(rg + 4 * r) * LDC + p + i] = v[r];
-            if (rg == 0) {
-                cgv[i] = g;
-                cuv[i] = u0;
-                if (g != 0.0) Rd[i * kNBW + i] = beta;
-            }
+        // column i's coefficients are kept by lane i and stored after the loop
+        // (no divergent store branch on the per-column chain)
+        if (lane == i) {
+            my_g = g;
+            my_u0 = u0;
+            my_beta = beta;
         }
         if (g != 0.0 && i + 1 < nbp) {
             // ---- apply H_i to the panel columns right of i: W_j = u0 R[i][j] + v^T a_j
@@ -1087,6 +1086,18 @@ __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, in
                 if (l1) Rd[i * kNBW + c1] = fma(f1, u0, rd1);
             }
         }
+    }
+    // the reflector vectors: lane (rg, cp) holds final columns 2cp, 2cp+1 of its rows
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+        double* row = C + (size_t)(rg + 4 * r) * LDC + p;
+        if (c0 < nbp) row[c0] = a0[r];
+        if (c1 < nbp) row[c1] = a1[r];
+    }
+    if (lane < nbp) {
+        cgv[lane] = my_g;
+        cuv[lane] = my_u0;
+        if (my_g != 0.0) Rd[lane * kNBW + lane] = my_beta;
     }
     __syncwarp();
 }
