@@ -1053,17 +1053,17 @@ __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, in
         // t <= 1e-280 is H = I (|beta u0| lies in [t, 2t]); testing t also keeps a
         // subnormal t away from rsqrt.approx.ftz, which would flush it to 0 (NaN
         // reflector) -- it occurs in deep noise cascades of rank-deficient partial R
-        double g = 0.0, u0 = 0.0, beta = 0.0;
+        // branch-free (every lane takes the same path anyway): evaluate on a safe t,
+        // then select H = I
         const double t = fma(x0, x0, s2);
-        if (s2 != 0.0 && t > 1e-280) {
-            const double rs = rsqrt_nr(t);
-            beta = -(x0 >= 0.0 ? 1.0 : -1.0) * (t * rs);
-            const double uu = x0 - beta;
-            if (fabs(beta * uu) > 1e-280) {
-                u0 = uu;
-                g = -rs * rs * rcp_nr(1.0 + fabs(x0) * rs);   // = 1 / (beta u0)
-            }
-        }
+        const bool refl_ok = s2 != 0.0 && t > 1e-280;
+        const double ts = refl_ok ? t : 1.0;
+        const double rs = rsqrt_nr(ts);
+        const double bt = -(x0 >= 0.0 ? 1.0 : -1.0) * (ts * rs);
+        const double uu = x0 - bt;
+        const bool app = refl_ok && fabs(bt * uu) > 1e-280;
+        const double gg = -rs * rs * rcp_nr(1.0 + fabs(x0) * rs);   // = 1 / (beta u0)
+        const double g = app ? gg : 0.0, u0 = app ? uu : 0.0, beta = app ? bt : 0.0;
         // column i's coefficients are kept by lane i and stored after the loop
         // (no divergent store branch on the per-column chain)
         if (lane == i) {
@@ -1071,8 +1071,8 @@ __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, in
             my_u0 = u0;
             my_beta = beta;
         }
-        if (g != 0.0 && i + 1 < nbp) {
-            // ---- apply H_i to the panel columns right of i: W_j = u0 R[i][j] + v^T a_j
+        {   // ---- apply H_i to the panel columns right of i: W_j = u0 R[i][j] + v^T a_j
+            // (unconditionally: f = 0 when H_i = I or the column is not right of i)
             const bool l0 = c0 > i && c0 < nbp, l1 = c1 > i && c1 < nbp;
             const double f0 = l0 ? g * fma(u0, rd0, w0) : 0.0;
             const double f1 = l1 ? g * fma(u0, rd1, w1) : 0.0;
@@ -1081,7 +1081,7 @@ __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, in
                 a0[r] = fma(f0, v[r], a0[r]);
                 a1[r] = fma(f1, v[r], a1[r]);
             }
-            if (rg == 0) {
+            if (rg == 0 && g != 0.0) {
                 if (l0) Rd[i * kNBW + c0] = fma(f0, u0, rd0);
                 if (l1) Rd[i * kNBW + c1] = fma(f1, u0, rd1);
             }
