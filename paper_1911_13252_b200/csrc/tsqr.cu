@@ -1519,12 +1519,12 @@ static int threads_2d(int n) { return (4 * ((n + kTC2 - 1) / kTC2) + 31) / 32 * 
 // n = M+1 above this takes the WY leaf/merge and the wide solve (columns > threads).
 constexpr int kWideN = 1024;
 // Blocked compact-WY leaf + merge (wy_fold).  ELMRNN_TSQR_WY=0/1 overrides the default.
-// Measured (B200, profiles/): M = 256 WY 113 ms vs 147 ms per-column fold at
-// C4; M <= 128 the per-column fold is faster (C3 10.4 vs 11.8 ms).
 static bool use_wy(int n) {
     if (n > kWideN) return true;   // the only leaf/merge for more columns than CTA threads
     if (const char* e = std::getenv("ELMRNN_TSQR_WY")) return std::atoi(e) != 0;
-    return n > 192;
+    // measured (tools/qr_time.py, B200): M = 128 x 1M rows WY 8.6 vs per-column fold
+    // 10.4 ms; M = 64 x 100k rows 1.22 vs 0.93 ms
+    return n > 128;
 }
 // multi-output [H | Y_1..Y_P] (P > 1) always takes the WY leaf/merge and the wide solve
 static bool use_wy_h(const elmrnn* h) { return h->nrhs > 1 || use_wy(h->M + h->nrhs); }
