@@ -1011,7 +1011,12 @@ __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, in
     double my_g = 0.0, my_u0 = 0.0, my_beta = 0.0;
     // two columns per loop body (the column parity selects a0 / a1 at compile
     // time); a full 16-column unroll overflows the instruction cache
-#pragma unroll 2
+#ifndef ELM_PANEL_UNROLL
+#define ELM_PANEL_UNROLL 2
+#endif
+#define ELM_PRAGMA_(x) _Pragma(#x)
+#define ELM_UNROLL_(n) ELM_PRAGMA_(unroll n)
+    ELM_UNROLL_(ELM_PANEL_UNROLL)
     for (int i = 0; i < kNBW; ++i) {
         if (i >= nbp) break;
         constexpr unsigned F = 0xffffffffu;
