@@ -1252,7 +1252,7 @@ __device__ __forceinline__ void wy_panel_rd(double* C, int LDC, int n, int p, do
 template <int ROWS>
 __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* __restrict__ R, double* Gs,
                         double* Rd, double* cgv, double* cuv, int pw, const int* pred_prog = nullptr,
-                        int* my_prog = nullptr) {
+                        int* my_prog = nullptr, bool la_wait = false) {
     const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int tw = warp < pw ? warp : warp - 1;
     const bool lane0 = (threadIdx.x & 31) == 0 && warp == pw;
@@ -1311,7 +1311,10 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
         } else {
             wy_trailing<ROWS>(C, LDC, n, p, pe, pe + nbn, tw, nw - 1, R, G0, g0, u0);   // panel p+1's columns first
             __threadfence_block();
-            named_bar_arrive(1, nw * 32);
+            // warps without a look-ahead tile wait with the panel warp (ELMRNN_WY_LA_WAIT, testing
+            // aid) so the look-ahead chain is not slowed by their trailing work
+            if (la_wait && 8 * tw >= nbn) named_bar_sync(1, nw * 32);
+            else named_bar_arrive(1, nw * 32);
             wy_trailing<ROWS>(C, LDC, n, p, pe + nbn, n, tw, nw - 1, R, G0, g0, u0);
         }
         __syncthreads();
@@ -1346,7 +1349,7 @@ template <int ROWS>
 __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
     k_tsqr_leaf_wy(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t ldy, int P,
                    int64_t N, int M, double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag,
-                   int* sm_slot) {
+                   int* sm_slot, int la_wait) {
     extern __shared__ __align__(16) double wsm[];
     // columns [0, M) of the tile are H, [M, M + P) the P outputs Y[row][0..P-1] (row stride ldy)
     const int n = M + P, LDC = wy_ldc(n), tid = threadIdx.x, nt = blockDim.x;
@@ -1407,7 +1410,7 @@ __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
             }
         }
         __syncthreads();
-        wy_fold<ROWS>(C, LDC, n, 0, R, Gs, Rd, cgv, cuv, pw);
+        wy_fold<ROWS>(C, LDC, n, 0, R, Gs, Rd, cgv, cuv, pw, nullptr, nullptr, la_wait != 0);
     }
     if (bad) atomicOr(flag, 1);
 }
@@ -1531,6 +1534,14 @@ static bool use_wy(int n) {
     // 10.4 ms; M = 64 x 100k rows 1.22 vs 0.93 ms
     return n > 128;
 }
+// Look-ahead isolation in the leaf: trailing warps without a look-ahead tile
+// wait for the look-ahead columns with the panel warp instead of competing with
+// that chain (measured C4 shape 81.6 -> 80.3 ms; neutral at 8 warps, n > 320).
+// ELMRNN_WY_LA_WAIT=0/1 overrides (testing aid).
+static int wy_la_wait(int n) {
+    const char* e = std::getenv("ELMRNN_WY_LA_WAIT");
+    return e ? std::atoi(e) : (n <= 320 ? 1 : 0);
+}
 // multi-output [H | Y_1..Y_P] (P > 1) always takes the WY leaf/merge and the wide solve
 static bool use_wy_h(const elmrnn* h) { return h->nrhs > 1 || use_wy(h->M + h->nrhs); }
 static bool wide_solve(const elmrnn* h) { return h->nrhs > 1 || h->M + h->nrhs > kWideN; }
@@ -1597,6 +1608,10 @@ int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
         return ps < 1 ? 1 : ps;
     });
     int64_t maxc = (int64_t)per_sm * h->sm_count;
+    if (const char* e = std::getenv("ELMRNN_TSQR_MAXSLABS")) {   // testing aid
+        const int64_t v = std::atoll(e);
+        if (v >= 1 && v < maxc) maxc = v;
+    }
     // at least n rows per leaf: a leaf R with fewer rows is rank deficient
     // and its noise rows only cost merges (and risk underflow cascades)
     int64_t byrows = N / n;
@@ -1741,7 +1756,7 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
             int* slot = reinterpret_cast<int*>(h->sdev + 1);   // per-SM arrival counters (ensure_solve_ws)
             cudaMemsetAsync(slot, 0, 1024 * sizeof(int), h->stream);
             k_tsqr_leaf_wy<RW><<<(unsigned)slabs, wy_threads(n), sm, h->stream>>>(
-                H, ldh, Y, ldy, h->nrhs, N, h->M, h->Rws, rows, h->flag, slot);
+                H, ldh, Y, ldy, h->nrhs, N, h->M, h->Rws, rows, h->flag, slot, wy_la_wait(n));
             h->launches++;
             return cudaGetLastError();
         });
