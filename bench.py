@@ -45,6 +45,9 @@ WORKLOAD_NAMES = {
     "C3lstm_diag": "C3 shape, LSTM with diagonal U (paper-literal per-cell) N=1M Q=30 M=128 d=4",
     "C3gru_diag": "C3 shape, GRU with diagonal U (paper-literal per-cell) N=1M Q=30 M=128 d=4",
     "C3fc_eq8": "C3 shape, fully connected by the letter of Eq. 8 (per-cell) N=1M Q=30 M=128 d=4",
+    "C2n_ef": "C2 NARMAX with error feedback (two passes: e = y - yhat(beta0), rebuild, re-solve) N=100k Q=20 M=64",
+    "C5lstm1024": "C5 LSTM M=1024 Q=10 d=1, one GPU's share (N=2M of 16M), Mackey-Glass + noise",
+    "C5gru1024": "C5 GRU M=1024 Q=10 d=1, one GPU's share (N=2M of 16M), Mackey-Glass + noise",
 }
 
 
@@ -149,15 +152,18 @@ def cpu_oracle_rate(cfg: str, n_sub: int, X, Y, threads: int, weight_grid: int =
     net = orc.Net(c["arch"], S=c["S"], M=c["M"], Q=c["Q"], weight_grid=weight_grid)
     blocks = orc.gen_weights(net, 1)
     t0 = time.perf_counter()
-    H = orc.build_H(net, blocks, X[:n_sub], threads=threads)
-    orc.lstsq(H, Y[:n_sub])
+    if c.get("mode") == "ef":
+        orc.train_narmax_ef(net, blocks, X[:n_sub], Y[:n_sub], None, threads=threads)
+    else:
+        H = orc.build_H(net, blocks, X[:n_sub], threads=threads)
+        orc.lstsq(H, Y[:n_sub])
     dt = time.perf_counter() - t0
     return n_sub / dt, dt
 
 
 def oracle_sample_rows(cfg: str) -> int:
     c = sy.CONFIGS[cfg]
-    f = algorithmic_flops_per_sample(c["arch"], c["S"], c["M"], c["Q"])
+    f = algorithmic_flops_per_sample(c["arch"], c["S"], c["M"], c["Q"]) + 2 * (c["M"] + 1) ** 2
     # ~2 GFLOP/s per core of plain fp64 loops, all cores, aim at ~10 s
     rows = int(10.0 * 2.0e9 * max(1, os.cpu_count() or 1) / max(f, 1.0))
     return int(min(c["N"], max(2 * (c["M"] + 1), min(rows, 200_000))))
@@ -237,6 +243,10 @@ def main():
     model = ELMRNN(c["arch"], c["S"], c["M"], c["Q"], seed=1, force_path=args.force_path,
                    weight_grid=args.weight_grid)
     stream = torch.cuda.current_stream()
+    two_pass = c.get("mode") == "ef"
+    if two_pass and world > 1:
+        raise SystemExit("C2n_ef: the error windows cross shard boundaries; single GPU only")
+    Ef = torch.empty((N_local, c["Q"]), dtype=torch.float32, device="cuda") if two_pass else None
 
     def step(ev_b0=None, ev_b1=None):
         if ev_b0 is not None:
@@ -248,6 +258,10 @@ def main():
             model.solve_beta(Hd, Yd, beta, info=False)
         else:
             par.solve_sharded(model, Hd, Yd, N_total, beta)
+        if two_pass:   # e = y - yhat(beta0), rebuild H with e, re-solve
+            model.error_windows(Hd, Yd, beta, Ef)
+            model.build_H(Xd, None, Hd, Ef=Ef)
+            model.solve_beta(Hd, Yd, beta, info=False)
 
     def barrier():
         if world > 1:
@@ -324,6 +338,10 @@ def main():
                 model.solve_beta(Hd, Yd, beta, info=False)
             else:
                 par.solve_sharded(model, Hd, Yd, N_total, beta)
+            if two_pass:
+                model.error_windows(Hd, Yd, beta, Ef)
+                model.build_H(Xd, None, Hd, Ef=Ef)
+                model.solve_beta(Hd, Yd, beta, info=False)
             beta_h.copy_(beta, non_blocking=True)
             stream.synchronize()
 

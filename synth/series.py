@@ -120,6 +120,11 @@ CONFIGS = {
     "C3lstm_diag": dict(arch="lstm_diag", series="sin4", N=1_000_000, Q=30, S=4, M=128, noise=0.0),
     "C3gru_diag": dict(arch="gru_diag", series="sin4", N=1_000_000, Q=30, S=4, M=128, noise=0.0),
     "C3fc_eq8": dict(arch="fc_eq8", series="sin4", N=1_000_000, Q=30, S=4, M=128, noise=0.0),
+    # NARMAX with real error feedback (two passes) at the C2 shape
+    "C2n_ef": dict(arch="narmax", series="ar5", N=100_000, Q=20, S=1, M=64, noise=0.0, mode="ef"),
+    # C5 (BASELINE configs[4]) widest point, one GPU's share of N = 16M over 8 GPUs
+    "C5lstm1024": dict(arch="lstm", series="mg", N=2_000_000, Q=10, S=1, M=1024, noise=0.01),
+    "C5gru1024": dict(arch="gru", series="mg", N=2_000_000, Q=10, S=1, M=1024, noise=0.01),
 }
 
 
