@@ -696,3 +696,24 @@ def test_solve_beta_multi_ridge_and_trained():
     cond = np.linalg.cond(io2[0].R[:M2, :M2])
     for p in range(2):
         assert np.linalg.norm(B2[p].cpu().numpy() - Bo2[p]) / np.linalg.norm(Bo2[p]) <= 1e-12 * cond
+
+
+@pytest.mark.parametrize("M,P", [(256, 2), (256, 5), (300, 8), (128, 3)])
+def test_virtual_ranks_wy_pipelined_merge(M, P):
+    """Row-sharded solve on one GPU through the WY path: P local TSQRs, then
+    elmrnn_solve_merge (unpack + pipelined merge tree + solve) equals the single
+    solve, and both match the oracle's Householder lstsq of the same H."""
+    N = 6000 + 37 * P
+    g = torch.Generator(device="cuda").manual_seed(M * P)
+    H = torch.rand(N, M, device="cuda", generator=g) - 0.5
+    Y = torch.rand(N, device="cuda", generator=g) - 0.5
+    e = E("lstm", 1, M, 4, 1, force_path=1)
+    b1, i1 = e.solve_beta(H, Y)
+    cuts = np.linspace(0, N, P + 1).astype(int)
+    parts = [e.solve_local(H[a:b], Y[a:b]).clone() for a, b in zip(cuts[:-1], cuts[1:])]
+    bP, iP = e.solve_merge(torch.stack(parts), P, N)
+    bo, io = orc.lstsq(H.double().cpu().numpy(), Y.double().cpu().numpy())
+    cond = np.linalg.cond(io.R[:M, :M])
+    assert float((bP - b1).norm() / b1.norm()) <= 1e-12 * cond
+    assert np.linalg.norm(bP.cpu().numpy() - bo) / np.linalg.norm(bo) <= 1e-12 * cond
+    assert iP.rmse == pytest.approx(io.rmse, rel=1e-10)
