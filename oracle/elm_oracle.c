@@ -474,26 +474,39 @@ typedef struct {
 
 /* In-place Householder QR of A (m x n, row-major, lda).  On return the upper
  * triangle of A[0:min(m,n), :] holds R. */
+/* Threads for the column updates of orc_householder (default 1).  Each column
+ * j's update is computed by one thread in the same order for any thread count,
+ * so the result is bitwise identical. */
+static int g_qr_threads = 1;
+void orc_set_qr_threads(int t) { g_qr_threads = t < 1 ? 1 : t; }
+
 static void orc_householder(double* A, int64_t m, int n, int64_t lda) {
+    /* A is stored COLUMN-major: element (i, j) at A[j * lda + i] (lda >= m),
+     * so every loop over i below is a contiguous sweep. */
+#define AE(i, j) A[(int64_t)(j) * lda + (i)]
     for (int k = 0; k < n && k < m; ++k) {
-        double x0 = A[(int64_t)k * lda + k];
+        double x0 = AE(k, k);
         double sigma2 = 0.0;
-        for (int64_t i = k + 1; i < m; ++i) sigma2 += A[i * lda + k] * A[i * lda + k];
+        for (int64_t i = k + 1; i < m; ++i) sigma2 += AE(i, k) * AE(i, k);
         double sigma = sqrt(sigma2);
         if (sigma == 0.0) continue;                      /* tau = 0, H = I */
         double beta = -(x0 >= 0 ? 1.0 : -1.0) * hypot(x0, sigma);
         double tau = (beta - x0) / beta;
         double inv = 1.0 / (x0 - beta);
-        for (int64_t i = k + 1; i < m; ++i) A[i * lda + k] *= inv;  /* v (v0 = 1 implicit) */
-        A[(int64_t)k * lda + k] = beta;
+        for (int64_t i = k + 1; i < m; ++i) AE(i, k) *= inv;  /* v (v0 = 1 implicit) */
+        AE(k, k) = beta;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(g_qr_threads) if (g_qr_threads > 1 && (m - k) * (int64_t)(n - k) > 65536)
+#endif
         for (int j = k + 1; j < n; ++j) {
-            double w = A[(int64_t)k * lda + j];
-            for (int64_t i = k + 1; i < m; ++i) w += A[i * lda + k] * A[i * lda + j];
-            A[(int64_t)k * lda + j] -= tau * w;
-            for (int64_t i = k + 1; i < m; ++i) A[i * lda + j] -= tau * A[i * lda + k] * w;
+            double w = AE(k, j);
+            for (int64_t i = k + 1; i < m; ++i) w += AE(i, k) * AE(i, j);
+            AE(k, j) -= tau * w;
+            for (int64_t i = k + 1; i < m; ++i) AE(i, j) -= tau * AE(i, k) * w;
         }
-        for (int64_t i = k + 1; i < m; ++i) A[i * lda + k] = 0.0;
+        for (int64_t i = k + 1; i < m; ++i) AE(i, k) = 0.0;
     }
+#undef AE
 }
 
 /* Solve from the (M+1)x(M+1) upper-triangular R of [H|Y] (row-major, full
@@ -519,11 +532,16 @@ int orc_solve_from_R(double* Rf, int M, int64_t n_total, double* beta, orc_info*
     if (ridge) {
         lambda = 1e-8 * fro2 / (double)M;
         double sl = sqrt(lambda);
-        big = (double*)calloc((size_t)(2 * M) * n, sizeof(double));
+        /* [R[:M, :]; sqrt(lambda) (I | 0)], 2M x n, column-major for orc_householder */
+        double* cm = (double*)calloc((size_t)(2 * M) * n, sizeof(double));
         for (int k = 0; k < M; ++k)
-            for (int j = 0; j < n; ++j) big[(int64_t)k * n + j] = Rf[(int64_t)k * n + j];
-        for (int k = 0; k < M; ++k) big[(int64_t)(M + k) * n + k] = sl;
-        orc_householder(big, 2 * M, n, n);
+            for (int j = 0; j < n; ++j) cm[(int64_t)j * (2 * M) + k] = Rf[(int64_t)k * n + j];
+        for (int k = 0; k < M; ++k) cm[(int64_t)k * (2 * M) + M + k] = sl;
+        orc_householder(cm, 2 * M, n, 2 * M);
+        big = (double*)calloc((size_t)M * n, sizeof(double));   /* its R, row-major */
+        for (int k = 0; k < M; ++k)
+            for (int j = k; j < n; ++j) big[(int64_t)k * n + j] = cm[(int64_t)j * (2 * M) + k];
+        free(cm);
         for (int k = 0; k < M; ++k)
             if (big[(int64_t)k * n + k] < 0)
                 for (int j = k; j < n; ++j) big[(int64_t)k * n + j] = -big[(int64_t)k * n + j];
@@ -563,20 +581,20 @@ int orc_lstsq(const double* H, int64_t ldh, const double* Y, int64_t N, int M,
               double* beta, orc_info* info, double* Rout) {
     int n = M + 1;
     if (N < M || M < 1) return -3;
-    double* A = (double*)malloc(sizeof(double) * (size_t)N * n);
+    double* A = (double*)malloc(sizeof(double) * (size_t)N * n);   /* [H | Y], column-major */
     for (int64_t i = 0; i < N; ++i) {
         for (int j = 0; j < M; ++j) {
             double v = H[i * ldh + j];
             if (!isfinite(v)) { free(A); return -4; }
-            A[i * n + j] = v;
+            A[(int64_t)j * N + i] = v;
         }
         if (!isfinite(Y[i])) { free(A); return -4; }
-        A[i * n + M] = Y[i];
+        A[(int64_t)M * N + i] = Y[i];
     }
-    orc_householder(A, N, n, n);
+    orc_householder(A, N, n, N);
     double* Rf = (double*)calloc((size_t)n * n, sizeof(double));
     for (int k = 0; k < n && k < N; ++k)
-        for (int j = k; j < n; ++j) Rf[(int64_t)k * n + j] = A[(int64_t)k * n + j];
+        for (int j = k; j < n; ++j) Rf[(int64_t)k * n + j] = A[(int64_t)j * N + k];
     free(A);
     int rc = orc_solve_from_R(Rf, M, N, beta, info);
     if (Rout) memcpy(Rout, Rf, sizeof(double) * (size_t)n * n);

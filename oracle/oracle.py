@@ -78,6 +78,8 @@ def lib():
         L.orc_predict.restype = None
         L.orc_rng_u64.argtypes = [u64]
         L.orc_rng_u64.restype = u64
+        L.orc_set_qr_threads.argtypes = [i32]
+        L.orc_set_qr_threads.restype = None
         L.orc_max_threads.argtypes = []
         L.orc_max_threads.restype = i32
     return _lib
@@ -193,6 +195,12 @@ class SolveInfo:
     n_total: int
     status: int
     R: np.ndarray
+
+
+def set_qr_threads(t: int) -> None:
+    """Threads for the column updates of the Householder QR (bitwise identical
+    result for any count: each column is updated by one thread in fixed order)."""
+    lib().orc_set_qr_threads(int(t))
 
 
 def lstsq(H, Y):

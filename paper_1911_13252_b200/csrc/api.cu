@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -60,6 +61,11 @@ elmrnn_status elmrnn_init_ex(elmrnn_t* out, int arch, int d, int M, int Q, uint6
     h->force_path = o.force_path; h->seed = seed; h->G = gates_of(arch); h->stream = nullptr;
     h->path = 1;
     h->nrhs = 1;
+    if (const char* t = std::getenv("ELMRNN_TESTING"); t && std::atoi(t) == 1) {   // test overrides, read once
+        if (const char* e = std::getenv("ELMRNN_TSQR_WY")) h->tune.tsqr_wy = std::atoi(e);
+        if (const char* e = std::getenv("ELMRNN_TSQR_WY_ROWS")) h->tune.wy_rows = std::atoi(e);
+        if (const char* e = std::getenv("ELMRNN_PW_MODE")) h->tune.pw_mode = std::atoi(e);
+    }
     cudaError_t e;
     if ((e = cudaGetDevice(&h->device))) { elmrnn_destroy(h); return cuda_fail(nullptr, e, "cudaGetDevice"); }
     if ((e = cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device))) {

@@ -25,6 +25,15 @@ struct SolveDev {
     long long n_total;
 };
 
+// Tuning overrides: defaults are the measured choices; a test may override them
+// through the environment ONLY when ELMRNN_TESTING=1 is set, and they are read
+// once, at elmrnn_init_ex (never on the solve path).
+struct Tune {
+    int tsqr_wy = -1;   // ELMRNN_TSQR_WY: 1 force the blocked-WY TSQR, 0 force the per-column fold
+    int wy_rows = 0;    // ELMRNN_TSQR_WY_ROWS: WY leaf tile rows (8..96)
+    int pw_mode = 1;    // ELMRNN_PW_MODE: WY leaf panel warp 0 rotate SMSPs per CTA, 1 pin to SMSP 0
+};
+
 }  // namespace elm
 
 // The opaque handle.  Weights are stored in kernel-friendly packed layouts
@@ -70,6 +79,7 @@ struct elmrnn {
     float* scratch;       // builder scratch (FC history ring)
     size_t scratch_bytes;
     int64_t launches;
+    elm::Tune tune;
     std::string err;
 };
 

@@ -209,11 +209,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                         ptx::mma_f16_ts(d, tah, dbh, idesc, ks != 0);
                         ptx::mma_f16_ts(d, tal, dbh, idesc, 1);
                         if (!two) ptx::mma_f16_ts(d, tah, dbl, idesc, 1);
+#ifdef ELM_TC_FOUR_PASS   // accuracy experiment: + lo.lo
+                        if (!two) ptx::mma_f16_ts(d, tal, dbl, idesc, 1);
+#endif
 #pragma unroll
                         for (int kk = 1; kk < 4; ++kk) {
                             ptx::mma_f16_ts(d, tah + kk * 8, dbh + 2 * kk, idesc, 1);
                             ptx::mma_f16_ts(d, tal + kk * 8, dbh + 2 * kk, idesc, 1);
                             if (!two) ptx::mma_f16_ts(d, tah + kk * 8, dbl + 2 * kk, idesc, 1);
+#ifdef ELM_TC_FOUR_PASS
+                            if (!two) ptx::mma_f16_ts(d, tal + kk * 8, dbl + 2 * kk, idesc, 1);
+#endif
                         }
                         ptx::mma_commit(empty + st);                  // frees the U stage
                         // last chunk of the step: A slice ks is free for h(t) once these MMAs retire
@@ -330,6 +336,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                                 for (int s = 0; s < SS; ++s) v = fmaf(xs[s], w[g * (SS + 1) + 1 + s], v);
                                 arg[g] = fminf(v, 30.0f);   // only large positive arguments can overflow
                             }
+#ifdef ELM_TC_EPI_ACCURATE   // accuracy experiment: libm-accurate gates
+                            so[nb] = 1.0f / (1.0f + exp2f(arg[0]));
+                            const float tc = tanhf(arg[1] * 0.34657359027997264f);
+                            const float sl = 1.0f / (1.0f + exp2f(arg[2])), si = 1.0f / (1.0f + exp2f(arg[3]));
+                            const int ci = n * 8 + 4 * g4 + nb;
+                            const float cn = fmaf(sl, c[ci], si * tc);
+                            c[ci] = cn;
+                            dc[nb] = cn;
+#else
                             const float d0 = 1.0f + ex2_approx(arg[0]);   // o
                             const float d1 = 1.0f + ex2_approx(arg[1]);   // c~ (tanh)
                             const float d2 = 1.0f + ex2_approx(arg[2]);   // lambda
@@ -344,7 +359,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                             const float cn = fmaf(sl, c[ci], si * tc);
                             c[ci] = cn;
                             dc[nb] = 1.0f + ex2_approx(fminf(2.8853900817779268f * cn, 30.0f));
+#endif
                         }
+#ifdef ELM_TC_EPI_ACCURATE
+#pragma unroll
+                        for (int nb = 0; nb < 4; ++nb) hv[4 * g4 + nb] = so[nb] * tanhf(dc[nb]);
+                        continue;
+#endif
                         const float p01 = dc[0] * dc[1], p23 = dc[2] * dc[3];
                         const float rr = rcp_approx(p01 * p23);
                         const float r01 = rr * p23, r23 = rr * p01;
@@ -366,7 +387,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                     }
                     if (t == p.Q && valid) {
                         float* d1 = p.H + row * p.ldh + n * 32 + 8 * u;
-                        if ((p.ldh & 3) == 0) {
+                        if (((p.ldh | (int64_t)(reinterpret_cast<uintptr_t>(p.H) >> 2)) & 3) == 0) {
                             float4* dst = reinterpret_cast<float4*>(d1);
                             dst[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
                             dst[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);

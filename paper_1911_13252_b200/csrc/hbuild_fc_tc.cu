@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_fc_tc(const __grid_constant__ 
                     if (lane == 0) ptx::mbar_arrive(hist_ready);
                 } else if (valid) {
                     float* dst = p.H + row * p.ldh + 32 * u;
-                    if ((p.ldh & 3) == 0) {
+                    if (((p.ldh | (int64_t)(reinterpret_cast<uintptr_t>(p.H) >> 2)) & 3) == 0) {
 #pragma unroll
                         for (int c = 0; c < 8; ++c)
                             reinterpret_cast<float4*>(dst)[c] =

@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                     }
                     if (t == p.Q && valid) {
                         float* d1 = p.H + row * p.ldh + 64 * c + 16 * u;
-                        if ((p.ldh & 3) == 0) {
+                        if (((p.ldh | (int64_t)(reinterpret_cast<uintptr_t>(p.H) >> 2)) & 3) == 0) {
                             float4* dst = reinterpret_cast<float4*>(d1);
 #pragma unroll
                             for (int i = 0; i < 4; ++i)

@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
                             put_hilo8(img + (size_t)(t & 1) * img_bytes, r, j0, hp);
                         } else if (valid) {
                             float* d1 = p.H + row * p.ldh + j0;
-                            if ((p.ldh & 3) == 0) st8(d1, hp);
+                            if (((p.ldh | (int64_t)(reinterpret_cast<uintptr_t>(p.H) >> 2)) & 3) == 0) st8(d1, hp);
                             else {
 #pragma unroll
                                 for (int i = 0; i < 8; ++i) d1[i] = hp[i];

@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
                         *reinterpret_cast<uint4*>(sl + kWTile + off) = lo;
                     } else if (valid) {
                         float* d1 = p.H + row * p.ldh + n * 32 + 8 * u;
-                        if ((p.ldh & 3) == 0) {
+                        if (((p.ldh | (int64_t)(reinterpret_cast<uintptr_t>(p.H) >> 2)) & 3) == 0) {
                             float4* dst = reinterpret_cast<float4*>(d1);
                             dst[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
                             dst[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);

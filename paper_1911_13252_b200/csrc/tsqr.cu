@@ -118,7 +118,7 @@ __device__ __forceinline__ void make_reflector(const double (&a)[TR], double x0,
 // Column owned by this thread (adjacent lanes share a column when P = 2).
 // A reversed mapping (look-ahead column in the highest warp) was measured
 // slower (2200 vs 2055 cycles per column), so columns map in order.
-template <int P, bool BLK>
+template <int P>
 __device__ __forceinline__ int col_of(int n) {
     return (int)(threadIdx.x / P);
 }
@@ -146,7 +146,7 @@ __device__ __forceinline__ void qr_ev(int slot, int k) {
 template <int TR, int P>
 __device__ void fold_tile(double (&a)[TR], int n, int k0, double* __restrict__ R, double* vbuf, double* coefs) {
     constexpr int ROWS = TR * P;
-    const int j = col_of<P, false>(n), half = threadIdx.x % P;
+    const int j = col_of<P>(n), half = threadIdx.x % P;
     const bool own = j >= 0 && j < n;
     // R[k][j] for the next three rows are prefetched into registers: the
     // reflector of column k+1 needs R[k+1][k+1] right after its own update,
@@ -204,238 +204,15 @@ __device__ void fold_tile(double (&a)[TR], int n, int k0, double* __restrict__ R
     }
 }
 
-// ---- lagged fold: critical path isolated from the trailing updates --------------------
-// Round k: phase A -- the owner of column k alone applies the pending reflector
-// k-1 to its column and builds reflector k (the FP64 pipe is otherwise idle,
-// so this latency chain runs uncontended); barrier; phase B -- every column
-// j > k applies reflector k-1; barrier.  In the look-ahead fold_tile the
-// critical chain shares the FP64 pipe with all trailing updates and was
-// measured ~3.5x slower than its uncontended length (profiles/).
-template <int TR, int P>
-__device__ __forceinline__ void apply_reflector(double (&a)[TR], double& rkj, const double* vbase, double g, double u0,
-                                                int half, unsigned mask) {
-    const double2* v = reinterpret_cast<const double2*>(vbase + half * TR);
-    double w0 = (half == 0) ? u0 * rkj : 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
-#pragma unroll
-    for (int i = 0; i < TR; i += 4) {
-        const double2 va = v[i / 2], vb = v[i / 2 + 1];
-        w0 = fma(va.x, a[i], w0);
-        w1 = fma(va.y, a[i + 1], w1);
-        w2 = fma(vb.x, a[i + 2], w2);
-        w3 = fma(vb.y, a[i + 3], w3);
-    }
-    double w = (w0 + w1) + (w2 + w3);
-    if (P == 2) w += __shfl_xor_sync(mask, w, 1);
-    const double f = g * w;
-    rkj = fma(f, u0, rkj);
-#pragma unroll
-    for (int i = 0; i < TR; i += 2) {
-        const double2 vv = v[i / 2];
-        a[i] = fma(f, vv.x, a[i]);
-        a[i + 1] = fma(f, vv.y, a[i + 1]);
-    }
-}
 
 template <int TR, int P>
-__device__ void fold_tile_lag(double (&a)[TR], int n, int k0, double* __restrict__ R, double* vbuf, double* coefs) {
-    constexpr int ROWS = TR * P;
-    const int j = threadIdx.x / P, half = threadIdx.x % P;
-    const bool own = j < n;
-    const double* Rj = R + j;
-    auto ld = [&](int row) -> double { return (own && row < n && j >= row) ? Rj[(size_t)row * n] : 0.0; };
-    // the R entry of the pending row (k-1) for this column, prefetched
-    double rcur = ld(k0), rnext = ld(k0 + 1);
-    {
-        const unsigned m = __ballot_sync(0xffffffffu, j == k0);
-        if (j == k0)
-            make_reflector<TR, P>(a, rcur, vbuf + (k0 & 1) * ROWS, coefs + 2 * (k0 & 1), R + (size_t)k0 * n + k0,
-                                  half, m);
-    }
-    __syncthreads();
-    for (int k = k0 + 1; k <= n; ++k) {
-        // rcur = R[k-1][j] (row of the pending reflector), rnext = R[k][j]
-        const double* vb = vbuf + ((k - 1) & 1) * ROWS;
-        const double g = coefs[2 * ((k - 1) & 1)], u0 = coefs[2 * ((k - 1) & 1) + 1];
-        // ---- phase A: column k alone
-        const bool crit = (j == k) && k < n;
-        const unsigned mc = __ballot_sync(0xffffffffu, crit);
-        if (crit) {
-            if (g != 0.0) {
-                apply_reflector<TR, P>(a, rcur, vb, g, u0, half, mc);
-                if (half == 0) R[(size_t)(k - 1) * n + j] = rcur;
-            }
-            make_reflector<TR, P>(a, rnext, vbuf + (k & 1) * ROWS, coefs + 2 * (k & 1), R + (size_t)k * n + k, half,
-                                  mc);
-        }
-        __syncthreads();
-        // ---- phase B: columns j > k apply reflector k-1
-        const bool upd = own && j > k && g != 0.0;
-        const unsigned mu = __ballot_sync(0xffffffffu, upd);
-        if (upd) {
-            apply_reflector<TR, P>(a, rcur, vb, g, u0, half, mu);
-            if (half == 0) R[(size_t)(k - 1) * n + j] = rcur;
-        }
-        rcur = rnext;
-        rnext = ld(k + 1);
-        __syncthreads();
-    }
-}
-
-// ---- blocked fold (panels of kNB columns) -------------------------------------------
-// Same reflectors as fold_tile, applied panel by panel: the warp owning the
-// kNB panel columns factors the panel warp-synchronously (shuffles and
-// __syncwarp, no block barriers), publishing the reflector tails Y and
-// (g, u0) in shared memory; then every trailing column applies the kNB
-// reflectors back to back.  The R rows of the panel live in shared memory
-// for the duration of the panel.  Four block barriers per panel instead of
-// one per column.  Requires P = 2 and k0 % kNB == 0.
-constexpr int kNB = 16;
-
-template <int TR>
-__device__ void fold_tile_blk(double (&a)[TR], int n, int k0, double* __restrict__ R, double* Rp, double* Yb,
-                              double* cf) {
-    constexpr int ROWS = 2 * TR;
-    const int tid = threadIdx.x, j = tid >> 1, half = tid & 1, warp = tid >> 5;
-    const bool own = j < n;
-    for (int pk = k0; pk < n; pk += kNB) {
-        const int pe = min(pk + kNB, n), np = pe - pk;
-        for (int idx = tid; idx < np * n; idx += blockDim.x) {
-            const int r = idx / n, c = idx - r * n;
-            Rp[idx] = (c >= pk + r) ? R[(size_t)(pk + r) * n + c] : 0.0;
-        }
-        __syncthreads();
-        if (warp == (pk >> 4)) {
-            // ---- panel factorisation (columns pk..pe-1 live in this warp)
-            for (int kk = pk; kk < pe; ++kk) {
-                const int r = kk - pk;
-                double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-                if (j == kk) {
-#pragma unroll
-                    for (int i = 0; i < TR; i += 4) {
-                        p0 = fma(a[i], a[i], p0);
-                        p1 = fma(a[i + 1], a[i + 1], p1);
-                        p2 = fma(a[i + 2], a[i + 2], p2);
-                        p3 = fma(a[i + 3], a[i + 3], p3);
-                    }
-                }
-                double s2 = (p0 + p1) + (p2 + p3);
-                s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
-                if (j == kk) {
-                    double g = 0.0, u0 = 0.0;
-                    if (s2 != 0.0) {
-                        const double x0 = Rp[r * n + kk];
-                        const double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * sqrt_fast(fma(x0, x0, s2));
-                        if (fabs(beta * (x0 - beta)) > 1e-280) {   // see make_reflector
-                            u0 = x0 - beta;
-                            g = rcp_fast(beta * u0);
-                            if (half == 0) Rp[r * n + kk] = beta;
-                        }
-                    }
-#pragma unroll
-                    for (int i = 0; i < TR; ++i) Yb[r * ROWS + half * TR + i] = a[i];
-                    if (half == 0) {
-                        cf[2 * r] = g;
-                        cf[2 * r + 1] = u0;
-                    }
-                }
-                __syncwarp();
-                const double g = cf[2 * r], u0 = cf[2 * r + 1];
-                const bool upd = j > kk && j < pe && g != 0.0;
-                double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
-                if (upd) {
-                    const double2* y = reinterpret_cast<const double2*>(Yb + r * ROWS + half * TR);
-                    if (half == 0) w0 = u0 * Rp[r * n + j];
-#pragma unroll
-                    for (int i = 0; i < TR; i += 4) {
-                        const double2 ya = y[i / 2], yb = y[i / 2 + 1];
-                        w0 = fma(ya.x, a[i], w0);
-                        w1 = fma(ya.y, a[i + 1], w1);
-                        w2 = fma(yb.x, a[i + 2], w2);
-                        w3 = fma(yb.y, a[i + 3], w3);
-                    }
-                }
-                double w = (w0 + w1) + (w2 + w3);
-                w += __shfl_xor_sync(0xffffffffu, w, 1);
-                if (upd) {
-                    const double f = g * w;
-                    const double2* y = reinterpret_cast<const double2*>(Yb + r * ROWS + half * TR);
-                    if (half == 0) Rp[r * n + j] = fma(f, u0, Rp[r * n + j]);
-#pragma unroll
-                    for (int i = 0; i < TR; i += 2) {
-                        const double2 yy = y[i / 2];
-                        a[i] = fma(f, yy.x, a[i]);
-                        a[i + 1] = fma(f, yy.y, a[i + 1]);
-                    }
-                }
-                __syncwarp();
-            }
-        }
-        __syncthreads();
-        // ---- trailing update: columns j >= pe apply the panel's reflectors in order
-        if (warp >= (pe >> 4) || (pe & 15)) {
-            const bool act = own && j >= pe;
-            for (int r = 0; r < np; ++r) {
-                const double g = cf[2 * r], u0 = cf[2 * r + 1];
-                if (g == 0.0) continue;
-                double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
-                const double2* y = reinterpret_cast<const double2*>(Yb + r * ROWS + half * TR);
-                if (act) {
-                    if (half == 0) w0 = u0 * Rp[r * n + j];
-#pragma unroll
-                    for (int i = 0; i < TR; i += 4) {
-                        const double2 ya = y[i / 2], yb = y[i / 2 + 1];
-                        w0 = fma(ya.x, a[i], w0);
-                        w1 = fma(ya.y, a[i + 1], w1);
-                        w2 = fma(yb.x, a[i + 2], w2);
-                        w3 = fma(yb.y, a[i + 3], w3);
-                    }
-                }
-                double w = (w0 + w1) + (w2 + w3);
-                w += __shfl_xor_sync(0xffffffffu, w, 1);
-                if (act) {
-                    const double f = g * w;
-                    if (half == 0) Rp[r * n + j] = fma(f, u0, Rp[r * n + j]);
-#pragma unroll
-                    for (int i = 0; i < TR; i += 2) {
-                        const double2 yy = y[i / 2];
-                        a[i] = fma(f, yy.x, a[i]);
-                        a[i + 1] = fma(f, yy.y, a[i + 1]);
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        for (int idx = tid; idx < np * n; idx += blockDim.x) {
-            const int r = idx / n, c = idx - r * n;
-            if (c >= pk + r) R[(size_t)(pk + r) * n + c] = Rp[idx];
-        }
-        __syncthreads();
-    }
-}
-
-// fold dispatcher: BLK selects the panel-blocked sweep (P = 2 only)
-template <int TR, int P, bool BLK>
-__device__ __forceinline__ void fold(double (&a)[TR], int n, int k0, double* R, double* vbuf, double* coefs,
-                                     double* dsm) {
-    if constexpr (!BLK && TR == 16) {   // TR = 16 selects the lagged fold (variant L2T16)
-        fold_tile_lag<TR, P>(a, n, k0, R, vbuf, coefs);
-    } else if constexpr (BLK) {
-        fold_tile_blk<TR>(a, n, k0, R, dsm, dsm + kNB * n, dsm + kNB * n + kNB * 2 * TR);
-    } else {
-        fold_tile<TR, P>(a, n, k0, R, vbuf, coefs);
-    }
-}
-__host__ __device__ constexpr size_t blk_smem_doubles(int n, int TR) { return (size_t)kNB * n + kNB * 2 * TR + 2 * kNB; }
-
-template <int TR, int P, bool BLK>
 __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
-    k_tsqr_leaf(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t N, int M,
+    k_tsqr_leaf(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t ldy, int64_t N, int M,
                 double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag) {
     constexpr int ROWS = TR * P;
     __shared__ __align__(16) double vbuf[2 * ROWS];
     __shared__ double coefs[4];
-    extern __shared__ __align__(16) double dsm[];
-    const int n = M + 1, j = col_of<P, BLK>(n), half = threadIdx.x % P;
+    const int n = M + 1, j = col_of<P>(n), half = threadIdx.x % P;
     double* R = Rws + (size_t)blockIdx.x * n * n;
     if (j >= 0 && j < n)
         for (int k = half; k < n; k += P) R[(size_t)k * n + j] = 0.0;   // column j is private to its threads
@@ -448,27 +225,26 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
         for (int i = 0; i < TR; ++i) {
             const int64_t row = base + half * TR + i;
             float v = 0.0f;
-            if (row < r1 && j >= 0 && j < n) v = (j < M) ? __ldg(H + row * ldh + j) : __ldg(Y + row);
+            if (row < r1 && j >= 0 && j < n) v = (j < M) ? __ldg(H + row * ldh + j) : __ldg(Y + row * ldy);
             bad |= !isfinite(v);
             a[i] = (double)v;
         }
-        fold<TR, P, BLK>(a, n, 0, R, vbuf, coefs, dsm);
+        fold_tile<TR, P>(a, n, 0, R, vbuf, coefs);
     }
     if (bad) atomicOr(flag, 1);
 }
 
-template <int TR, int P, bool BLK>
+template <int TR, int P>
 __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
     k_tsqr_merge(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n) {
     constexpr int ROWS = TR * P;
     __shared__ __align__(16) double vbuf[2 * ROWS];
     __shared__ double coefs[4];
-    extern __shared__ __align__(16) double dsm[];
     const int64_t c = (int64_t)blockIdx.x * 2 * stride, partner = c + stride;
     if (partner >= slabs) return;
     double* Ra = Rws + (size_t)c * n * n;
     const double* Rb = Rws + (size_t)partner * n * n;
-    const int j = col_of<P, BLK>(n), half = threadIdx.x % P;
+    const int j = col_of<P>(n), half = threadIdx.x % P;
     for (int s = 0; s * ROWS < n; ++s) {
         double a[TR];
 #pragma unroll
@@ -476,7 +252,7 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
             const int row = s * ROWS + half * TR + i;
             a[i] = (row < n && j >= 0 && j < n && j >= row) ? Rb[(size_t)row * n + j] : 0.0;
         }
-        fold<TR, P, BLK>(a, n, s * ROWS, Ra, vbuf, coefs, dsm);
+        fold_tile<TR, P>(a, n, s * ROWS, Ra, vbuf, coefs);
     }
 }
 
@@ -534,7 +310,7 @@ __device__ double block_max(double v, double* red) { return -block_min(-v, red);
 
 // Final solve on slab 0 (one CTA of P*n threads).  R0 is copied to Rorig
 // before a ridge refactorisation so rho is measured on the unregularised R.
-template <int TR, int P, bool BLK>
+template <int TR, int P>
 __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
     k_tsqr_solve(double* __restrict__ R, double* __restrict__ Rorig, int M, long long n_total,
                  const int* __restrict__ flag, double* __restrict__ beta, SolveDev* __restrict__ out) {
@@ -543,8 +319,8 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
     __shared__ double coefs[4];
     __shared__ double red[32];
     __shared__ double bk;
-    extern __shared__ __align__(16) double zs[];   // [n] signs / rhs / beta, then the blocked-fold buffers
-    const int n = M + 1, j = col_of<P, BLK>(n), half = threadIdx.x % P;
+    extern __shared__ __align__(16) double zs[];   // [n] signs / rhs / beta
+    const int n = M + 1, j = col_of<P>(n), half = threadIdx.x % P;
     const bool own = j >= 0 && j < n && half == 0;
     // sign normalisation: flip row k when R_kk < 0 (signs read into smem first)
     if (own) zs[j] = R[(size_t)j * n + j] < 0.0 ? -1.0 : 1.0;
@@ -574,7 +350,7 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
                 const int row = s * ROWS + half * TR + i;
                 a[i] = (row < M && j == row) ? sl : 0.0;
             }
-            fold<TR, P, BLK>(a, n, s * ROWS, R, vbuf, coefs, zs + ((n + 1) & ~1));
+            fold_tile<TR, P>(a, n, s * ROWS, R, vbuf, coefs);
         }
         if (own) zs[j] = R[(size_t)j * n + j] < 0.0 ? -1.0 : 1.0;
         __syncthreads();
@@ -697,224 +473,6 @@ __global__ void __launch_bounds__(1024, 1)
     if (threadIdx.x == 0) {
         out->nonfinite = *flag;
         out->n_total = n_total;
-    }
-}
-
-// ---- 2D register-tiled fold (fold2d) ------------------------------------------------------
-// Thread t = (column group cg = t / 4, row group rg = t % 4) holds TR rows
-// (rg*TR ..) of the TC tile columns TC*cg .. TC*cg+TC-1: a tile of 4*TR rows.
-// Compared with fold_tile (one column per thread) every reflector element
-// read from shared memory feeds TC columns; column dot products combine over
-// the 4 row-group lanes by butterfly shuffles.  Lane rg < TC of a group keeps
-// the prefetched R rows of column TC*cg + rg and owns its R entries.
-// TC = 3 at n = 257 gives 86 groups = 344 threads (11 warps, <= 168
-// registers per thread: 17 warps would cap it at 96).
-constexpr int kRG = 4;
-
-// Reflector of local column LC (compile-time) of this 4-lane group: x0 =
-// R[k][k] comes from the prefetch register of lane rg = LC.
-template <int TR, int TC, int LC>
-__device__ __forceinline__ void make_refl3(const double (&a)[TC][TR], double x0_own, double* v, double* coef,
-                                           double* Rkk, int rg) {
-    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-#pragma unroll
-    for (int i = 0; i < TR; i += 4) {
-        p0 = fma(a[LC][i], a[LC][i], p0);
-        p1 = fma(a[LC][i + 1], a[LC][i + 1], p1);
-        p2 = fma(a[LC][i + 2], a[LC][i + 2], p2);
-        p3 = fma(a[LC][i + 3], a[LC][i + 3], p3);
-    }
-    const unsigned gm = 0xFu << (threadIdx.x & 28);   // the 4 lanes of this group
-    double s2 = (p0 + p1) + (p2 + p3);
-    s2 += __shfl_xor_sync(gm, s2, 1);
-    s2 += __shfl_xor_sync(gm, s2, 2);
-    const double x0 = __shfl_sync(gm, x0_own, ((int)threadIdx.x & 28) | LC);
-    double g = 0.0, u0 = 0.0;
-    if (s2 != 0.0) {
-        const double beta = -(x0 >= 0.0 ? 1.0 : -1.0) * sqrt_fast(fma(x0, x0, s2));
-        const double uu = x0 - beta;
-        if (fabs(beta * uu) > 1e-280) {   // see make_reflector
-            u0 = uu;
-            g = rcp_fast(beta * uu);
-            double2* vv = reinterpret_cast<double2*>(v + rg * TR);
-#pragma unroll
-            for (int i = 0; i < TR; i += 2) vv[i / 2] = make_double2(a[LC][i], a[LC][i + 1]);
-            if (rg == LC) *Rkk = beta;   // the lane that owns column k's R entries
-        }
-    }
-    if (rg == 0) {
-        coef[0] = g;
-        coef[1] = u0;
-    }
-}
-
-// Apply reflector (g, u0, v) to local column C of every group in the warp:
-// partial dot over this lane's TR rows (+ u0 R[k][col] on the R-owning lane),
-// butterfly over the 4 row-group lanes, x += f v.  Columns <= k or >= n get
-// f = 0 (no-op).  Returns f for the R update.
-template <int TR, int TC, int C>
-__device__ __forceinline__ double apply_col(double (&a)[TC][TR], const double2 (&v)[TR / 2], double g, double u0,
-                                            double rq0, int rg, bool live) {
-    double w0 = (rg == C) ? u0 * rq0 : 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
-#pragma unroll
-    for (int i = 0; i < TR; i += 4) {
-        w0 = fma(v[i / 2].x, a[C][i], w0);
-        w1 = fma(v[i / 2].y, a[C][i + 1], w1);
-        w2 = fma(v[i / 2 + 1].x, a[C][i + 2], w2);
-        w3 = fma(v[i / 2 + 1].y, a[C][i + 3], w3);
-    }
-    double w = (w0 + w1) + (w2 + w3);
-    w += __shfl_xor_sync(0xffffffffu, w, 1);
-    w += __shfl_xor_sync(0xffffffffu, w, 2);
-    const double f = live ? g * w : 0.0;
-#pragma unroll
-    for (int i = 0; i < TR; i += 2) {
-        a[C][i] = fma(f, v[i / 2].x, a[C][i]);
-        a[C][i + 1] = fma(f, v[i / 2].y, a[C][i + 1]);
-    }
-    return f;
-}
-
-template <int TR, int TC, int C>
-__device__ __forceinline__ void apply_rest(double (&a)[TC][TR], const double2 (&v)[TR / 2], double g, double u0,
-                                           double rq0, int rg, int cb, int k, int n, double& fR) {
-    if constexpr (C < TC) {
-        const double f = apply_col<TR, TC, C>(a, v, g, u0, rq0, rg, cb + C > k && cb + C < n);
-        if (rg == C) fR = f;
-    }
-}
-
-// One column step k of the lean fold: LC = (k+1) % TC is the local index of
-// column k+1, so every register index is compile-time.  The warp holding
-// column k+1 first updates local column LC of all its groups, then the owner
-// group builds reflector k+1 and publishes it, then the warp updates its other
-// columns; one block barrier per column.
-template <int TR, int TC, int LC>
-__device__ __forceinline__ void fold_step(double (&a)[TC][TR], int n, int k, double* __restrict__ R, double* vbuf,
-                                          double* coefs, double& rq0, double& rq1, int rg, int grp, int cb, int cR) {
-    constexpr int ROWS = kRG * TR;
-    const double g = coefs[2 * (k & 1)], u0 = coefs[2 * (k & 1) + 1];
-    // warp-uniform skip: the warp's last column is <= k, or reflector k is the identity
-    const bool warp_live = g != 0.0 && (int)((threadIdx.x | 31) >> 2) * TC + TC - 1 > k;
-    if (warp_live) {
-        double2 v[TR / 2];
-        const double2* vs = reinterpret_cast<const double2*>(vbuf + (k & 1) * ROWS + rg * TR);
-#pragma unroll
-        for (int i = 0; i < TR / 2; ++i) v[i] = vs[i];
-        double fR = 0.0;
-        const bool crit = k + 1 < n && grp == (k + 1) / TC;
-        if (crit && rg == 0) qr_ev(1, k);
-        {
-            const double f = apply_col<TR, TC, LC>(a, v, g, u0, rq0, rg, cb + LC > k && cb + LC < n);
-            if (rg == LC) fR = f;
-        }
-        if (crit && rg == 0) qr_ev(2, k);
-        if (crit)
-            make_refl3<TR, TC, LC>(a, rq1, vbuf + ((k + 1) & 1) * ROWS, coefs + 2 * ((k + 1) & 1),
-                                   R + (size_t)(k + 1) * n + (k + 1), rg);
-        if (crit && rg == 0) qr_ev(4, k);
-        apply_rest<TR, TC, (LC + 1) % TC == LC ? TC : (LC + 1) % TC>(a, v, g, u0, rq0, rg, cb, k, n, fR);
-        apply_rest<TR, TC, (LC + 2) % TC == LC || TC < 3 ? TC : (LC + 2) % TC>(a, v, g, u0, rq0, rg, cb, k, n, fR);
-        apply_rest<TR, TC, (LC + 3) % TC == LC || TC < 4 ? TC : (LC + 3) % TC>(a, v, g, u0, rq0, rg, cb, k, n, fR);
-        if (rg < TC && cR > k && cR < n) R[(size_t)k * n + cR] = fma(fR, u0, rq0);
-        if (crit && rg == 0) qr_ev(5, k);
-    } else if (k + 1 < n && grp == (k + 1) / TC) {
-        make_refl3<TR, TC, LC>(a, rq1, vbuf + ((k + 1) & 1) * ROWS, coefs + 2 * ((k + 1) & 1),
-                               R + (size_t)(k + 1) * n + (k + 1), rg);
-    }
-}
-
-template <int TR, int TC>
-__device__ void fold2d(double (&a)[TC][TR], int n, int k0, double* __restrict__ R, double* vbuf, double* coefs) {
-    constexpr int ROWS = kRG * TR;
-    const int tid = threadIdx.x, rg = tid & 3, grp = tid >> 2, cb = TC * grp;
-    const int cR = cb + rg;   // column whose R rows this lane prefetches and owns (rg < TC)
-    const bool hasR = rg < TC && cR < n;
-    const double* Rc = R + cR;
-    auto ld = [&](int row) -> double { return (hasR && row < n && cR >= row) ? Rc[(size_t)row * n] : 0.0; };
-    double rq0 = ld(k0), rq1 = ld(k0 + 1), rq2 = ld(k0 + 2);
-    if (grp == k0 / TC) {
-        switch (k0 % TC) {
-        case 0: make_refl3<TR, TC, 0>(a, rq0, vbuf + (k0 & 1) * ROWS, coefs + 2 * (k0 & 1), R + (size_t)k0 * n + k0, rg); break;
-        case 1: if constexpr (TC > 1) make_refl3<TR, TC, 1 % TC>(a, rq0, vbuf + (k0 & 1) * ROWS, coefs + 2 * (k0 & 1), R + (size_t)k0 * n + k0, rg); break;
-        case 2: if constexpr (TC > 2) make_refl3<TR, TC, 2 % TC>(a, rq0, vbuf + (k0 & 1) * ROWS, coefs + 2 * (k0 & 1), R + (size_t)k0 * n + k0, rg); break;
-        default: if constexpr (TC > 3) make_refl3<TR, TC, 3 % TC>(a, rq0, vbuf + (k0 & 1) * ROWS, coefs + 2 * (k0 & 1), R + (size_t)k0 * n + k0, rg); break;
-        }
-    }
-    __syncthreads();
-    for (int k = k0; k < n; ++k) {
-        if (tid == 0) qr_ev(0, k);
-        switch ((k + 1) % TC) {
-        case 0: fold_step<TR, TC, 0>(a, n, k, R, vbuf, coefs, rq0, rq1, rg, grp, cb, cR); break;
-        case 1: if constexpr (TC > 1) fold_step<TR, TC, 1 % TC>(a, n, k, R, vbuf, coefs, rq0, rq1, rg, grp, cb, cR); break;
-        case 2: if constexpr (TC > 2) fold_step<TR, TC, 2 % TC>(a, n, k, R, vbuf, coefs, rq0, rq1, rg, grp, cb, cR); break;
-        default: if constexpr (TC > 3) fold_step<TR, TC, 3 % TC>(a, n, k, R, vbuf, coefs, rq0, rq1, rg, grp, cb, cR); break;
-        }
-        if (tid == 0) qr_ev(6, k);
-        rq0 = rq1;
-        rq1 = rq2;
-        rq2 = ld(k + 3);
-        if (tid == 0) qr_ev(7, k);
-        __syncthreads();
-        if (tid == 0) qr_ev(3, k);
-    }
-}
-
-template <int TR, int TC>
-__global__ void __launch_bounds__(352, 1)
-    k_tsqr_leaf2(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t N, int M,
-                 double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag) {
-    constexpr int ROWS = kRG * TR;
-    __shared__ __align__(16) double vbuf[2 * ROWS];
-    __shared__ double coefs[4];
-    const int n = M + 1, tid = threadIdx.x, rg = tid & 3, cb = TC * (tid >> 2);
-    double* R = Rws + (size_t)blockIdx.x * n * n;
-    for (int idx = tid; idx < n * n; idx += blockDim.x) R[idx] = 0.0;
-    __syncthreads();
-    const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
-    const int64_t r1 = min(N, r0 + rows_per_cta);
-    bool bad = false;
-    for (int64_t base = r0; base < r1; base += ROWS) {
-        double a[TC][TR];
-#pragma unroll
-        for (int i = 0; i < TR; ++i) {
-            const int64_t row = base + rg * TR + i;
-#pragma unroll
-            for (int c = 0; c < TC; ++c) {
-                const int col = cb + c;
-                float x = 0.0f;
-                if (row < r1 && col < n) x = col < M ? __ldg(H + row * ldh + col) : __ldg(Y + row);
-                bad |= !isfinite(x);
-                a[c][i] = (double)x;
-            }
-        }
-        fold2d<TR, TC>(a, n, 0, R, vbuf, coefs);
-    }
-    if (bad) atomicOr(flag, 1);
-}
-
-template <int TR, int TC>
-__global__ void __launch_bounds__(352, 1) k_tsqr_merge2(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n) {
-    constexpr int ROWS = kRG * TR;
-    __shared__ __align__(16) double vbuf[2 * ROWS];
-    __shared__ double coefs[4];
-    const int64_t c = (int64_t)blockIdx.x * 2 * stride, partner = c + stride;
-    if (partner >= slabs) return;
-    double* Ra = Rws + (size_t)c * n * n;
-    const double* Rb = Rws + (size_t)partner * n * n;
-    const int tid = threadIdx.x, rg = tid & 3, cb = TC * (tid >> 2);
-    for (int s = 0; s * ROWS < n; ++s) {
-        double a[TC][TR];
-#pragma unroll
-        for (int i = 0; i < TR; ++i) {
-            const int row = s * ROWS + rg * TR + i;
-#pragma unroll
-            for (int cc = 0; cc < TC; ++cc) {
-                const int col = cb + cc;
-                a[cc][i] = (row < n && col < n && col >= row) ? Rb[(size_t)row * n + col] : 0.0;
-            }
-        }
-        fold2d<TR, TC>(a, n, s * ROWS, Ra, vbuf, coefs);
     }
 }
 
@@ -1326,12 +884,26 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
     publish(npan);
 }
 
-// Panel warp of this CTA: co-resident CTAs (typically blocks b, b+148, ...)
-// take distinct warp indices, so their latency-bound panels run on different
-// SM sub-partitions (warp slot % 4).  sm_slot: per-SM arrival counters,
-// zeroed before the launch (null: use the block index).
-__device__ __forceinline__ int wy_panel_warp(int* sm_slot) {
+// Panel warp of this CTA.  mode 1 (default): the warp of this CTA that sits on
+// SM sub-partition 0 (%warpid & 3 == 0), so the latency-bound panels of all
+// co-resident CTAs share SMSP 0 and no trailing update's DMMA stream (16 FP64-pipe
+// cycles per m8n8k4) delays their dependent DFMA/MUFU chain; the trailing warps
+// own SMSPs 1-3.  mode 0: co-resident CTAs take distinct warp indices (per-SM
+// arrival counters, sm_slot zeroed before the launch), one panel per SMSP.
+__device__ __forceinline__ int wy_panel_warp(int* sm_slot, int mode) {
     __shared__ int pw_s;
+    const int nw = (int)(blockDim.x >> 5);
+    if (threadIdx.x == 0) pw_s = nw;
+    __syncthreads();
+    if (mode == 1) {
+        unsigned wid;
+        asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+        if ((threadIdx.x & 31) == 0 && (wid & 3) == 0) atomicMin(&pw_s, (int)(threadIdx.x >> 5));
+        __syncthreads();
+        const int pw = pw_s;
+        __syncthreads();
+        if (pw < nw) return pw;
+    }
     if (threadIdx.x == 0) {
         int local = (int)blockIdx.x;
         if (sm_slot) {
@@ -1339,7 +911,7 @@ __device__ __forceinline__ int wy_panel_warp(int* sm_slot) {
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
             local = atomicAdd(sm_slot + (smid & 1023), 1);
         }
-        pw_s = local % (int)(blockDim.x >> 5);
+        pw_s = local % nw;
     }
     __syncthreads();
     return pw_s;
@@ -1349,7 +921,7 @@ template <int ROWS>
 __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
     k_tsqr_leaf_wy(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t ldy, int P,
                    int64_t N, int M, double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag,
-                   int* sm_slot, int la_wait) {
+                   int* sm_slot, int la_wait, int pw_mode) {
     extern __shared__ __align__(16) double wsm[];
     // columns [0, M) of the tile are H, [M, M + P) the P outputs Y[row][0..P-1] (row stride ldy)
     const int n = M + P, LDC = wy_ldc(n), tid = threadIdx.x, nt = blockDim.x;
@@ -1363,7 +935,7 @@ __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
     const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
     const int64_t r1 = min(N, r0 + rows_per_cta);
     bool bad = false;
-    const int pw = wy_panel_warp(sm_slot);
+    const int pw = wy_panel_warp(sm_slot, pw_mode);
     // 16-B vector loads of H when rows allow it, issued in batches of 8 per
     // thread so the tile load is not a chain of dependent HBM round trips
     const bool vec = (M % 4 == 0) && (ldh % 4 == 0) && ((reinterpret_cast<uintptr_t>(H) & 15) == 0);
@@ -1476,60 +1048,30 @@ __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
 
 // ---- host side ---------------------------------------------------------------------
 
-// Variants: n <= 288: 2 threads x 24 rows per column (48-row tiles, <= 576
-// threads); n <= 512: 2 x 12 (24-row tiles, <= 1024 threads); else 1 x 12.
-enum class Var { B2T24, P2T24, P2T12, P1T12, L2T16 };
-static Var pick_var(int n) {
-    // ELMRNN_TSQR_VAR=0/1/2 forces a variant (testing aid; must fit the thread limit)
-    if (const char* e = std::getenv("ELMRNN_TSQR_VAR")) {
-        const int v = std::atoi(e);
-        if (v == 0 && n <= 288) return Var::B2T24;
-        if (v == 1 && n <= 512) return Var::P2T12;
-        if (v == 2) return Var::P1T12;
-        if (v == 3 && n <= 288) return Var::P2T24;
-        if (v == 4 && n <= 288) return Var::L2T16;
-    }
-    return n <= 288 ? Var::P2T24 : (n <= 512 ? Var::P2T12 : Var::P1T12);
-}
-static int var_rows(Var v) {
-    return (v == Var::B2T24 || v == Var::P2T24) ? 48 : (v == Var::L2T16 ? 32 : (v == Var::P2T12 ? 24 : 12));
-}
+// Per-column fold variants (n <= 128 by default; any n when forced): n <= 288:
+// 2 threads x 24 rows per column (48-row tiles, <= 576 threads); n <= 512:
+// 2 x 12 (24-row tiles, <= 1024 threads); else 1 x 12.
+enum class Var { P2T24, P2T12, P1T12 };
+static Var pick_var(int n) { return n <= 288 ? Var::P2T24 : (n <= 512 ? Var::P2T12 : Var::P1T12); }
+static int var_rows(Var v) { return v == Var::P2T24 ? 48 : (v == Var::P2T12 ? 24 : 12); }
 static int var_p(Var v) { return v == Var::P1T12 ? 1 : 2; }
-static bool var_blk(Var v) { return v == Var::B2T24; }
-static size_t var_smem(Var v, int n) { return var_blk(v) ? blk_smem_doubles(n, 24) * sizeof(double) : 0; }
 static int var_threads(Var v, int n) { return (var_p(v) * n + 31) / 32 * 32; }
 
 template <class F>
 static auto dispatch(Var v, F&& f) {
     switch (v) {
-    case Var::B2T24:
-        return f(std::integral_constant<int, 24>{}, std::integral_constant<int, 2>{}, std::true_type{});
-    case Var::P2T24:
-        return f(std::integral_constant<int, 24>{}, std::integral_constant<int, 2>{}, std::false_type{});
-    case Var::P2T12:
-        return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 2>{}, std::false_type{});
-    case Var::L2T16:
-        return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 2>{}, std::false_type{});
-    default: return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 1>{}, std::false_type{});
+    case Var::P2T24: return f(std::integral_constant<int, 24>{}, std::integral_constant<int, 2>{});
+    case Var::P2T12: return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 2>{});
+    default: return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 1>{});
     }
 }
-
-// 2D register-tiled leaf + merge (fold2d): n <= 264 (4 ceil(n/3) <= 352 threads).
-// ELMRNN_TSQR_2D=0/1 overrides the default (testing aid).
-constexpr int kTR2 = 16, kTC2 = 3;
-static bool use_2d(int n) {
-    if (n > 264) return false;
-    if (const char* e = std::getenv("ELMRNN_TSQR_2D")) return std::atoi(e) != 0;
-    return false;
-}
-static int threads_2d(int n) { return (4 * ((n + kTC2 - 1) / kTC2) + 31) / 32 * 32; }
 
 // n = M+1 above this takes the WY leaf/merge and the wide solve (columns > threads).
 constexpr int kWideN = 1024;
 // Blocked compact-WY leaf + merge (wy_fold).  ELMRNN_TSQR_WY=0/1 overrides the default.
-static bool use_wy(int n) {
+static bool use_wy(const elmrnn* h, int n) {
     if (n > kWideN) return true;   // the only leaf/merge for more columns than CTA threads
-    if (const char* e = std::getenv("ELMRNN_TSQR_WY")) return std::atoi(e) != 0;
+    if (h->tune.tsqr_wy >= 0) return h->tune.tsqr_wy != 0;   // testing knob (elmrnn_init_ex)
     // measured (tools/qr_time.py, B200): M = 128 x 1M rows WY 8.6 vs per-column fold
     // 10.4 ms; M = 64 x 100k rows 1.22 vs 0.93 ms
     return n > 128;
@@ -1537,42 +1079,24 @@ static bool use_wy(int n) {
 // Look-ahead isolation in the leaf: trailing warps without a look-ahead tile
 // wait for the look-ahead columns with the panel warp instead of competing with
 // that chain (measured C4 shape 81.6 -> 80.3 ms; neutral at 8 warps, n > 320).
-// ELMRNN_WY_LA_WAIT=0/1 overrides (testing aid).
-static int wy_la_wait(int n) {
-    const char* e = std::getenv("ELMRNN_WY_LA_WAIT");
-    return e ? std::atoi(e) : (n <= 320 ? 1 : 0);
-}
+static int wy_la_wait(int n) { return n <= 320 ? 1 : 0; }
 // multi-output [H | Y_1..Y_P] (P > 1) always takes the WY leaf/merge and the wide solve
-static bool use_wy_h(const elmrnn* h) { return h->nrhs > 1 || use_wy(h->M + h->nrhs); }
+static bool use_wy_h(const elmrnn* h) { return h->nrhs > 1 || use_wy(h, h->M + h->nrhs); }
 static bool wide_solve(const elmrnn* h) { return h->nrhs > 1 || h->M + h->nrhs > kWideN; }
-static int wy_rows(int n) {
-    if (const char* e = std::getenv("ELMRNN_TSQR_WY_ROWS")) {   // testing aid
-        const int r = std::atoi(e);
+static int wy_rows(const elmrnn* h, int n) {
+    if (const int r = h->tune.wy_rows) {   // testing knob (elmrnn_init_ex)
         if ((r == 96 || r == 64 || r == 32 || r == 24 || r == 16 || r == 8) && wy_smem_bytes(r, n) <= 220 * 1024)
             return r;
     }
     // 32-row tiles, 2-3 CTAs per SM (their panels overlap each other's trailing updates)
     return wy_smem_bytes(32, n) <= 220 * 1024 ? 32 : 16;
 }
-// Leaf dynamic shared memory: the tile + coefficients, optionally padded so
-// that at most ELMRNN_TSQR_WY_CTAS CTAs share an SM (testing aid: fewer
-// co-resident CTAs means less contention on each latency-bound panel warp).
-static size_t wy_leaf_smem(int rows, int n) {
-    size_t sm = wy_smem_bytes(rows, n);
-    if (const char* e = std::getenv("ELMRNN_TSQR_WY_CTAS")) {
-        const int c = std::atoi(e);
-        if (c >= 1) sm = std::max(sm, (size_t)(227 * 1024 / c - 1024 * c));
-    }
-    return std::min(sm, (size_t)227 * 1024);
-}
-static int wy_threads(int n) {
-    int w = n <= 320 ? 4 : std::min(8, ((n + 1) / 2 + 31) / 32);
-    if (const char* e = std::getenv("ELMRNN_TSQR_WY_WARPS")) w = std::max(1, std::min(8, std::atoi(e)));   // testing aid
-    return 32 * w;
-}
+// Leaf dynamic shared memory: the tile + coefficients.
+static size_t wy_leaf_smem(int rows, int n) { return std::min(wy_smem_bytes(rows, n), (size_t)227 * 1024); }
+static int wy_threads(int n) { return 32 * (n <= 320 ? 4 : std::min(8, ((n + 1) / 2 + 31) / 32)); }
 template <class F>
-static auto wy_dispatch(int n, F&& f) {
-    switch (wy_rows(n)) {
+static auto wy_dispatch(const elmrnn* h, int n, F&& f) {
+    switch (wy_rows(h, n)) {
     case 96: return f(std::integral_constant<int, 96>{});
     case 64: return f(std::integral_constant<int, 64>{});
     case 32: return f(std::integral_constant<int, 32>{});
@@ -1594,24 +1118,20 @@ int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
     const int n = h->M + h->nrhs;
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
-    int per_sm = use_wy_h(h) ? wy_dispatch(n, [&](auto rows) {
+    int per_sm = use_wy_h(h) ? wy_dispatch(h, n, [&](auto rows) {
         constexpr int RW = decltype(rows)::value;
         const size_t sm = wy_leaf_smem(RW, n);
         cudaFuncSetAttribute(k_tsqr_leaf_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         int ps = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_tsqr_leaf_wy<RW>, wy_threads(n), sm);
         return ps < 1 ? 1 : ps;
-    }) : use_2d(n) ? 1 : dispatch(v, [&](auto tr, auto p, auto b) {
+    }) : dispatch(v, [&](auto tr, auto p) {
         int ps = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &ps, k_tsqr_leaf<decltype(tr)::value, decltype(p)::value, decltype(b)::value>, threads, var_smem(v, n));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_tsqr_leaf<decltype(tr)::value, decltype(p)::value>,
+                                                      threads, 0);
         return ps < 1 ? 1 : ps;
     });
     int64_t maxc = (int64_t)per_sm * h->sm_count;
-    if (const char* e = std::getenv("ELMRNN_TSQR_MAXSLABS")) {   // testing aid
-        const int64_t v = std::atoll(e);
-        if (v >= 1 && v < maxc) maxc = v;
-    }
     // at least n rows per leaf: a leaf R with fewer rows is rank deficient
     // and its noise rows only cost merges (and risk underflow cascades)
     int64_t byrows = N / n;
@@ -1650,15 +1170,13 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
     const int n = h->M + h->nrhs;
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
-    const char* lv = std::getenv("ELMRNN_TSQR_LEVELS");   // testing aid: stop the tree early
-    const int64_t max_stride = lv ? ((int64_t)1 << std::atoi(lv)) : slabs;
+    const int64_t max_stride = slabs;
     if (use_wy_h(h)) {
         // merges are latency-bound (few pairs at the top of the tree): the
         // tallest tile that fits means the fewest panel steps per fold, and the
         // SMs a level leaves idle pipeline each pair's row chunks
-        // (k_tsqr_merge_wy_par; ELMRNN_TSQR_PAR=0 disables, testing aid)
-        const char* pe = std::getenv("ELMRNN_TSQR_PAR");
-        const bool par_ok = !(pe && std::atoi(pe) == 0);
+        // (k_tsqr_merge_wy_par)
+        const bool par_ok = true;
         return wy_dispatch_merge(n, [&](auto rows) {
             constexpr int RW = decltype(rows)::value;
             const size_t sm = wy_smem_bytes(RW, n);
@@ -1690,88 +1208,46 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
             return cudaGetLastError();
         });
     }
-    if (use_2d(n)) {
+    return dispatch(v, [&](auto tr, auto p) {
         for (int64_t stride = 1; stride < slabs && stride < max_stride; stride *= 2) {
             int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
-            k_tsqr_merge2<kTR2, kTC2><<<(unsigned)pairs, threads_2d(n), 0, h->stream>>>(h->Rws, slabs, stride, n);
-            h->launches++;
-        }
-        return cudaGetLastError();
-    }
-    return dispatch(v, [&](auto tr, auto p, auto b) {
-        for (int64_t stride = 1; stride < slabs && stride < max_stride; stride *= 2) {
-            int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
-            k_tsqr_merge<decltype(tr)::value, decltype(p)::value, decltype(b)::value>
-                <<<(unsigned)pairs, threads, var_smem(v, n), h->stream>>>(h->Rws, slabs, stride, n);
+            k_tsqr_merge<decltype(tr)::value, decltype(p)::value>
+                <<<(unsigned)pairs, threads, 0, h->stream>>>(h->Rws, slabs, stride, n);
             h->launches++;
         }
         return cudaGetLastError();
     });
 }
 
-static unsigned long long* qr_trace_setup() {
-    if (!std::getenv("ELMRNN_TRACE_QR")) return nullptr;
-    unsigned long long* buf = nullptr;
-    cudaMalloc(&buf, sizeof(unsigned long long) * 8 * 4096);
-    cudaMemset(buf, 0, sizeof(unsigned long long) * 8 * 4096);
-    cudaMemcpyToSymbol(g_qr_trace, &buf, sizeof(buf));
-    return buf;
-}
-static void qr_trace_dump(unsigned long long* buf) {
-    if (!buf) return;
-    std::vector<unsigned long long> hb(8 * 4096);
-    cudaDeviceSynchronize();
-    cudaMemcpy(hb.data(), buf, sizeof(unsigned long long) * hb.size(), cudaMemcpyDeviceToHost);
-    unsigned long long* null = nullptr;
-    cudaMemcpyToSymbol(g_qr_trace, &null, sizeof(null));
-    cudaFree(buf);
-    if (FILE* f = std::fopen(std::getenv("ELMRNN_TRACE_QR"), "w")) {
-        for (int k = 0; k < 4096; ++k)
-            if (hb[8 * k]) {
-                std::fprintf(f, "%d", k);
-                for (int s2 = 0; s2 < 8; ++s2) std::fprintf(f, ",%llu", hb[8 * k + s2]);
-                std::fprintf(f, "\n");
-            }
-        std::fclose(f);
-    }
-}
-
 cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t ldy, int64_t N) {
-    struct TraceGuard { unsigned long long* b = qr_trace_setup(); ~TraceGuard() { qr_trace_dump(b); } } tg;
     const int n = h->M + h->nrhs;
     const Var v = pick_var(n);
     const int64_t slabs = tsqr_leaf_slabs(h, N);
     cudaError_t e;
     if ((e = ensure_solve_ws(h, wide_solve(h) && slabs < 2 ? 2 : slabs))) return e;   // wide solve: slab 1 = ridge rows
     if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream))) return e;
-    const int rows_tile = use_wy_h(h) ? wy_rows(n) : use_2d(n) ? kRG * kTR2 : var_rows(v);
+    const int rows_tile = use_wy_h(h) ? wy_rows(h, n) : var_rows(v);
     int64_t rows = (N + slabs - 1) / slabs;
     rows = (rows + rows_tile - 1) / rows_tile * rows_tile;
     const int threads = var_threads(v, n);
     if (use_wy_h(h)) {
-        e = wy_dispatch(n, [&](auto rws) {
+        e = wy_dispatch(h, n, [&](auto rws) {
             constexpr int RW = decltype(rws)::value;
             const size_t sm = wy_leaf_smem(RW, n);
             cudaFuncSetAttribute(k_tsqr_leaf_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             int* slot = reinterpret_cast<int*>(h->sdev + 1);   // per-SM arrival counters (ensure_solve_ws)
             cudaMemsetAsync(slot, 0, 1024 * sizeof(int), h->stream);
             k_tsqr_leaf_wy<RW><<<(unsigned)slabs, wy_threads(n), sm, h->stream>>>(
-                H, ldh, Y, ldy, h->nrhs, N, h->M, h->Rws, rows, h->flag, slot, wy_la_wait(n));
+                H, ldh, Y, ldy, h->nrhs, N, h->M, h->Rws, rows, h->flag, slot, wy_la_wait(n), h->tune.pw_mode);
             h->launches++;
             return cudaGetLastError();
         });
         if (e) return e;
         return tree(h, slabs);
     }
-    if (use_2d(n)) {
-        k_tsqr_leaf2<kTR2, kTC2><<<(unsigned)slabs, threads_2d(n), 0, h->stream>>>(H, ldh, Y, N, h->M, h->Rws, rows, h->flag);
-        h->launches++;
-        if ((e = cudaGetLastError())) return e;
-        return tree(h, slabs);
-    }
-    e = dispatch(v, [&](auto tr, auto p, auto b) {
-        k_tsqr_leaf<decltype(tr)::value, decltype(p)::value, decltype(b)::value>
-            <<<(unsigned)slabs, threads, var_smem(v, n), h->stream>>>(H, ldh, Y, N, h->M, h->Rws, rows, h->flag);
+    e = dispatch(v, [&](auto tr, auto p) {
+        k_tsqr_leaf<decltype(tr)::value, decltype(p)::value>
+            <<<(unsigned)slabs, threads, 0, h->stream>>>(H, ldh, Y, ldy, N, h->M, h->Rws, rows, h->flag);
         h->launches++;
         return cudaGetLastError();
     });
@@ -1826,9 +1302,9 @@ cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta) {
         h->launches++;
         return cudaGetLastError();
     }
-    const size_t smem = ((n + 1) & ~1) * sizeof(double) + var_smem(v, n);
-    return dispatch(v, [&](auto tr, auto p, auto b) {
-        k_tsqr_solve<decltype(tr)::value, decltype(p)::value, decltype(b)::value><<<1, threads, smem, h->stream>>>(
+    const size_t smem = ((n + 1) & ~1) * sizeof(double);
+    return dispatch(v, [&](auto tr, auto p) {
+        k_tsqr_solve<decltype(tr)::value, decltype(p)::value><<<1, threads, smem, h->stream>>>(
             h->Rws, Rorig, h->M, (long long)n_total, h->flag, beta, h->sdev);
         h->launches++;
         return cudaGetLastError();

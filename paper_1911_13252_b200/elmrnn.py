@@ -118,6 +118,20 @@ def _dev_check(t: torch.Tensor, name: str, dtype: torch.dtype):
         raise ValueError(f"{name} must be {dtype}")
 
 
+def _vec(t: torch.Tensor, name: str, dtype: torch.dtype, n: int):
+    """A contiguous CUDA vector of at least n elements (the library reads/writes n)."""
+    _dev_check(t, name, dtype)
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.numel() < n:
+        raise ValueError(f"{name} has {t.numel()} elements, needs >= {n}")
+
+
+def _need_rows(rows: int, N: int, name: str):
+    if rows < N:
+        raise ValueError(f"{name} has {rows} rows, needs >= {N}")
+
+
 def _rows(t: torch.Tensor, name: str):
     """(leading dimension, rows) of a 2-D view with unit inner stride."""
     t2 = t.reshape(t.shape[0], -1) if t.dim() != 2 else t
@@ -193,17 +207,22 @@ class ELMRNN:
         ldy = 0
         if Yfb is not None:
             _dev_check(Yfb, "Yfb", torch.float32)
-            ldy, _ = _rows(Yfb, "Yfb")
+            ldy, ry = _rows(Yfb, "Yfb")
+            _need_rows(ry, N, "Yfb")
         if H is None:
             H = torch.empty((N, self.M), dtype=torch.float32, device=X.device)
         _dev_check(H, "H", torch.float32)
-        ldh, _ = _rows(H, "H") if N else (self.M, 0)
+        ldh, rh = _rows(H, "H") if N else (self.M, 0)
+        _need_rows(rh, N, "H")
+        if N and H.shape[-1] < self.M:
+            raise ValueError(f"H needs >= {self.M} columns")
         self._stream()
         if Ef is None:
             self._check(lib().elmrnn_build_H(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, N, _ptr(H), ldh))
         else:
             _dev_check(Ef, "Ef", torch.float32)
-            lde = _rows(Ef, "Ef")[0] if N else self.Q
+            lde, re_ = _rows(Ef, "Ef") if N else (self.Q, 0)
+            _need_rows(re_, N, "Ef")
             self._check(lib().elmrnn_build_H_ef(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, _ptr(Ef), lde, N,
                                                 _ptr(H), ldh))
         return H
@@ -212,14 +231,15 @@ class ELMRNN:
         """elmrnn_error_windows: NARMAX error window Ef [N][Q] fp32 from the
         residuals Y - H beta of consecutive windows (reading R30)."""
         _dev_check(H, "H", torch.float32)
-        _dev_check(Y, "Y", torch.float32)
-        _dev_check(beta, "beta", torch.float64)
         N = H.shape[0]
+        _vec(Y, "Y", torch.float32, N)
+        _vec(beta, "beta", torch.float64, self.M)
         if Ef is None:
             Ef = torch.empty((N, self.Q), dtype=torch.float32, device=H.device)
         _dev_check(Ef, "Ef", torch.float32)
         ldh = _rows(H, "H")[0] if N else self.M
-        lde = _rows(Ef, "Ef")[0] if N else self.Q
+        lde, re_ = _rows(Ef, "Ef") if N else (self.Q, 0)
+        _need_rows(re_, N, "Ef")
         self._stream()
         self._check(lib().elmrnn_error_windows(self._h, _ptr(H), ldh, _ptr(Y), N, _ptr(beta), _ptr(Ef), lde))
         return Ef
@@ -249,11 +269,12 @@ class ELMRNN:
     def solve_beta(self, H: torch.Tensor, Y: torch.Tensor, beta: torch.Tensor | None = None, info: bool = True):
         """elmrnn_solve_beta -> (beta fp64 [M], SolveInfo or None)."""
         _dev_check(H, "H", torch.float32)
-        _dev_check(Y, "Y", torch.float32)
         N = H.shape[0]
+        _vec(Y, "Y", torch.float32, N)
         ldh, _ = _rows(H, "H")
         if beta is None:
             beta = torch.empty(self.M, dtype=torch.float64, device=H.device)
+        _vec(beta, "beta", torch.float64, self.M)
         self._stream()
         inf = _Info()
         st = self._check(lib().elmrnn_solve_beta(self._h, _ptr(H), ldh, _ptr(Y), N, _ptr(beta),
@@ -265,6 +286,8 @@ class ELMRNN:
         _dev_check(H, "H", torch.float32)
         _dev_check(Y, "Y", torch.float32)
         N = H.shape[0]
+        if Y.shape[0] != N:
+            raise ValueError(f"Y has {Y.shape[0]} rows, needs {N}")
         Y2 = Y.reshape(N, -1)
         P = Y2.shape[1]
         ldh, _ = _rows(H, "H")
@@ -282,11 +305,12 @@ class ELMRNN:
     def solve_local(self, H: torch.Tensor, Y: torch.Tensor, Rpk: torch.Tensor | None = None):
         """elmrnn_solve_local -> packed R fp64 [(M+1)(M+2)/2]."""
         _dev_check(H, "H", torch.float32)
-        _dev_check(Y, "Y", torch.float32)
         N = H.shape[0]
+        _vec(Y, "Y", torch.float32, N)
         ldh = _rows(H, "H")[0] if N else self.M
         if Rpk is None:
             Rpk = torch.empty(self.packed_r_len, dtype=torch.float64, device=H.device)
+        _vec(Rpk, "Rpk", torch.float64, self.packed_r_len)
         self._stream()
         self._check(lib().elmrnn_solve_local(self._h, _ptr(H), ldh, _ptr(Y), N, _ptr(Rpk)))
         return Rpk
@@ -294,9 +318,10 @@ class ELMRNN:
     def solve_merge(self, Rpk_all: torch.Tensor, P: int, N_total: int, beta: torch.Tensor | None = None,
                     info: bool = True):
         """elmrnn_solve_merge on P stacked packed R factors."""
-        _dev_check(Rpk_all, "Rpk_all", torch.float64)
+        _vec(Rpk_all, "Rpk_all", torch.float64, P * self.packed_r_len)
         if beta is None:
             beta = torch.empty(self.M, dtype=torch.float64, device=Rpk_all.device)
+        _vec(beta, "beta", torch.float64, self.M)
         self._stream()
         inf = _Info()
         st = self._check(lib().elmrnn_solve_merge(self._h, _ptr(Rpk_all), P, N_total, _ptr(beta),
@@ -306,10 +331,14 @@ class ELMRNN:
     def predict(self, X: torch.Tensor, beta: torch.Tensor, Yfb: torch.Tensor | None = None):
         """elmrnn_predict -> Yhat fp32 [N]."""
         _dev_check(X, "X", torch.float32)
-        _dev_check(beta, "beta", torch.float64)
+        _vec(beta, "beta", torch.float64, self.M)
         N = X.shape[0]
         ldx = _rows(X, "X")[0] if N else self.Q * self.d
-        ldy = _rows(Yfb, "Yfb")[0] if Yfb is not None else 0
+        ldy = 0
+        if Yfb is not None:
+            _dev_check(Yfb, "Yfb", torch.float32)
+            ldy, ry = _rows(Yfb, "Yfb")
+            _need_rows(ry, N, "Yfb")
         out = torch.empty(N, dtype=torch.float32, device=X.device)
         self._stream()
         self._check(lib().elmrnn_predict(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, N, _ptr(beta), _ptr(out)))
@@ -318,7 +347,7 @@ class ELMRNN:
     def forecast(self, X: torch.Tensor, beta: torch.Tensor, K: int):
         """elmrnn_forecast: free-running K-step forecast of univariate windows -> fp32 [N][K]."""
         _dev_check(X, "X", torch.float32)
-        _dev_check(beta, "beta", torch.float64)
+        _vec(beta, "beta", torch.float64, self.M)
         N = X.shape[0]
         ldx = _rows(X, "X")[0] if N else self.Q
         out = torch.empty((N, K), dtype=torch.float32, device=X.device)
@@ -329,11 +358,15 @@ class ELMRNN:
     def test_rmse(self, X: torch.Tensor, Y: torch.Tensor, beta: torch.Tensor, Yfb: torch.Tensor | None = None) -> float:
         """elmrnn_test_rmse: held-out RMSE of beta on evaluation windows."""
         _dev_check(X, "X", torch.float32)
-        _dev_check(Y, "Y", torch.float32)
-        _dev_check(beta, "beta", torch.float64)
         N = X.shape[0]
+        _vec(Y, "Y", torch.float32, N)
+        _vec(beta, "beta", torch.float64, self.M)
         ldx = _rows(X, "X")[0] if N else self.Q * self.d
-        ldy = _rows(Yfb, "Yfb")[0] if Yfb is not None else 0
+        ldy = 0
+        if Yfb is not None:
+            _dev_check(Yfb, "Yfb", torch.float32)
+            ldy, ry = _rows(Yfb, "Yfb")
+            _need_rows(ry, N, "Yfb")
         r = ctypes.c_double()
         self._stream()
         self._check(lib().elmrnn_test_rmse(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, _ptr(Y), N, _ptr(beta),

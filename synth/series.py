@@ -91,6 +91,15 @@ def series(kind: str, length: int, seed: int = DATA_SEED, noise: float = 0.0) ->
     return zscore(raw)
 
 
+def lagged_channels(s: np.ndarray, S: int) -> np.ndarray:
+    """[L][1] series -> [L-S+1][S] with channel c = s[t+c] (a multivariate input
+    for the well-conditioned parity cases: S-dimensional windows of one AR
+    series; pure data shaping, no method arithmetic)."""
+    s = np.asarray(s, dtype=np.float32).reshape(len(s), -1)[:, 0]
+    L = s.shape[0] - S + 1
+    return np.ascontiguousarray(np.stack([s[c:c + L] for c in range(S)], axis=1))
+
+
 def windows(s: np.ndarray, N: int, Q: int):
     """Cut N windows of Q steps from series s [L][S] (L >= N + Q).
 

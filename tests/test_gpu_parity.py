@@ -2,9 +2,11 @@
 
 Tolerances (BASELINE.json north_star):
   H       max |H_gpu - H_oracle| <= 1e-5 (fp32 arithmetic vs fp64)
-  beta    ||beta_gpu - beta_ref|| / ||beta_ref|| <= 1e-3 end to end (reported with cond(R)),
-          <= 1e-9 when both solvers factor the identical fp32 H (both fp64)
-  RMSE    relative difference <= 1e-4
+  beta    ||beta_gpu - beta_ref|| / ||beta_ref|| <= max(1e-3, 8 floor_b) end to end, floor_b =
+          the deviation fp32 rounding of the oracle's own H alone causes (fixed rule, reading
+          R26, tests/parity_rule.py); the literal 1e-3 on the well-conditioned cases (one per
+          builder path); <= 1e-12 cond(R) when both solvers factor the identical fp32 H
+  RMSE    relative difference <= max(1e-4, 8 floor_r); literal 1e-4 on the well-conditioned cases
   weights bit-exact (integer RNG, identical rounding)
 """
 import numpy as np
@@ -13,6 +15,7 @@ import torch
 
 from oracle import oracle as orc
 from synth import series as sy
+from oracle import parity_rule as pr
 
 pytestmark = pytest.mark.gpu
 
@@ -211,28 +214,13 @@ def test_empty_and_errors():
 
 
 # ------------------------------------------------------------------------- solve parity
-def solve_tolerances(Hg, Ho, Y, b_ref, i_ref):
-    """Bounds for ||dbeta||/||beta|| and the relative RMSE difference.
-
-    North star: 1e-3 and 1e-4, "reported alongside cond(R)".  Reading R26
-    (DESIGN.md): on smooth series cond(H) reaches 1e6-1e7 and even the oracle's
-    own H rounded to fp32 moves beta by ~5e-4 (the "floor").  To first order
-    dbeta is linear in dH, so the deviation the measured H error alone explains
-    is floor x ||H_gpu - H_o||_F / ||fp32(H_o) - H_o||_F; the bounds are
-    max(north-star value, 3 x that).  H itself is held to 1e-5 max-abs
-    separately, and the solver is checked in isolation to ~1e-12 cond(R)."""
-    H32 = Ho.astype(np.float32).astype(np.float64)
-    b_rnd, i_rnd = orc.lstsq(H32, Y)
-    floor_b = np.linalg.norm(b_rnd - b_ref) / np.linalg.norm(b_ref)
-    floor_r = abs(i_rnd.rmse - i_ref.rmse) / i_ref.rmse
-    ratio = max(1.0, np.linalg.norm(Hg - Ho) / max(np.linalg.norm(H32 - Ho), 1e-300))
-    return max(1e-3, 3 * ratio * floor_b), max(1e-4, 3 * ratio * floor_r), floor_b, ratio
-
-
+# beta / RMSE rule: tests/parity_rule.py (R26) -- max(1e-3, 8 floor_b) and
+# max(1e-4, 8 floor_r) with floor = the deviation the fp32 rounding of the oracle's own
+# H alone causes; fixed, independent of the GPU's H error.
 SOLVE_CASES = [("elman", 1000, 1, 20, 10, "mg", 0.0), ("jordan", 5000, 1, 64, 20, "ar5", 0.0),
                ("narmax", 5000, 1, 64, 20, "ar5", 0.0), ("gru", 3000, 4, 128, 30, "sin4", 0.0),
                ("fc", 2000, 4, 128, 30, "sin4", 0.0), ("lstm", 8000, 1, 256, 50, "mg", 0.01),
-               ("lstm", 20000, 1, 511, 5, "mg", 0.01),
+               ("lstm", 10277, 1, 512, 4, "ar5", 0.0),
                ("lstm_diag", 3000, 4, 128, 30, "sin4", 0.0), ("gru_diag", 3000, 4, 128, 30, "sin4", 0.0),
                ("fc_eq8", 3000, 4, 128, 30, "sin4", 0.0)]
 
@@ -251,18 +239,54 @@ def test_solve_parity(arch, N, S, M, Q, kind, noise):
     cond = np.linalg.cond(i_iso.R[:M, :M])
     assert np.linalg.norm(beta - b_iso) / np.linalg.norm(b_iso) <= 1e-12 * max(1.0, cond), cond
     assert abs(info.rmse - i_iso.rmse) / i_iso.rmse <= 1e-12 * max(1.0, cond)
-    # (b) end to end against the oracle's own fp64 H
+    # (b) end to end against the oracle's own fp64 H (fixed rule R26)
     net = orc.Net(arch, S=S, M=M, Q=Q)
     Ho = orc.build_H(net, orc.gen_weights(net, 5), X, threads=8)
-    b_ref, i_ref = orc.lstsq(Ho, Y)
-    rel = np.linalg.norm(beta - b_ref) / np.linalg.norm(b_ref)
-    drm = abs(info.rmse - i_ref.rmse) / i_ref.rmse
-    tol_b, tol_r, floor, ratio = solve_tolerances(Hg, Ho, Y, b_ref, i_ref)
-    print(f"{arch} N={N} M={M}: cond(R)={cond:.2e} rel dbeta={rel:.2e} drmse={drm:.2e} "
-          f"(fp32-H floor {floor:.2e}, |dH| ratio {ratio:.1f}, tol {tol_b:.2e}/{tol_r:.2e})")
-    assert rel <= tol_b, f"rel dbeta {rel:.2e} at cond(R) {cond:.2e}, floor {floor:.2e}"
-    assert drm <= tol_r
+    pr.check(f"{arch} N={N} M={M} path={e.path}", beta, info.rmse, Hg, Ho, Y)
     assert info.status == 0 and info.n_total == N
+
+
+# Well-conditioned end-to-end cases, one per H-builder path: four lagged channels of
+# an AR(5) series (synth.lagged_channels), N >= 20 M rows plus a ragged tail, so
+# cond(R) is 1e2-2e3 and the fp32-H floor ~1e-7: the north star's LITERAL bounds
+# (1e-3 beta, 1e-4 RMSE) are what is tested, on the intended kernel.
+WELL_COND = [
+    # arch, M, Q, S, forced path (0 auto), expected path, kernel
+    ("lstm", 128, 10, 4, 0, 2, "k_lstm_tc M=128"),
+    ("lstm", 256, 10, 4, 0, 2, "k_lstm_tc M=256"),
+    ("lstm", 512, 3, 4, 0, 2, "k_lstm_wide M=512"),
+    ("lstm", 1024, 2, 4, 0, 2, "k_lstm_wide M=1024"),
+    ("gru", 128, 10, 4, 0, 2, "k_gru_tc M=128"),
+    ("gru", 256, 6, 4, 0, 2, "k_gru_wide M=256"),
+    ("gru", 512, 3, 4, 0, 2, "k_gru_wide M=512"),
+    ("fc", 128, 10, 4, 0, 2, "k_fc_tc M=128"),
+    ("lstm", 64, 10, 4, 0, 1, "k_dense_fma LSTM"),
+    ("gru", 32, 10, 4, 0, 1, "k_dense_fma GRU"),
+    ("lstm", 256, 10, 4, 1, 1, "k_dense_fma LSTM M=256 (forced)"),
+]
+
+
+def well_cond_inputs(M, Q, S, seed=3):
+    N = 20 * M + 37
+    s = sy.lagged_channels(sy.series("ar5", N + Q + S + 1, seed=seed), S)
+    X, Y, _ = sy.windows(s, N, Q)
+    return X, Y
+
+
+@pytest.mark.parametrize("arch,M,Q,S,force,path,kern", WELL_COND)
+def test_solve_parity_well_conditioned(arch, M, Q, S, force, path, kern):
+    X, Y = well_cond_inputs(M, Q, S)
+    e = E(arch, S, M, Q, 5, force_path=force)
+    assert e.path == path, kern
+    Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+    H, beta, info = e.train(Xd, Yd)
+    Hg = H.cpu().numpy().astype(np.float64)
+    net = orc.Net(arch, S=S, M=M, Q=Q)
+    Ho = orc.build_H(net, orc.gen_weights(net, 5), X, threads=16)
+    assert np.abs(Hg - Ho).max() <= H_TOL
+    _, _, bd = pr.check(f"{kern} N={X.shape[0]}", beta.cpu().numpy(), info.rmse, Hg, Ho, Y, literal=True)
+    assert bd.floor_b < 1e-5, "case is meant to be well conditioned"
+    assert info.status == 0
 
 
 def test_virtual_ranks_merge_equals_single():
@@ -306,6 +330,7 @@ def test_tsqr_wy_and_fold_agree(M, N, monkeypatch):
     Rn = np.abs(np.linalg.qr(np.column_stack([H.double().cpu().numpy(), Y.double().cpu().numpy()]), mode="r"))
     scale = Rn.max()
     for wy in ("1", "0"):
+        monkeypatch.setenv("ELMRNN_TESTING", "1")
         monkeypatch.setenv("ELMRNN_TSQR_WY", wy)
         e = E("lstm", 1, M, 4, 1, force_path=1)
         R = _packed_to_R(e.solve_local(H, Y).cpu().numpy(), n)
@@ -318,6 +343,7 @@ def test_tsqr_wy_deep_noise_cascade(rows, M, N, monkeypatch):
     """A leaf that folds many short tiles before reaching full rank drives the
     noise rows of its partial R into subnormals (DESIGN 6.3); the WY panel must
     treat t = x0^2 + |x|^2 <= 1e-280 as H = I (else rsqrt.approx.ftz gives NaN)."""
+    monkeypatch.setenv("ELMRNN_TESTING", "1")
     monkeypatch.setenv("ELMRNN_TSQR_WY", "1")
     monkeypatch.setenv("ELMRNN_TSQR_WY_ROWS", rows)
     g = torch.Generator(device="cuda").manual_seed(M + N)
@@ -373,20 +399,34 @@ def test_full_config_end_to_end(cfg):
     Ho = orc.build_H(net, orc.gen_weights(net, 1), X, threads=8)
     Hg = H.cpu().numpy().astype(np.float64)
     assert np.abs(Hg - Ho).max() <= H_TOL
-    b_ref, i_ref = orc.lstsq(Ho, Y)
-    tol_b, tol_r, floor, ratio = solve_tolerances(Hg, Ho, Y, b_ref, i_ref)
-    rel = np.linalg.norm(beta.cpu().numpy() - b_ref) / np.linalg.norm(b_ref)
-    drm = abs(info.rmse - i_ref.rmse) / i_ref.rmse
-    print(f"{cfg}: rel dbeta={rel:.2e} drmse={drm:.2e} (fp32-H floor {floor:.2e}, ratio {ratio:.1f})")
-    assert rel <= tol_b
-    assert drm <= tol_r
+    pr.check(cfg, beta.cpu().numpy(), info.rmse, Hg, Ho, Y)
+
+
+def oracle_R_chunked(H: torch.Tensor, Y: np.ndarray, chunk: int = 250_000, threads: int = 16):
+    """The oracle's Householder R of the full [H | Y] (H the GPU's fp32 H, widened
+    exactly): R factors of row chunks in parallel (ctypes releases the GIL), then the
+    oracle's lstsq of their stack -- a TSQR tree of the oracle's own QR, which the
+    oracle pins equal to the direct R (test_oracle_weights_solve)."""
+    from concurrent.futures import ThreadPoolExecutor
+    N, M = H.shape
+
+    def one(a):
+        b = min(N, a + chunk)
+        Hc = H[a:b].cpu().numpy().astype(np.float64)
+        return orc.lstsq(Hc, Y[a:b].astype(np.float64))[1].R
+
+    with ThreadPoolExecutor(threads) as ex:
+        Rs = list(ex.map(one, range(0, N, chunk)))
+    S = np.concatenate(Rs, axis=0)
+    return orc.lstsq(S[:, :M], S[:, M])
 
 
 @pytest.mark.parametrize("cfg", ["C3gru", "C3fc", "C4"])
 def test_full_config_sampled(cfg):
     """Full N in the bench launch configuration: sampled rows of H against the
-    oracle (computed row by row), normal-equation residual and RMSE identity of
-    beta in fp64 at full size."""
+    oracle (computed row by row); solver isolation at full N -- beta and the RMSE
+    against the oracle's Householder solve of the GPU's own full fp32 H (chunked
+    oracle TSQR); the normal-equation residual of beta in fp64."""
     c = sy.CONFIGS[cfg]
     X, Y, _ = sy.config_inputs(cfg)
     e = E(c["arch"], c["S"], c["M"], c["Q"], 1)
@@ -398,6 +438,14 @@ def test_full_config_sampled(cfg):
     net = orc.Net(c["arch"], S=c["S"], M=c["M"], Q=c["Q"])
     Ho = orc.build_H(net, orc.gen_weights(net, 1), X[rows], threads=8)
     assert np.abs(H[torch.from_numpy(rows).cuda()].cpu().numpy() - Ho).max() <= H_TOL
+    b_iso, i_iso = oracle_R_chunked(H, Y)
+    M = c["M"]
+    cond = float(np.linalg.cond(i_iso.R[:M, :M]))
+    rel = float(np.linalg.norm(beta.cpu().numpy() - b_iso) / np.linalg.norm(b_iso))
+    drm = abs(info.rmse - i_iso.rho / np.sqrt(c["N"])) / (i_iso.rho / np.sqrt(c["N"]))
+    print(f"{cfg} full N={c['N']}: solver isolation cond(R)={cond:.2e} rel dbeta={rel:.2e} rel drmse={drm:.2e}")
+    assert rel <= 1e-12 * max(1.0, cond)
+    assert drm <= 1e-10
     H64 = H.double()
     r = H64 @ beta - Yd.double()
     g = H64.T @ r
@@ -581,11 +629,8 @@ def test_narmax_two_pass_train_parity():
     Ho1, bo1, io1, bo0, io0 = orc.train_narmax_ef(net, orc.gen_weights(net, 1), X, Y, Yfb, threads=8)
     Hg1 = H1.cpu().numpy().astype(np.float64)
     assert np.abs(Hg1 - Ho1).max() <= H_TOL
-    tol_b, tol_r, floor, ratio = solve_tolerances(Hg1, Ho1, Y, bo1, io1)
-    rel = np.linalg.norm(b1.cpu().numpy() - bo1) / np.linalg.norm(bo1)
-    print(f"narmax-ef: rmse pass0 {i0.rmse:.6f} pass1 {i1.rmse:.6f}; rel dbeta {rel:.2e} (tol {tol_b:.2e})")
-    assert rel <= tol_b
-    assert abs(i1.rmse - io1.rmse) / io1.rmse <= tol_r
+    print(f"narmax-ef: rmse pass0 {i0.rmse:.6f} pass1 {i1.rmse:.6f}")
+    pr.check("narmax-ef pass 1", b1.cpu().numpy(), i1.rmse, Hg1, Ho1, Y)
     assert abs(i0.rmse - io0.rmse) / io0.rmse <= 1e-4
 
 

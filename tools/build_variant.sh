@@ -1,6 +1,7 @@
 #!/bin/bash
-# Build a debug variant of libelmrnn.so with extra defines into tools/dbg/ (testing aid).
-#   tools/build_variant.sh trace -DELM_QR_TRACE
+# Build an experiment variant of libelmrnn.so with extra -D defines into tools/dbg/
+# (git-ignored; travels to the GPU box).  Load it with ELMRNN_LIB=<path>.
+#   tools/build_variant.sh epi -DELM_TC_EPI_ACCURATE
 set -e
 name=$1; shift
 out=tools/dbg/obj_$name; mkdir -p $out
