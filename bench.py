@@ -73,6 +73,21 @@ def algorithmic_bytes_per_sample(arch: str, S: int, M: int, Q: int) -> float:
     return 4 * Q * S + 4 * M
 
 
+def qr_flops(M: int, N: int, nrhs: int = 1) -> float:
+    """fp64 Householder TSQR of [H | Y]: 2 (M+P)^2 flop per row."""
+    return 2.0 * N * (M + nrhs) ** 2
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -190,7 +205,8 @@ def run_reference(args, rank: int, world: int):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD_NAMES[cfg], "rows_per_step": n},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -328,8 +344,8 @@ def main():
         barrier()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         cs = torch.cuda.Stream()
-        # chunked copy/build overlap pays only when the copy is long; small inputs
-        # (C1, C2) take one copy and one launch
+        # chunked copy/build overlap pays only when the copy is long; inputs under
+        # 4 MiB (C1) take one copy and one launch
         e2e_chunks = 4 if Xh.numel() * 4 > 4 * 2**20 else 1
 
         def e2e_step():
@@ -389,21 +405,78 @@ def main():
         achieved = flops / (build_ms / 1e3) / 1e12
         peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         peak_note = "derived FP32 FFMA: 148 SMs x 128 lanes x 2 flop x sm_max_mhz"
-    traffic = None
+    traffic = qr_traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
-        traffic = json.load(open(tf)).get(f"{cfg}:path{path}")
+        tj = json.load(open(tf))
+        traffic = tj.get(f"{cfg}:path{path}")
+        qr_traffic = tj.get(f"{cfg}:qr")
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
             "traffic": traffic, "kernel": "build_H", "kernel_ms": build_ms, "peak_source": peak_note}
+
+    # ---- per-phase and overall fractions (the paper's Fig. 6 runtime
+    # decomposition): lower bound of a phase = max over pipes of work / peak;
+    # overall = sum of the phase bounds / measured step.  "burst" peaks: measured bf16
+    # burst, derived FP32/FP64 at sm_max_mhz; "sustained": measured bf16 sustained,
+    # derived FP32/FP64 at the median SM clock seen during the timed region.
+    ck = clk.summary()
+    mhz_max = float(peaks.get("sm_max_mhz", 1965.0))
+    mhz_live = float(ck.get("sm_mhz") or mhz_max)
+    hbm = peaks["hbm_gbs"] * 1e9
+    passes = 2 if args.weight_grid == 1 else 3
+
+    def lb_build(basis):
+        f = flops
+        by = algorithmic_bytes_per_sample(c["arch"], c["S"], c["M"], c["Q"]) * N_local
+        mhz = mhz_max if basis == "burst" else mhz_live
+        t = {"hbm": by / hbm}
+        if path == 2 and c["arch"] in ("lstm", "gru", "fc"):
+            tens = peaks["bf16_tflops" if basis == "burst" else "bf16_tflops_sustained"] * 1e12 / passes
+            t["tensor"] = f / tens
+        else:
+            t["alu"] = f / (148 * 128 * 2 * mhz * 1e6)
+        return t
+
+    def lb_qr(basis):
+        mhz = mhz_max if basis == "burst" else mhz_live
+        return {"fp64": qr_flops(c["M"], N_local) / (148 * 64 * 2 * mhz * 1e6),
+                "hbm": 4.0 * (c["M"] + 1) * N_local / hbm}
+
+    reps = 2 if two_pass else 1   # C2n_ef: two builds and two solves per step
+    phases = {}
+    for name, fn, meas in (("build_H", lb_build, build_ms), ("solve", lb_qr, ms_step_eager - build_ms)):
+        b, su = fn("burst"), fn("sustained")
+        lb_b = reps * max(b.values()) * 1e3
+        lb_s = reps * max(su.values()) * 1e3
+        phases[name] = {"bound": max(b, key=b.get), "lb_ms_burst": lb_b, "lb_ms_sustained": lb_s, "ms": meas,
+                        "frac_burst": lb_b / meas if meas > 0 else None,
+                        "frac_sustained": lb_s / meas if meas > 0 else None}
+    lb_tot_b = phases["build_H"]["lb_ms_burst"] + phases["solve"]["lb_ms_burst"]
+    lb_tot_s = phases["build_H"]["lb_ms_sustained"] + phases["solve"]["lb_ms_sustained"]
+    phases["overall"] = {"lb_ms_burst": lb_tot_b, "lb_ms_sustained": lb_tot_s, "ms": ms_step,
+                         "frac_burst": lb_tot_b / ms_step, "frac_sustained": lb_tot_s / ms_step}
+    roof["phases"] = phases
+    roof["qr_traffic"] = qr_traffic
+    roof["peaks_note"] = (f"tensor = {src} bf16 (burst {peaks['bf16_tflops']}, sustained "
+                          f"{peaks.get('bf16_tflops_sustained')}) / {passes}; FP64 = 148 SMs x 64 FMA x 2 x clock "
+                          f"({mhz_max:.0f} MHz burst, {mhz_live:.0f} MHz live); FP32 FFMA likewise x 128 lanes; "
+                          f"HBM = {src} copy {peaks['hbm_gbs']} GB/s")
 
     cpu = None
     if not args.no_cpu_baseline and not args.profile and world == 1:
         n_sub = oracle_sample_rows(cfg)
         threads = os.cpu_count() or 1
         rate, dt = cpu_oracle_rate(cfg, n_sub, X, Y, threads, args.weight_grid)
+        # single-thread figure on a smaller bounded sample (same per-row work)
+        n1 = max(2 * (c["M"] + 1), n_sub // threads)
+        rate1, dt1 = cpu_oracle_rate(cfg, n1, X, Y, 1, args.weight_grid)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"{n_sub} windows of the same workload, fp64 H build ({threads} threads) + fp64 "
-                         f"Householder QR (1 thread), {dt:.1f} s"}
+               "sample": f"{n_sub} windows of the same workload, fp64 H build ({threads} threads, OpenMP row "
+                         f"split) + unblocked fp64 Householder QR (1 thread), {dt:.1f} s; per-row work is "
+                         f"independent of N, so the rate extrapolates linearly to the full N",
+               "threads_1": {"value": rate1, "unit": UNIT, "cores": 1,
+                             "sample": f"{n1} windows, H build and QR on 1 thread, {dt1:.1f} s"},
+               "cpu_model": cpu_model(), "nproc": threads}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -417,7 +490,7 @@ def main():
                        "phases_ms": {"build_H": build_ms, "solve": ms_step_eager - build_ms,
                                      "step_eager": ms_step_eager}},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary()}
+            "clocks": ck}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -189,6 +189,33 @@ ELMRNN_API elmrnn_status elmrnn_solve_local(elmrnn_t h, const float* H, int64_t 
 ELMRNN_API elmrnn_status elmrnn_solve_merge(elmrnn_t h, const double* Rpk_all, int P, int64_t N_total,
                                  double* beta, elmrnn_solve_info* info);
 
+/* Row-sharded multi-output solve, step 1: factor the
+ * local [H | Y_1 .. Y_P] (N rows) into its (M+P)x(M+P) upper-triangular R, packed
+ * row-major to Rpk dev fp64 [elmrnn_packed_r_len_multi(h, P)].  H dev fp32
+ * [N][ldh]; Y dev fp32 [N][ldy], ldy >= P.  N may be 0.  Asynchronous.
+ * Errors: ARG, SHAPE, UNSUPPORTED (M + P > 1536), OOM, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_solve_local_multi(elmrnn_t h, const float* H, int64_t ldh, const float* Y,
+                                       int64_t ldy, int P, int64_t N, double* Rpk);
+
+/* Step 2: merge `ranks` packed R factors of step 1 (dev fp64 [ranks][len]) by
+ * Householder QR of their stack, then P back substitutions as
+ * elmrnn_solve_beta_multi: beta dev fp64 [P][M]; rmse host fp64 [P] or NULL
+ * (synchronises); info as elmrnn_solve_beta_multi.
+ * Errors: ARG, UNSUPPORTED, UNDERDETERMINED (N_total < M), NONFINITE, OOM, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_solve_merge_multi(elmrnn_t h, const double* Rpk_all, int ranks, int P,
+                                       int64_t N_total, double* beta, double* rmse,
+                                       elmrnn_solve_info* info);
+
+/* (M+P)(M+P+1)/2: length of one packed multi-output R in doubles (-1 if P < 1). */
+ELMRNN_API int64_t elmrnn_packed_r_len_multi(elmrnn_t h, int P);
+
+/* Synchronise the handle's stream and report what asynchronous solves (info ==
+ * NULL) could not: ERR_NONFINITE when any solve since the last synchronising
+ * check (this call, or a solve with info != NULL) met NaN/Inf in H or Y (the
+ * leaf kernels OR a device flag that the solve kernel accumulates).  The
+ * flag is cleared.  Errors: ARG, NONFINITE, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_sync(elmrnn_t h);
+
 /* (M+1)(M+2)/2: length of one packed R in doubles. */
 ELMRNN_API int64_t elmrnn_packed_r_len(elmrnn_t h);
 

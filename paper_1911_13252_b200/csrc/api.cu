@@ -176,15 +176,24 @@ elmrnn_status elmrnn_error_windows(elmrnn_t h, const float* H, int64_t ldh, cons
     return ELMRNN_OK;
 }
 
+// Read the device diagnostics (synchronises the stream) and clear the sticky
+// non-finite flag that asynchronous solves accumulate.
+static cudaError_t read_solve_dev(elmrnn* h) {
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(h->shost, h->sdev, sizeof(SolveDev), cudaMemcpyDeviceToHost, h->stream)) ||
+        (e = cudaMemsetAsync(&h->sdev->nf_sticky, 0, sizeof(int), h->stream)) ||
+        (e = cudaStreamSynchronize(h->stream)))
+        return e;
+    return cudaSuccess;
+}
+
 static elmrnn_status finish_solve(elmrnn* h, elmrnn_solve_info* info) {
     cudaError_t e;
     if (!info) {
         if ((e = cudaGetLastError())) return cuda_fail(h, e, "solve");
         return ELMRNN_OK;
     }
-    if ((e = cudaMemcpyAsync(h->shost, h->sdev, sizeof(SolveDev), cudaMemcpyDeviceToHost, h->stream)) ||
-        (e = cudaStreamSynchronize(h->stream)))
-        return cuda_fail(h, e, "solve");
+    if ((e = read_solve_dev(h))) return cuda_fail(h, e, "solve");
     const SolveDev& s = *h->shost;
     info->rho = s.rho; info->rmse = s.rmse; info->rdiag_min_abs = s.dmin; info->rdiag_max_abs = s.dmax;
     info->ridge_lambda = s.lambda; info->rank_flag = s.rank_flag; info->n_total = s.n_total;
@@ -259,6 +268,71 @@ elmrnn_status elmrnn_solve_merge(elmrnn_t h, const double* Rpk_all, int P, int64
     if ((e = tsqr_merge_packed(h, Rpk_all, P))) return cuda_fail(h, e, "tsqr_merge");
     if ((e = tsqr_solve(h, N_total, beta))) return cuda_fail(h, e, "tsqr_solve");
     return finish_solve(h, info);
+}
+
+elmrnn_status elmrnn_sync(elmrnn_t h) {
+    if (!h) return ELMRNN_ERR_ARG;
+    cudaError_t e;
+    if ((e = cudaStreamSynchronize(h->stream))) return cuda_fail(h, e, "sync");
+    if (!h->sdev) return ELMRNN_OK;   // no solve has run on this handle
+    if ((e = read_solve_dev(h))) return cuda_fail(h, e, "sync");
+    if (h->shost->nf_sticky)
+        return fail(h, ELMRNN_ERR_NONFINITE, "NaN or Inf in H or Y in an asynchronous solve since the last check");
+    return ELMRNN_OK;
+}
+
+elmrnn_status elmrnn_solve_local_multi(elmrnn_t h, const float* H, int64_t ldh, const float* Y, int64_t ldy, int P,
+                                       int64_t N, double* Rpk) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (!Rpk || N < 0 || P < 1 || (N > 0 && (!H || !Y))) return fail(h, ELMRNN_ERR_ARG, "bad argument");
+    if (ldh < h->M) return fail(h, ELMRNN_ERR_SHAPE, "ldh < M");
+    if (ldy < P) return fail(h, ELMRNN_ERR_SHAPE, "ldy < P");
+    if (h->M + P > 1536) return fail(h, ELMRNN_ERR_UNSUPPORTED, "M + P <= 1536 (one 16-row WY tile in shared memory)");
+    struct Nrhs { elmrnn* h; ~Nrhs() { h->nrhs = 1; } } guard{h};
+    h->nrhs = P;
+    cudaError_t e;
+    if ((e = tsqr_factor(h, H, ldh, Y, ldy, N))) return cuda_fail(h, e, "tsqr_factor");
+    if ((e = tsqr_pack(h, Rpk))) return cuda_fail(h, e, "tsqr_pack");
+    return ELMRNN_OK;
+}
+
+elmrnn_status elmrnn_solve_merge_multi(elmrnn_t h, const double* Rpk_all, int ranks, int P, int64_t N_total,
+                                       double* beta, double* rmse, elmrnn_solve_info* info) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (!Rpk_all || !beta || ranks < 1 || P < 1) return fail(h, ELMRNN_ERR_ARG, "bad argument");
+    if (h->M + P > 1536) return fail(h, ELMRNN_ERR_UNSUPPORTED, "M + P <= 1536");
+    if (N_total < h->M) return fail(h, ELMRNN_ERR_UNDERDETERMINED, "N_total < M");
+    cudaError_t e;
+    if (P > h->rho_multi_len) {
+        if (h->rho_multi) cudaFree(h->rho_multi);
+        h->rho_multi = nullptr;
+        h->rho_multi_len = 0;
+        if ((e = cudaMalloc(&h->rho_multi, sizeof(double) * P))) return cuda_fail(h, e, "workspace");
+        h->rho_multi_len = P;
+    }
+    struct Nrhs { elmrnn* h; ~Nrhs() { h->nrhs = 1; } } guard{h};
+    h->nrhs = P;
+    if ((e = tsqr_merge_packed(h, Rpk_all, ranks))) return cuda_fail(h, e, "tsqr_merge");
+    if ((e = tsqr_solve(h, N_total, beta))) return cuda_fail(h, e, "tsqr_solve");
+    elmrnn_solve_info tmp;
+    elmrnn_solve_info* ip = info ? info : (rmse ? &tmp : nullptr);
+    const elmrnn_status st = finish_solve(h, ip);
+    if (st < 0 || !rmse) return st;
+    if (P == 1) {
+        rmse[0] = ip->rmse;
+        return st;
+    }
+    std::vector<double> rho(P);
+    if ((e = cudaMemcpyAsync(rho.data(), h->rho_multi, sizeof(double) * P, cudaMemcpyDeviceToHost, h->stream)) ||
+        (e = cudaStreamSynchronize(h->stream)))
+        return cuda_fail(h, e, "solve");
+    for (int p = 0; p < P; ++p) rmse[p] = rho[p] / std::sqrt((double)N_total);
+    return st;
+}
+
+int64_t elmrnn_packed_r_len_multi(elmrnn_t h, int P) {
+    if (!h || P < 1) return -1;
+    return (int64_t)(h->M + P) * (h->M + P + 1) / 2;
 }
 
 int64_t elmrnn_packed_r_len(elmrnn_t h) {

@@ -23,6 +23,7 @@ struct SolveDev {
     int rank_flag;
     int nonfinite;
     long long n_total;
+    int nf_sticky;   // OR of `nonfinite` over the solves since the last synchronising check
 };
 
 // Tuning overrides: defaults are the measured choices; a test may override them
@@ -158,6 +159,30 @@ __device__ __forceinline__ float act_g(float a, int act) { return act == 1 ? tan
 // fp64 forms for the latency-bound per-cell builders
 __device__ __forceinline__ double sigmoid64(double a) { return 1.0 / (1.0 + exp(-a)); }
 __device__ __forceinline__ double act_g64(double a, int act) { return act == 1 ? tanh(a) : sigmoid64(a); }
+// Gate forms of the tensor-core epilogues, from exp2-domain arguments (the
+// gate's log2(e) factor and the 2^-sigma operand scale are folded into the
+// accumulator scale and W|b on the host):
+//   sig_e2(a2)  = 1 / (1 + 2^a2)            = sigma(x) for a2 = -log2(e) x
+//   tanh_e2(a2) = tanh(a2 / (2 log2(e)))    = tanh(x)  for a2 = 2 log2(e) x
+// Accuracy matters more than MUFU count here: a shared reciprocal of 2-4 gate
+// denominators and tanh(x) as 1 - 2/(1 + e^2x) left a systematic bias in H
+// (mean -7e-9, measured) that ill-conditioned solves amplify into beta (6-7x
+// the fp32-rounding floor; DESIGN R26).  ex2.approx + rcp.approx with one
+// Newton step is correctly rounded in practice (bitwise equal to
+// 1.0f / (1.0f + exp2f(a2)) on the parity cases), tanhf is libm's (<= 2 ulp).
+__device__ __forceinline__ float sig_e2(float a2) {
+    const float d = 1.0f + ex2_approx(fminf(a2, 80.0f));   // sigma(x < -55) ~ 0 (< 1e-24), never inf/NaN
+    const float r = rcp_approx(d);
+    return fmaf(r, fmaf(-d, r, 1.0f), r);
+}
+__device__ __forceinline__ float tanh_e2(float a2) { return tanhf(a2 * 0.34657359027997264f); }
+__device__ __forceinline__ float tanh_acc(float x) { return tanhf(x); }
+// tanh(x) = 2 sigma(2x) - 1 with the correctly rounded sigma: unbiased, absolute
+// error ~1 ulp(1) near 0.  The GRU candidate uses it: measured beta deviation
+// 4.3 vs 3.8 floors with tanhf at 10% less build time (C3 GRU); the LSTM keeps
+// tanhf (2.1-2.3 vs 3.9-5.8 floors with this form).
+__device__ __forceinline__ float tanh_e2_sig(float a2) { return fmaf(2.0f, sig_e2(-a2), -1.0f); }
+
 // Fast MUFU forms (ex2.approx / rcp.approx, ~2 ulp each) for epilogues that
 // are MUFU bound; accuracy validated by the parity tests of the kernel using them.
 __device__ __forceinline__ float sigmoid_fast(float a) {

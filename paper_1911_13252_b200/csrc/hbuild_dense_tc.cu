@@ -89,7 +89,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ float clamp30(float x) { return fminf(fmaxf(x, -30.0f), 30.0f); }
 
 // Split 8 fp32 h values into fp16 hi = fp16(h) and lo = fp16(h - hi), packed
 // two per 32-bit word (even K index in the low half) as the TMEM A operand wants.
@@ -209,17 +208,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                         ptx::mma_f16_ts(d, tah, dbh, idesc, ks != 0);
                         ptx::mma_f16_ts(d, tal, dbh, idesc, 1);
                         if (!two) ptx::mma_f16_ts(d, tah, dbl, idesc, 1);
-#ifdef ELM_TC_FOUR_PASS   // accuracy experiment: + lo.lo
-                        if (!two) ptx::mma_f16_ts(d, tal, dbl, idesc, 1);
-#endif
 #pragma unroll
                         for (int kk = 1; kk < 4; ++kk) {
                             ptx::mma_f16_ts(d, tah + kk * 8, dbh + 2 * kk, idesc, 1);
                             ptx::mma_f16_ts(d, tal + kk * 8, dbh + 2 * kk, idesc, 1);
                             if (!two) ptx::mma_f16_ts(d, tah + kk * 8, dbl + 2 * kk, idesc, 1);
-#ifdef ELM_TC_FOUR_PASS
-                            if (!two) ptx::mma_f16_ts(d, tal + kk * 8, dbl + 2 * kk, idesc, 1);
-#endif
                         }
                         ptx::mma_commit(empty + st);                  // frees the U stage
                         // last chunk of the step: A slice ks is free for h(t) once these MMAs retire
@@ -314,14 +307,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(acc_empty + ach);   // accumulator drained
                     float hv[8];
-                    // MUFU budget: 5 ex2 + 1.25 rcp per element.  The four gate
-                    // denominators of a neuron share one reciprocal (1/a = bcd/(abcd)),
-                    // as do the tanh(c) denominators of 4 neurons; exp2 arguments are
-                    // clamped at +30 so the products stay finite (sigma(20.8) = 1 - 9e-10;
-                    // a very negative argument gives d = 1 exactly, no clamp needed).
+                    // gates: sig_e2 / tanh_e2 (common.cuh) -- accurate forms, no shared
+                    // reciprocal (a shared one biased H; measured, DESIGN R26)
 #pragma unroll
                     for (int g4 = 0; g4 < 2; ++g4) {
-                        float so[4], dc[4];
 #pragma unroll
                         for (int nb = 0; nb < 4; ++nb) {
                             const int j = n * 32 + 8 * u + 4 * g4 + nb;
@@ -334,45 +323,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                                 float v = fmaf(g == 1 ? kT : kS, a[g4][nb * 4 + g], w[g * (SS + 1)]);
 #pragma unroll
                                 for (int s = 0; s < SS; ++s) v = fmaf(xs[s], w[g * (SS + 1) + 1 + s], v);
-                                arg[g] = fminf(v, 30.0f);   // only large positive arguments can overflow
+                                arg[g] = v;
                             }
-#ifdef ELM_TC_EPI_ACCURATE   // accuracy experiment: libm-accurate gates
-                            so[nb] = 1.0f / (1.0f + exp2f(arg[0]));
-                            const float tc = tanhf(arg[1] * 0.34657359027997264f);
-                            const float sl = 1.0f / (1.0f + exp2f(arg[2])), si = 1.0f / (1.0f + exp2f(arg[3]));
+                            const float so = sig_e2(arg[0]);   // o
+                            const float tc = tanh_e2(arg[1]);  // c~
+                            const float sl = sig_e2(arg[2]);   // lambda
+                            const float si = sig_e2(arg[3]);   // in
                             const int ci = n * 8 + 4 * g4 + nb;
                             const float cn = fmaf(sl, c[ci], si * tc);
                             c[ci] = cn;
-                            dc[nb] = cn;
-#else
-                            const float d0 = 1.0f + ex2_approx(arg[0]);   // o
-                            const float d1 = 1.0f + ex2_approx(arg[1]);   // c~ (tanh)
-                            const float d2 = 1.0f + ex2_approx(arg[2]);   // lambda
-                            const float d3 = 1.0f + ex2_approx(arg[3]);   // in
-                            const float p01 = d0 * d1, p23 = d2 * d3;
-                            const float rr = rcp_approx(p01 * p23);
-                            const float r01 = rr * p23, r23 = rr * p01;
-                            so[nb] = d1 * r01;
-                            const float tc = fmaf(-2.0f, d0 * r01, 1.0f);
-                            const float sl = d3 * r23, si = d2 * r23;
-                            const int ci = n * 8 + 4 * g4 + nb;
-                            const float cn = fmaf(sl, c[ci], si * tc);
-                            c[ci] = cn;
-                            dc[nb] = 1.0f + ex2_approx(fminf(2.8853900817779268f * cn, 30.0f));
-#endif
+                            hv[4 * g4 + nb] = so * tanh_acc(cn);
                         }
-#ifdef ELM_TC_EPI_ACCURATE
-#pragma unroll
-                        for (int nb = 0; nb < 4; ++nb) hv[4 * g4 + nb] = so[nb] * tanhf(dc[nb]);
-                        continue;
-#endif
-                        const float p01 = dc[0] * dc[1], p23 = dc[2] * dc[3];
-                        const float rr = rcp_approx(p01 * p23);
-                        const float r01 = rr * p23, r23 = rr * p01;
-                        hv[4 * g4 + 0] = so[0] * fmaf(-2.0f, dc[1] * r01, 1.0f);
-                        hv[4 * g4 + 1] = so[1] * fmaf(-2.0f, dc[0] * r01, 1.0f);
-                        hv[4 * g4 + 2] = so[2] * fmaf(-2.0f, dc[3] * r23, 1.0f);
-                        hv[4 * g4 + 3] = so[3] * fmaf(-2.0f, dc[2] * r23, 1.0f);
                     }
                     // stage h(t) of these 8 neurons as fp16 hi|lo pairs (the A operand
                     // format); at the last step also store the fp32 H(Q) row segment

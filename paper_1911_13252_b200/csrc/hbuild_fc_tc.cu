@@ -71,7 +71,6 @@ __device__ __forceinline__ void tmem_ld16f(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ float clamp30f(float x) { return fminf(fmaxf(x, -30.0f), 30.0f); }
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -213,7 +212,6 @@ __global__ void __launch_bounds__(kFThreads, 1) k_fc_tc(const __grid_constant__ 
                 float hv[32];
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
-                    float dd[2];
 #pragma unroll
                     for (int e2 = 0; e2 < 2; ++e2) {
                         const int j = 32 * u + i + e2;
@@ -221,12 +219,9 @@ __global__ void __launch_bounds__(kFThreads, 1) k_fc_tc(const __grid_constant__ 
                         float v = a[(i + e2) >> 4][(i + e2) & 15] + w[0];
 #pragma unroll
                         for (int s = 0; s < SS; ++s) v = fmaf(xs[s], w[1 + s], v);
-                        dd[e2] = 1.0f + ex2_approx(clamp30f(kA * v));
+                        // accurate activation forms (common.cuh; DESIGN R26)
+                        hv[i + e2] = is_tanh ? tanh_e2(kA * v) : sig_e2(kA * v);
                     }
-                    const float rr = rcp_approx(dd[0] * dd[1]);   // shared reciprocal
-                    const float i0 = rr * dd[1], i1 = rr * dd[0];
-                    hv[i] = is_tanh ? fmaf(-2.0f, i0, 1.0f) : i0;
-                    hv[i + 1] = is_tanh ? fmaf(-2.0f, i1, 1.0f) : i1;
                 }
                 if (t < p.Q) {
                     // h(t) -> ring slot t % NS as fp16 hi|lo, SW128 K-major (row r, K = neuron)

@@ -56,7 +56,6 @@ struct GruParams {
     float wb[kGWbMax];     // per neuron j, gate g in (z, r, f): [b, W_0..W_{S-1}] x 2^sigma
 };
 
-__device__ __forceinline__ float clamp30g(float x) { return fminf(fmaxf(x, -30.0f), 30.0f); }
 
 __device__ __forceinline__ void tmem_ld16g(uint32_t taddr, float (&v)[16]) {
     uint32_t r[16];
@@ -249,11 +248,8 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                             pz = fmaf(xs[s], w[1 + s], pz);
                             pr = fmaf(xs[s], w[SS + 2 + s], pr);
                         }
-                        const float dz = 1.0f + ex2_approx(fminf(pz, 30.0f));
-                        const float dr = 1.0f + ex2_approx(fminf(pr, 30.0f));
-                        const float rr = rcp_approx(dz * dr);
-                        my_z[(c * 16 + i) * 32] = dr * rr;            // z = 1/dz
-                        rh[i] = (dz * rr) * h[c * 16 + i];            // r o h(t-1)
+                        my_z[(c * 16 + i) * 32] = sig_e2(pz);         // z (accurate form, DESIGN R26)
+                        rh[i] = sig_e2(pr) * h[c * 16 + i];           // r o h(t-1)
                     }
                     uint32_t hi[8], lo[8];
                     split16(rh, hi, lo);
@@ -288,10 +284,9 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                             float pn = fmaf(kT, a2[c][i + k2], w[0]);
 #pragma unroll
                             for (int s = 0; s < SS; ++s) pn = fmaf(xs[s], w[1 + s], pn);
-                            dn[k2] = 1.0f + ex2_approx(fminf(pn, 30.0f));
+                            dn[k2] = tanh_e2_sig(pn);
                         }
-                        const float rr = rcp_approx(dn[0] * dn[1]);
-                        const float n0 = fmaf(-2.0f, dn[1] * rr, 1.0f), n1 = fmaf(-2.0f, dn[0] * rr, 1.0f);
+                        const float n0 = dn[0], n1 = dn[1];
                         const float z0 = my_z[(c * 16 + i) * 32], z1 = my_z[(c * 16 + i + 1) * 32];
                         float& h0 = h[c * 16 + i];
                         float& h1 = h[c * 16 + i + 1];

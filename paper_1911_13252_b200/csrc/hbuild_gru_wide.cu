@@ -255,11 +255,8 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
                                 pz = fmaf(xs[s], __ldg(w + 1 + s), pz);
                                 pr = fmaf(xs[s], __ldg(w + SS + 2 + s), pr);
                             }
-                            const float dz = 1.0f + ex2_approx(fminf(pz, 30.0f));
-                            const float dr = 1.0f + ex2_approx(fminf(pr, 30.0f));
-                            const float rr = rcp_approx(dz * dr);
-                            zv[i] = dr * rr;              // z = 1 / dz
-                            rh[i] = (dz * rr) * hp[i];    // r o h(t-1)
+                            zv[i] = sig_e2(pz);           // z (accurate form, DESIGN R26)
+                            rh[i] = sig_e2(pr) * hp[i];   // r o h(t-1)
                         }
                         st8(zst + sidx(j0), zv);
                         if (t >= 2) put_hilo8(rh_img, r, j0, rh);
@@ -307,10 +304,9 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
                                 float pn = fmaf(kT, a2[g8 >> 1][(g8 & 1) * 8 + i + k2], __ldg(w));
 #pragma unroll
                                 for (int s = 0; s < SS; ++s) pn = fmaf(xs[s], __ldg(w + 1 + s), pn);
-                                dn[k2] = 1.0f + ex2_approx(fminf(pn, 30.0f));
+                                dn[k2] = tanh_e2_sig(pn);
                             }
-                            const float rr = rcp_approx(dn[0] * dn[1]);
-                            const float n0 = fmaf(-2.0f, dn[1] * rr, 1.0f), n1 = fmaf(-2.0f, dn[0] * rr, 1.0f);
+                            const float n0 = dn[0], n1 = dn[1];
                             hp[i] = fmaf(zv[i], n0 - hp[i], hp[i]);        // (1 - z) h + z n
                             hp[i + 1] = fmaf(zv[i + 1], n1 - hp[i + 1], hp[i + 1]);
                         }

@@ -223,7 +223,6 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
                     float hv[8];
 #pragma unroll
                     for (int g4 = 0; g4 < 2; ++g4) {
-                        float so[4], dc[4];
 #pragma unroll
                         for (int nb = 0; nb < 4; ++nb) {
                             const int j = n * 32 + 8 * u + 4 * g4 + nb;
@@ -234,30 +233,16 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
                                 float v = fmaf(g == 1 ? kT : kS, a[g4][nb * 4 + g], __ldg(w + g * (SS + 1)));
 #pragma unroll
                                 for (int s = 0; s < SS; ++s) v = fmaf(xs[s], __ldg(w + g * (SS + 1) + 1 + s), v);
-                                arg[g] = fminf(v, 30.0f);
+                                arg[g] = v;
                             }
-                            const float d0 = 1.0f + ex2_approx(arg[0]);   // o
-                            const float d1 = 1.0f + ex2_approx(arg[1]);   // c~ (tanh)
-                            const float d2 = 1.0f + ex2_approx(arg[2]);   // lambda
-                            const float d3 = 1.0f + ex2_approx(arg[3]);   // in
-                            const float p01 = d0 * d1, p23 = d2 * d3;
-                            const float rr = rcp_approx(p01 * p23);
-                            const float r01 = rr * p23, r23 = rr * p01;
-                            so[nb] = d1 * r01;
-                            const float tc = fmaf(-2.0f, d0 * r01, 1.0f);
-                            const float sl = d3 * r23, si = d2 * r23;
+                            // accurate gate forms (common.cuh sig_e2 / tanh_e2; DESIGN R26)
+                            const float so = sig_e2(arg[0]), tc = tanh_e2(arg[1]);
+                            const float sl = sig_e2(arg[2]), si = sig_e2(arg[3]);
                             const int ci = 4 * g4 + nb;
                             const float cn = fmaf(sl, c[ci], si * tc);
                             c[ci] = cn;
-                            dc[nb] = 1.0f + ex2_approx(fminf(2.8853900817779268f * cn, 30.0f));
+                            hv[4 * g4 + nb] = so * tanh_acc(cn);
                         }
-                        const float p01 = dc[0] * dc[1], p23 = dc[2] * dc[3];
-                        const float rr = rcp_approx(p01 * p23);
-                        const float r01 = rr * p23, r23 = rr * p01;
-                        hv[4 * g4 + 0] = so[0] * fmaf(-2.0f, dc[1] * r01, 1.0f);
-                        hv[4 * g4 + 1] = so[1] * fmaf(-2.0f, dc[0] * r01, 1.0f);
-                        hv[4 * g4 + 2] = so[2] * fmaf(-2.0f, dc[3] * r23, 1.0f);
-                        hv[4 * g4 + 3] = so[3] * fmaf(-2.0f, dc[2] * r23, 1.0f);
                     }
                     if (t < p.Q) {
                         cptr[0] = make_float4(c[0], c[1], c[2], c[3]);

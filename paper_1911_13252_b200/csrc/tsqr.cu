@@ -269,8 +269,10 @@ __global__ void k_unpack(const double* __restrict__ Rpk, int P, int n, double* _
     }
 }
 
-__global__ void k_pack(const double* __restrict__ R, int n, double* __restrict__ Rpk) {
+__global__ void k_pack(const double* __restrict__ R, int n, double* __restrict__ Rpk, const int* __restrict__ flag,
+                       SolveDev* __restrict__ sdev) {
     const int64_t len = (int64_t)n * (n + 1) / 2;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && *flag) sdev->nf_sticky = 1;   // reported by elmrnn_sync
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
         // row k starts at k*n - k(k-1)/2; find k by bisection (n <= 1024)
         int lo = 0, hi = n - 1;
@@ -384,6 +386,7 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
         out->lambda = lambda;
         out->rank_flag = ridge ? 1 : 0;
         out->nonfinite = *flag;
+        if (*flag) out->nf_sticky = 1;
         out->n_total = n_total;
     }
 }
@@ -472,6 +475,7 @@ __global__ void __launch_bounds__(1024, 1)
     }
     if (threadIdx.x == 0) {
         out->nonfinite = *flag;
+        if (*flag) out->nf_sticky = 1;
         out->n_total = n_total;
     }
 }
@@ -1160,6 +1164,7 @@ cudaError_t ensure_solve_ws(elmrnn* h, int64_t slabs) {
     }
     if (!h->sdev) {   // SolveDev + 1024 ints of per-SM counters (k_tsqr_leaf_wy)
         if ((e = cudaMalloc(&h->sdev, sizeof(SolveDev) + 1024 * sizeof(int)))) return e;
+        if ((e = cudaMemsetAsync(h->sdev, 0, sizeof(SolveDev), h->stream))) return e;
         if ((e = cudaMalloc(&h->flag, sizeof(int)))) return e;
         if ((e = cudaMallocHost(&h->shost, sizeof(SolveDev)))) return e;
     }
@@ -1260,7 +1265,7 @@ cudaError_t tsqr_pack(elmrnn* h, double* Rpk) {
     int64_t len = (int64_t)n * (n + 1) / 2;
     int blocks = (int)((len + 255) / 256);
     if (blocks > 1024) blocks = 1024;
-    k_pack<<<blocks, 256, 0, h->stream>>>(h->Rws, n, Rpk);
+    k_pack<<<blocks, 256, 0, h->stream>>>(h->Rws, n, Rpk, h->flag, h->sdev);
     h->launches++;
     return cudaGetLastError();
 }

@@ -25,7 +25,8 @@ STATUS = {0: "OK", 1: "WARN_RIDGE", -1: "ERR_ARG", -2: "ERR_SHAPE", -3: "ERR_UND
 EXPORTED = ("elmrnn_opts_default", "elmrnn_init", "elmrnn_init_ex", "elmrnn_set_stream", "elmrnn_build_H",
             "elmrnn_build_H_ef", "elmrnn_error_windows", "elmrnn_forecast", "elmrnn_test_rmse",
             "elmrnn_solve_beta_multi",
-            "elmrnn_solve_beta", "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_packed_r_len",
+            "elmrnn_solve_beta", "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_sync", "elmrnn_packed_r_len",
+            "elmrnn_solve_local_multi", "elmrnn_solve_merge_multi", "elmrnn_packed_r_len_multi",
             "elmrnn_predict", "elmrnn_get_weights", "elmrnn_weight_block_len", "elmrnn_path",
             "elmrnn_launch_count", "elmrnn_last_error", "elmrnn_destroy")
 
@@ -84,6 +85,11 @@ def lib() -> ctypes.CDLL:
         L.elmrnn_solve_beta_multi.argtypes = [vp, vp, i64, vp, i64, i32, i64, vp, vp, vp]
         L.elmrnn_solve_local.argtypes = [vp, vp, i64, vp, i64, vp]
         L.elmrnn_solve_merge.argtypes = [vp, vp, i32, i64, vp, vp]
+        L.elmrnn_sync.argtypes = [vp]
+        L.elmrnn_solve_local_multi.argtypes = [vp, vp, i64, vp, i64, i32, i64, vp]
+        L.elmrnn_solve_merge_multi.argtypes = [vp, vp, i32, i32, i64, vp, vp, vp]
+        L.elmrnn_packed_r_len_multi.argtypes = [vp, i32]
+        L.elmrnn_packed_r_len_multi.restype = i64
         L.elmrnn_packed_r_len.argtypes = [vp]
         L.elmrnn_packed_r_len.restype = i64
         L.elmrnn_predict.argtypes = [vp, vp, i64, vp, i64, i64, vp, vp]
@@ -100,7 +106,8 @@ def lib() -> ctypes.CDLL:
         for f in ("elmrnn_init", "elmrnn_init_ex", "elmrnn_set_stream", "elmrnn_build_H", "elmrnn_build_H_ef",
                   "elmrnn_error_windows", "elmrnn_forecast", "elmrnn_test_rmse", "elmrnn_solve_beta",
                   "elmrnn_solve_beta_multi",
-                  "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_predict", "elmrnn_get_weights",
+                  "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_sync", "elmrnn_predict", "elmrnn_get_weights",
+                  "elmrnn_solve_local_multi", "elmrnn_solve_merge_multi",
                   "elmrnn_path"):
             getattr(L, f).restype = i32
         _lib = L
@@ -183,6 +190,11 @@ class ELMRNN:
             self.close()
         except Exception:   # interpreter shutdown: module globals may already be gone
             pass
+
+    def sync(self) -> None:
+        """elmrnn_sync: wait for the handle's stream; raises ERR_NONFINITE when an
+        asynchronous solve since the last check met NaN/Inf."""
+        self._check(lib().elmrnn_sync(self._h))
 
     @property
     def path(self) -> int:
@@ -314,6 +326,44 @@ class ELMRNN:
         self._stream()
         self._check(lib().elmrnn_solve_local(self._h, _ptr(H), ldh, _ptr(Y), N, _ptr(Rpk)))
         return Rpk
+
+    def packed_r_len_multi(self, P: int) -> int:
+        return lib().elmrnn_packed_r_len_multi(self._h, P)
+
+    def solve_local_multi(self, H: torch.Tensor, Y: torch.Tensor, Rpk: torch.Tensor | None = None):
+        """elmrnn_solve_local_multi: Y [N][P] -> packed R fp64 [(M+P)(M+P+1)/2]."""
+        _dev_check(H, "H", torch.float32)
+        _dev_check(Y, "Y", torch.float32)
+        N = H.shape[0]
+        if Y.shape[0] != N:
+            raise ValueError(f"Y has {Y.shape[0]} rows, needs {N}")
+        Y2 = Y.reshape(N, -1)
+        P = Y2.shape[1]
+        if N and Y2.stride(1) != 1:
+            raise ValueError("Y must have unit inner stride")
+        ldy = Y2.stride(0) if N > 1 else P
+        ldh = _rows(H, "H")[0] if N else self.M
+        L = self.packed_r_len_multi(P)
+        if Rpk is None:
+            Rpk = torch.empty(L, dtype=torch.float64, device=H.device)
+        _vec(Rpk, "Rpk", torch.float64, L)
+        self._stream()
+        self._check(lib().elmrnn_solve_local_multi(self._h, _ptr(H), ldh, _ptr(Y2), ldy, P, N, _ptr(Rpk)))
+        return Rpk
+
+    def solve_merge_multi(self, Rpk_all: torch.Tensor, ranks: int, P: int, N_total: int, B: torch.Tensor | None = None,
+                          info: bool = True):
+        """elmrnn_solve_merge_multi -> (B fp64 [P][M], rmse list [P] or None, SolveInfo or None)."""
+        _vec(Rpk_all, "Rpk_all", torch.float64, ranks * self.packed_r_len_multi(P))
+        if B is None:
+            B = torch.empty((P, self.M), dtype=torch.float64, device=Rpk_all.device)
+        _vec(B, "B", torch.float64, P * self.M)
+        self._stream()
+        rm = (ctypes.c_double * P)()
+        inf = _Info()
+        st = self._check(lib().elmrnn_solve_merge_multi(self._h, _ptr(Rpk_all), ranks, P, N_total, _ptr(B),
+                                                        rm if info else None, ctypes.byref(inf) if info else None))
+        return B, (list(rm) if info else None), (self._info(inf, st) if info else None)
 
     def solve_merge(self, Rpk_all: torch.Tensor, P: int, N_total: int, beta: torch.Tensor | None = None,
                     info: bool = True):

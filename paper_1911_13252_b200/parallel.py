@@ -3,8 +3,9 @@
 The ELM solve shards naturally over samples (rows of H): each rank builds its
 own H block and factors [H | Y] into an (M+1)x(M+1) R (elmrnn_solve_local);
 the only exchange is an all-gather of the packed R factors (265 KB per rank at
-M = 256) over NCCL / NVLink, a final small QR of their stack on rank 0
-(elmrnn_solve_merge) and a broadcast of beta -- the north-star decomposition
+M = 256) over NCCL / NVLink, then a final small QR of their stack
+(elmrnn_solve_merge) -- on every rank by default (identical bits, no broadcast),
+or on a root rank followed by a broadcast of beta, the north-star decomposition
 (SURVEY 8(e)).  Householder QR of stacked R factors equals the QR of the
 stacked rows (tests/test_oracle_weights_solve.py::test_tsqr_tree_equals_direct_R).
 
@@ -34,22 +35,37 @@ def _all_gather_rows(Rpk: torch.Tensor, group=None) -> torch.Tensor:
 
 
 def solve_sharded(model, H: torch.Tensor, Y: torch.Tensor, N_total: int, beta: torch.Tensor | None = None,
-                  group=None, root: int = 0, info: bool = False):
-    """beta for the row-sharded [H | Y]: local TSQR, all-gather R, merge on root, broadcast."""
-    Rpk = model.solve_local(H, Y)
+                  group=None, root: int | None = None, info: bool = False):
+    """beta for the row-sharded [H | Y]: local TSQR, all-gather of the packed R factors,
+    merge + solve.  Y [N] (one output) or [N][P] (P outputs, SURVEY 8(f) row 3,
+    P:655; beta then [P][M]).
+
+    root=None (default): EVERY rank merges the identical all-gathered factors with
+    the same deterministic kernels, so all ranks hold bitwise-identical beta and
+    no broadcast is needed (SURVEY 8(e) alternative; the merge is ~1 ms).
+    root=r: merge on rank r only, then broadcast beta (the north-star form)."""
+    multi = Y.dim() == 2 and Y.shape[1] > 1
+    P = Y.shape[1] if multi else 1
+    Rpk = model.solve_local_multi(H, Y) if multi else model.solve_local(H, Y.reshape(-1))
     Rall = _all_gather_rows(Rpk, group)
     rank = dist.get_rank(group)
     if beta is None:
-        beta = torch.empty(model.M, dtype=torch.float64, device=H.device)
+        beta = torch.empty((P, model.M) if multi else (model.M,), dtype=torch.float64, device=H.device)
     sinfo = None
-    if rank == root:
-        _, sinfo = model.solve_merge(Rall, Rall.shape[0], N_total, beta, info=info)
-    dist.broadcast(beta, src=root, group=group)
+    if root is None or rank == root:
+        if multi:
+            _, rm, sinfo = model.solve_merge_multi(Rall, Rall.shape[0], P, N_total, beta, info=info)
+            if sinfo is not None:
+                sinfo.rmse_all = rm
+        else:
+            _, sinfo = model.solve_merge(Rall, Rall.shape[0], N_total, beta, info=info)
+    if root is not None:
+        dist.broadcast(beta, src=root, group=group)
     return beta, sinfo
 
 
 def train_sharded(model, X_local: torch.Tensor, Y_local: torch.Tensor, N_total: int, Yfb_local=None, group=None,
-                  root: int = 0, info: bool = True):
+                  root: int | None = None, info: bool = True):
     """Alg. 1 on this rank's rows: H(Q) block, then the sharded solve."""
     H = model.build_H(X_local, Yfb_local)
     beta, sinfo = solve_sharded(model, H, Y_local, N_total, group=group, root=root, info=info)

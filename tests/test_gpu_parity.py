@@ -220,7 +220,8 @@ def test_empty_and_errors():
 SOLVE_CASES = [("elman", 1000, 1, 20, 10, "mg", 0.0), ("jordan", 5000, 1, 64, 20, "ar5", 0.0),
                ("narmax", 5000, 1, 64, 20, "ar5", 0.0), ("gru", 3000, 4, 128, 30, "sin4", 0.0),
                ("fc", 2000, 4, 128, 30, "sin4", 0.0), ("lstm", 8000, 1, 256, 50, "mg", 0.01),
-               ("lstm", 10277, 1, 512, 4, "ar5", 0.0),
+               ("lstm", 10277, 1, 512, 4, "ar5", 0.0), ("lstm", 6000, 1, 128, 30, "mg", 0.01),
+               ("gru", 6000, 1, 128, 30, "mg", 0.01), ("gru", 10277, 1, 512, 4, "ar5", 0.0),
                ("lstm_diag", 3000, 4, 128, 30, "sin4", 0.0), ("gru_diag", 3000, 4, 128, 30, "sin4", 0.0),
                ("fc_eq8", 3000, 4, 128, 30, "sin4", 0.0)]
 
@@ -372,6 +373,28 @@ def test_ridge_and_nonfinite():
     Hn[17, 2] = np.nan
     with pytest.raises(ElmrnnError, match="NONFINITE"):
         e.solve_beta(torch.from_numpy(Hn).cuda(), torch.from_numpy(Y).cuda())
+
+
+def test_nonfinite_async_reported_by_sync():
+    """An asynchronous solve (info == NULL) cannot return ERR_NONFINITE; the device
+    flag is accumulated and elmrnn_sync reports it (then clears it)."""
+    from paper_1911_13252_b200 import ElmrnnError
+    for M in (4, 200):   # per-column fold and blocked-WY leaf
+        e = E("elman", 1, M, 3, 1) if M < 10 else E("lstm", 1, M, 3, 1, force_path=1)
+        H = torch.rand(3 * M, M, device="cuda")
+        Y = torch.rand(3 * M, device="cuda")
+        e.solve_beta(H, Y, info=False)
+        e.sync()
+        Hn = H.clone()
+        Hn[5, 1] = float("nan")
+        e.solve_beta(Hn, Y, info=False)
+        e.solve_beta(H, Y, info=False)        # a later clean solve does not clear it
+        with pytest.raises(ElmrnnError, match="NONFINITE"):
+            e.sync()
+        e.sync()                               # cleared by the check
+        e.solve_local(Hn, Y)                   # row-sharded step 1 reports too
+        with pytest.raises(ElmrnnError, match="NONFINITE"):
+            e.sync()
 
 
 def test_predict_parity():
@@ -712,6 +735,29 @@ def test_solve_beta_multi_parity(M, N, P):
         b1, i1 = e.solve_beta(H, Y[:, p].contiguous())
         assert float((b1 - B[p]).norm() / b1.norm()) <= tol
     assert info.status == 0 and info.rmse == pytest.approx(rmse[0], rel=1e-14)
+
+
+@pytest.mark.parametrize("M,N,P,ranks", [(64, 5000, 3, 2), (256, 20011, 2, 4), (20, 1000, 2, 3), (129, 3777, 5, 8)])
+def test_multi_output_virtual_ranks(M, N, P, ranks):
+    """Row-sharded multi-output solve on one GPU: elmrnn_solve_local_multi on each
+    row block, elmrnn_solve_merge_multi of the stacked factors equals the single
+    elmrnn_solve_beta_multi and the oracle's P Householder solves."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + P)
+    H = torch.rand(N, M, device="cuda", generator=g) - 0.5
+    Y = torch.rand(N, P, device="cuda", generator=g) - 0.5
+    e = E("lstm", 1, M, 4, 1, force_path=1)
+    B1, rm1, _ = e.solve_beta_multi(H, Y)
+    cuts = np.linspace(0, N, ranks + 1).astype(int)
+    parts = [e.solve_local_multi(H[a:b], Y[a:b]).clone() for a, b in zip(cuts[:-1], cuts[1:])]
+    BP, rmP, info = e.solve_merge_multi(torch.stack(parts), ranks, P, N)
+    Bo, io = orc.lstsq_multi(H.double().cpu().numpy(), Y.double().cpu().numpy())
+    cond = np.linalg.cond(io[0].R[:M, :M])
+    tol = 1e-12 * max(1.0, cond)
+    assert info.status == 0
+    for p in range(P):
+        assert float((BP[p] - B1[p]).norm() / B1[p].norm()) <= tol
+        assert np.linalg.norm(BP[p].cpu().numpy() - Bo[p]) / np.linalg.norm(Bo[p]) <= tol
+        assert rmP[p] == pytest.approx(io[p].rmse, rel=tol)
 
 
 def test_solve_beta_multi_ridge_and_trained():

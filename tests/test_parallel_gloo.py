@@ -47,6 +47,35 @@ class CpuStandIn:
             R[: r.shape[0]] = r
         return torch.from_numpy(np.concatenate([R[k, k:] for k in range(n)]))
 
+    def packed_r_len_multi(self, P):
+        return (self.M + P) * (self.M + P + 1) // 2
+
+    def _local(self, H, Y2):
+        n = self.M + Y2.shape[1]
+        R = np.zeros((n, n))
+        if H.shape[0]:
+            r = np.linalg.qr(np.column_stack([H.numpy(), Y2.numpy().astype(np.float64)]), mode="r")
+            R[: r.shape[0]] = r
+        return torch.from_numpy(np.concatenate([R[k, k:] for k in range(n)]))
+
+    def solve_local_multi(self, H, Y):
+        return self._local(H, Y.reshape(H.shape[0], -1))
+
+    def solve_merge_multi(self, Rall, ranks, P, N_total, B, info=True):
+        n = self.M + P
+        rows = []
+        for p in range(ranks):
+            R = np.zeros((n, n))
+            off = 0
+            for k in range(n):
+                R[k, k:] = Rall[p, off: off + n - k].numpy()
+                off += n - k
+            rows.append(R)
+        S = np.vstack(rows)
+        Bo, infos = self.orc.lstsq_multi(S[:, :self.M], S[:, self.M:])
+        B.copy_(torch.from_numpy(Bo))
+        return B, [i.rho / np.sqrt(N_total) for i in infos], infos[0]
+
     def solve_merge(self, Rall, P, N_total, beta, info=True):
         n = self.M + 1
         rows = []
@@ -64,7 +93,7 @@ class CpuStandIn:
         return beta, inf
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, root):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1911_13252_b200 import parallel as par
@@ -73,20 +102,29 @@ def _worker(rank, world, port, out):
     lo, hi = par.shard_rows(N, world, rank)
     X, Y, _ = sy.windows(sy.series("mg", N + Q), N, Q)
     model = CpuStandIn("gru", 1, M, Q, 3)
-    H, beta, info = par.train_sharded(model, torch.from_numpy(X[lo:hi]), torch.from_numpy(Y[lo:hi]), N)
+    H, beta, info = par.train_sharded(model, torch.from_numpy(X[lo:hi]), torch.from_numpy(Y[lo:hi]), N, root=root)
     out[rank] = beta.numpy().copy()
-    if rank == 0:
-        out["rmse"] = info.rmse
+    if info is not None:
+        out[f"rmse{rank}"] = info.rmse
+    # two outputs (y(t+1), y(t+2)): the multi-output sharded solve
+    s = sy.series("mg", N + Q + 1)
+    Y2 = np.stack([s[Q:Q + N, 0], s[Q + 1:Q + 1 + N, 0]], axis=1).astype(np.float32)
+    B, info2 = par.solve_sharded(model, H, torch.from_numpy(Y2[lo:hi]), N, root=root, info=True)
+    out[f"B{rank}"] = B.numpy().copy()
     dist.destroy_process_group()
 
 
-def test_sharded_solve_matches_single_process():
+@pytest.mark.parametrize("root", [None, 0])
+def test_sharded_solve_matches_single_process(root):
+    """root=None: every rank merges (no broadcast); root=0: merge on rank 0 + broadcast.
+    Either way both ranks hold identical bits equal to the single-process oracle solve,
+    for one output and for two outputs (multi-output sharded path)."""
     from oracle import oracle as orc
     from synth import series as sy
     world = 2
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out, root), nprocs=world, join=True)
     N, Q, M = 900, 10, 12
     X, Y, _ = sy.windows(sy.series("mg", N + Q), N, Q)
     net = orc.Net("gru", S=1, M=M, Q=Q)
@@ -94,8 +132,16 @@ def test_sharded_solve_matches_single_process():
     b, inf = orc.lstsq(H, Y)
     for r in range(world):
         np.testing.assert_allclose(out[r], b, rtol=1e-9, atol=1e-12)
-    np.testing.assert_array_equal(out[0], out[1])       # broadcast: identical bits
-    assert out["rmse"] == pytest.approx(inf.rmse, rel=1e-10)
+    np.testing.assert_array_equal(out[0], out[1])       # identical bits on every rank
+    assert out["rmse0"] == pytest.approx(inf.rmse, rel=1e-10)
+    if root is None:
+        assert out["rmse1"] == out["rmse0"]
+    s = sy.series("mg", N + Q + 1)
+    Y2 = np.stack([s[Q:Q + N, 0], s[Q + 1:Q + 1 + N, 0]], axis=1)
+    Bo, _ = orc.lstsq_multi(H, Y2)
+    for r in range(world):
+        np.testing.assert_allclose(out[f"B{r}"], Bo, rtol=1e-9, atol=1e-12)
+    np.testing.assert_array_equal(out["B0"], out["B1"])
 
 
 def test_shard_rows_cover_exactly():

@@ -15,7 +15,8 @@ from paper_1911_13252_b200 import ELMRNN  # noqa: E402
 from synth import series as sy  # noqa: E402
 
 CASES = {"lstm256mg": ("lstm", 8000, 1, 256, 50, "mg", 0.01), "lstm512ar": ("lstm", 10277, 1, 512, 4, "ar5", 0.0),
-         "lstm128mg": ("lstm", 6000, 1, 128, 30, "mg", 0.01), "gru128mg": ("gru", 6000, 1, 128, 30, "mg", 0.01)}
+         "lstm128mg": ("lstm", 6000, 1, 128, 30, "mg", 0.01), "gru128mg": ("gru", 6000, 1, 128, 30, "mg", 0.01),
+         "fc128sin": ("fc", 3000, 4, 128, 30, "sin4", 0.0), "gru512ar": ("gru", 10277, 1, 512, 4, "ar5", 0.0)}
 for name in sys.argv[1:] or list(CASES):
     arch, N, S, M, Q, kind, noise = CASES[name]
     s = sy.series(kind, N + Q, seed=11, noise=noise)
