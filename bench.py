@@ -49,6 +49,10 @@ WORKLOAD_NAMES = {
     "C5lstm1024": "C5 LSTM M=1024 Q=10 d=1, one GPU's share (N=2M of 16M), Mackey-Glass + noise",
     "C5gru1024": "C5 GRU M=1024 Q=10 d=1, one GPU's share (N=2M of 16M), Mackey-Glass + noise",
 }
+for _k, _c in sy.CONFIGS.items():
+    if _k not in WORKLOAD_NAMES:
+        WORKLOAD_NAMES[_k] = (f"C5 {_c['arch'].upper()} M={_c['M']} Q={_c['Q']} d=1, one GPU's share "
+                              f"(N=2M of 16M), Mackey-Glass + noise")
 
 
 def algorithmic_flops_per_sample(arch: str, S: int, M: int, Q: int) -> float:

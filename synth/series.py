@@ -135,6 +135,12 @@ CONFIGS = {
     "C5lstm1024": dict(arch="lstm", series="mg", N=2_000_000, Q=10, S=1, M=1024, noise=0.01),
     "C5gru1024": dict(arch="gru", series="mg", N=2_000_000, Q=10, S=1, M=1024, noise=0.01),
 }
+# The full C5 sweep (BASELINE configs[4]): LSTM/GRU x M in {32, 128, 512, 1024} x Q in
+# {10, 50, 100}, one GPU's share of N = 16M over 8 GPUs (2M rows): "C5{arch}{M}q{Q}".
+for _a in ("lstm", "gru"):
+    for _m in (32, 128, 512, 1024):
+        for _q in (10, 50, 100):
+            CONFIGS[f"C5{_a}{_m}q{_q}"] = dict(arch=_a, series="mg", N=2_000_000, Q=_q, S=1, M=_m, noise=0.01)
 
 
 def config_inputs(name: str, N: int | None = None, seed: int = DATA_SEED):
