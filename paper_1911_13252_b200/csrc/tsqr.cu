@@ -921,8 +921,11 @@ __device__ __forceinline__ int wy_panel_warp(int* sm_slot, int mode) {
     return pw_s;
 }
 
-template <int ROWS>
-__global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
+// NW = 4 warps (n <= 320): 3 CTAs of 32-row tiles share an SM, so the register
+// cap is 65536 / 384 = 168 (the 2-CTA bound of 128 spilled the panel warp's R
+// prefetch to local memory right behind its load: measured, profiles/r02).
+template <int ROWS, int NW>
+__global__ void __launch_bounds__(32 * NW, (NW == 4 && ROWS <= 32) ? 3 : 1)
     k_tsqr_leaf_wy(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t ldy, int P,
                    int64_t N, int M, double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag,
                    int* sm_slot, int la_wait, int pw_mode) {
@@ -991,8 +994,8 @@ __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
     if (bad) atomicOr(flag, 1);
 }
 
-template <int ROWS>
-__global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1) k_tsqr_merge_wy(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n) {
+template <int ROWS, int NW>
+__global__ void __launch_bounds__(32 * NW, (NW == 4 && ROWS <= 32) ? 3 : 1) k_tsqr_merge_wy(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n) {
     extern __shared__ __align__(16) double wsm[];
     const int64_t c = (int64_t)blockIdx.x * 2 * stride, partner = c + stride;
     if (partner >= slabs) return;
@@ -1021,8 +1024,8 @@ __global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1) k_tsqr_merge_wy(doubl
 // apart) instead of for the whole previous chunk.  All CTAs of the grid must be
 // co-resident: launched cooperatively.  prog: [pairs][kMaxChunks] zeroed ints.
 constexpr int kMaxChunks = 128;
-template <int ROWS>
-__global__ void __launch_bounds__(256, ROWS <= 32 ? 2 : 1)
+template <int ROWS, int NW>
+__global__ void __launch_bounds__(32 * NW, (NW == 4 && ROWS <= 32) ? 3 : 1)
     k_tsqr_merge_wy_par(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n, int P, int* prog) {
     extern __shared__ __align__(16) double wsm[];
     const int64_t m = blockIdx.x / P;
@@ -1097,37 +1100,43 @@ static int wy_rows(const elmrnn* h, int n) {
 }
 // Leaf dynamic shared memory: the tile + coefficients.
 static size_t wy_leaf_smem(int rows, int n) { return std::min(wy_smem_bytes(rows, n), (size_t)227 * 1024); }
-static int wy_threads(int n) { return 32 * (n <= 320 ? 4 : std::min(8, ((n + 1) / 2 + 31) / 32)); }
+static int wy_nw(int n) { return n <= 320 ? 4 : 8; }
+static int wy_threads(int n) { return 32 * wy_nw(n); }
+template <int RW, class F>
+static auto wy_nw_dispatch(int n, F& f) {
+    if (wy_nw(n) == 4) return f(std::integral_constant<int, RW>{}, std::integral_constant<int, 4>{});
+    return f(std::integral_constant<int, RW>{}, std::integral_constant<int, 8>{});
+}
 template <class F>
 static auto wy_dispatch(const elmrnn* h, int n, F&& f) {
     switch (wy_rows(h, n)) {
-    case 96: return f(std::integral_constant<int, 96>{});
-    case 64: return f(std::integral_constant<int, 64>{});
-    case 32: return f(std::integral_constant<int, 32>{});
-    case 24: return f(std::integral_constant<int, 24>{});
-    case 8: return f(std::integral_constant<int, 8>{});
-    default: return f(std::integral_constant<int, 16>{});
+    case 96: return wy_nw_dispatch<96>(n, f);
+    case 64: return wy_nw_dispatch<64>(n, f);
+    case 32: return wy_nw_dispatch<32>(n, f);
+    case 24: return wy_nw_dispatch<24>(n, f);
+    case 8: return wy_nw_dispatch<8>(n, f);
+    default: return wy_nw_dispatch<16>(n, f);
     }
 }
 
 template <class F>
 static auto wy_dispatch_merge(int n, F&& f) {
-    if (wy_smem_bytes(96, n) <= 220 * 1024) return f(std::integral_constant<int, 96>{});
-    if (wy_smem_bytes(64, n) <= 220 * 1024) return f(std::integral_constant<int, 64>{});
-    if (wy_smem_bytes(32, n) <= 220 * 1024) return f(std::integral_constant<int, 32>{});
-    return f(std::integral_constant<int, 16>{});
+    if (wy_smem_bytes(96, n) <= 220 * 1024) return wy_nw_dispatch<96>(n, f);
+    if (wy_smem_bytes(64, n) <= 220 * 1024) return wy_nw_dispatch<64>(n, f);
+    if (wy_smem_bytes(32, n) <= 220 * 1024) return wy_nw_dispatch<32>(n, f);
+    return wy_nw_dispatch<16>(n, f);
 }
 
 int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
     const int n = h->M + h->nrhs;
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
-    int per_sm = use_wy_h(h) ? wy_dispatch(h, n, [&](auto rows) {
-        constexpr int RW = decltype(rows)::value;
+    int per_sm = use_wy_h(h) ? wy_dispatch(h, n, [&](auto rows, auto nwc) {
+        constexpr int RW = decltype(rows)::value, NW = decltype(nwc)::value;
         const size_t sm = wy_leaf_smem(RW, n);
-        cudaFuncSetAttribute(k_tsqr_leaf_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_tsqr_leaf_wy<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         int ps = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_tsqr_leaf_wy<RW>, wy_threads(n), sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_tsqr_leaf_wy<RW, NW>, wy_threads(n), sm);
         return ps < 1 ? 1 : ps;
     }) : dispatch(v, [&](auto tr, auto p) {
         int ps = 0;
@@ -1182,13 +1191,13 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
         // SMs a level leaves idle pipeline each pair's row chunks
         // (k_tsqr_merge_wy_par)
         const bool par_ok = true;
-        return wy_dispatch_merge(n, [&](auto rows) {
-            constexpr int RW = decltype(rows)::value;
+        return wy_dispatch_merge(n, [&](auto rows, auto nwc) {
+            constexpr int RW = decltype(rows)::value, NW = decltype(nwc)::value;
             const size_t sm = wy_smem_bytes(RW, n);
-            cudaFuncSetAttribute(k_tsqr_merge_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            cudaFuncSetAttribute(k_tsqr_merge_wy_par<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            cudaFuncSetAttribute(k_tsqr_merge_wy<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            cudaFuncSetAttribute(k_tsqr_merge_wy_par<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             int occ = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tsqr_merge_wy_par<RW>, wy_threads(n), sm);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tsqr_merge_wy_par<RW, NW>, wy_threads(n), sm);
             const int64_t resident = (int64_t)occ * h->sm_count;
             const int nch = (n + RW - 1) / RW;
             for (int64_t stride = 1; stride < slabs && stride < max_stride; stride *= 2) {
@@ -1202,11 +1211,11 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
                     int nn = n;
                     int* pg = h->prog;
                     void* args[] = {&rws, &sl, &sd, &nn, &P, &pg};
-                    e = cudaLaunchCooperativeKernel((const void*)k_tsqr_merge_wy_par<RW>, dim3((unsigned)(pairs * P)),
+                    e = cudaLaunchCooperativeKernel((const void*)k_tsqr_merge_wy_par<RW, NW>, dim3((unsigned)(pairs * P)),
                                                     dim3(wy_threads(n)), args, sm, h->stream);
                     if (e) return e;
                 } else {
-                    k_tsqr_merge_wy<RW><<<(unsigned)pairs, wy_threads(n), sm, h->stream>>>(h->Rws, slabs, stride, n);
+                    k_tsqr_merge_wy<RW, NW><<<(unsigned)pairs, wy_threads(n), sm, h->stream>>>(h->Rws, slabs, stride, n);
                 }
                 h->launches++;
             }
@@ -1236,13 +1245,13 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
     rows = (rows + rows_tile - 1) / rows_tile * rows_tile;
     const int threads = var_threads(v, n);
     if (use_wy_h(h)) {
-        e = wy_dispatch(h, n, [&](auto rws) {
-            constexpr int RW = decltype(rws)::value;
+        e = wy_dispatch(h, n, [&](auto rws, auto nwc) {
+            constexpr int RW = decltype(rws)::value, NW = decltype(nwc)::value;
             const size_t sm = wy_leaf_smem(RW, n);
-            cudaFuncSetAttribute(k_tsqr_leaf_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            cudaFuncSetAttribute(k_tsqr_leaf_wy<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             int* slot = reinterpret_cast<int*>(h->sdev + 1);   // per-SM arrival counters (ensure_solve_ws)
             cudaMemsetAsync(slot, 0, 1024 * sizeof(int), h->stream);
-            k_tsqr_leaf_wy<RW><<<(unsigned)slabs, wy_threads(n), sm, h->stream>>>(
+            k_tsqr_leaf_wy<RW, NW><<<(unsigned)slabs, wy_threads(n), sm, h->stream>>>(
                 H, ldh, Y, ldy, h->nrhs, N, h->M, h->Rws, rows, h->flag, slot, wy_la_wait(n), h->tune.pw_mode);
             h->launches++;
             return cudaGetLastError();
@@ -1293,11 +1302,11 @@ cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta) {
         const size_t zsm = ((n + 1) & ~1) * sizeof(double);
         k_solve_wide_prep<<<1, 1024, zsm, h->stream>>>(h->Rws, h->Rws + (size_t)n * n, Rorig, h->M, n, h->sdev);
         h->launches++;
-        cudaError_t e = wy_dispatch_merge(n, [&](auto rows) {
-            constexpr int RW = decltype(rows)::value;
+        cudaError_t e = wy_dispatch_merge(n, [&](auto rows, auto nwc) {
+            constexpr int RW = decltype(rows)::value, NW = decltype(nwc)::value;
             const size_t sm = wy_smem_bytes(RW, n);
-            cudaFuncSetAttribute(k_tsqr_merge_wy<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k_tsqr_merge_wy<RW><<<1, wy_threads(n), sm, h->stream>>>(h->Rws, 2, 1, n);
+            cudaFuncSetAttribute(k_tsqr_merge_wy<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_tsqr_merge_wy<RW, NW><<<1, wy_threads(n), sm, h->stream>>>(h->Rws, 2, 1, n);
             h->launches++;
             return cudaGetLastError();
         });
