@@ -545,83 +545,92 @@ __device__ __forceinline__ double rcp_nr(double d) {
     return fma(r, e, r);
 }
 
+// fp64 warp shuffles as two explicit 32-bit halves (the generic double
+// shuffle made ptxas land the halves swapped and fix them with three dependent
+// LOP3 XORs per value -- on the panel's critical path; profiles/r02).
+__device__ __forceinline__ double shfl_idx_d(double v, int src) {
+    const int lo = __shfl_sync(0xffffffffu, __double2loint(v), src);
+    const int hi = __shfl_sync(0xffffffffu, __double2hiint(v), src);
+    return __hiloint2double(hi, lo);
+}
+__device__ __forceinline__ double shfl_xor_d(double v, int m) {
+    const int lo = __shfl_xor_sync(0xffffffffu, __double2loint(v), m);
+    const int hi = __shfl_xor_sync(0xffffffffu, __double2hiint(v), m);
+    return __hiloint2double(hi, lo);
+}
+
 // Panel factorisation by one warp.  Lane = (row group rg, column pair cp):
 // rows rg, rg+4, ... of panel columns 2cp, 2cp+1 in registers.  Per column i
 // the critical path is ONE shuffle round (v = column i from its owner lanes)
 // and ONE 2-level butterfly that reduces |v|^2 and both dot products v^T a
 // together; every lane then forms the reflector itself from identical bits
-// (commutative butterfly sums), so g, u0 and beta need no broadcast.
+// (commutative butterfly sums), so g, u0 and beta need no broadcast.  Columns
+// are processed in pairs with the parity a compile-time constant (no per-column
+// register selects), and the per-column stores (Gram entries, R row, the
+// coefficients) are predicated, off the dependency chain.
 template <int ROWS>
 __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, int nbp, double* Rd, double* cgv,
                                       double* cuv, double* Gp) {
     constexpr int RPL = ROWS / 4;   // rows per lane: rows rg, rg+4, ... (interleaved: no bank conflicts)
     const int lane = threadIdx.x & 31, rg = lane >> 3, cp = lane & 7;
     const int c0 = 2 * cp, c1 = c0 + 1;
-    double a0[RPL], a1[RPL];
+    double a[2][RPL];
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
         const double* row = C + (size_t)(rg + 4 * r) * LDC + p;
-        a0[r] = c0 < nbp ? row[c0] : 0.0;
-        a1[r] = c1 < nbp ? row[c1] : 0.0;
+        a[0][r] = c0 < nbp ? row[c0] : 0.0;
+        a[1][r] = c1 < nbp ? row[c1] : 0.0;
     }
     // Gram matrix G = striu(V^T V) of this panel for the trailing update: zero here,
-    // strict-upper entries filled below from the butterfly sums (see w0 / w1)
+    // strict-upper entries filled below from the butterfly sums (see w[0] / w[1])
 #pragma unroll
     for (int t = 0; t < kNBW * kNBW / 32; ++t) Gp[lane + 32 * t] = 0.0;
+    __syncwarp();
+    double* const g_row0 = Gp + c0 * kNBW;   // G[c0][.], G[c1][.] = g_row0[kNBW + .]
+    double* const rd_c = Rd + c0;            // R[i][c0] = rd_c[i * kNBW], R[i][c1] = rd_c[i * kNBW + 1]
     // R entries of row i are read one column ahead: row i+1 is untouched until reflector i+1
-    double x0n = Rd[0], rd0n = Rd[c0], rd1n = Rd[c1];
-    double my_g = 0.0, my_u0 = 0.0, my_beta = 0.0;
-    // two columns per loop body (the column parity selects a0 / a1 at compile
-    // time); a full 16-column unroll overflows the instruction cache
-#ifndef ELM_PANEL_UNROLL
-#define ELM_PANEL_UNROLL 2
-#endif
-#define ELM_PRAGMA_(x) _Pragma(#x)
-#define ELM_UNROLL_(n) ELM_PRAGMA_(unroll n)
-    ELM_UNROLL_(ELM_PANEL_UNROLL)
-    for (int i = 0; i < kNBW; ++i) {
-        if (i >= nbp) break;
-        constexpr unsigned F = 0xffffffffu;
-        const int src = (lane & 24) | (i >> 1);   // owner lane of column i with this lane's rows
-        const double x0 = x0n, rd0 = rd0n, rd1 = rd1n;
+    double x0n = Rd[0], rdn[2] = {rd_c[0], rd_c[1]};
+
+    auto step = [&](auto par, const int i) {
+        constexpr int PAR = decltype(par)::value;   // column i = 2 * (i >> 1) + PAR
+        const int src = (lane & 24) | (i >> 1);     // owner lane of column i with this lane's rows
+        const double x0 = x0n, rd0 = rdn[0], rd1 = rdn[1];
         if (i + 1 < kNBW) {
-            x0n = Rd[(i + 1) * kNBW + i + 1];
-            rd0n = Rd[(i + 1) * kNBW + c0];
-            rd1n = Rd[(i + 1) * kNBW + c1];
+            x0n = Rd[(i + 1) * (kNBW + 1)];
+            rdn[0] = rd_c[(i + 1) * kNBW];
+            rdn[1] = rd_c[(i + 1) * kNBW + 1];
         }
         double v[RPL];
 #pragma unroll
-        for (int r = 0; r < RPL; ++r) v[r] = __shfl_sync(F, (i & 1) ? a1[r] : a0[r], src);
+        for (int r = 0; r < RPL; ++r) v[r] = shfl_idx_d(a[PAR][r], src);
         double s2a = 0.0, s2b = 0.0, w0 = 0.0, w0b = 0.0, w1 = 0.0, w1b = 0.0;
 #pragma unroll
         for (int r = 0; r < RPL; r += 2) {
             s2a = fma(v[r], v[r], s2a);
             s2b = fma(v[r + 1], v[r + 1], s2b);
-            w0 = fma(v[r], a0[r], w0);
-            w0b = fma(v[r + 1], a0[r + 1], w0b);
-            w1 = fma(v[r], a1[r], w1);
-            w1b = fma(v[r + 1], a1[r + 1], w1b);
+            w0 = fma(v[r], a[0][r], w0);
+            w0b = fma(v[r + 1], a[0][r + 1], w0b);
+            w1 = fma(v[r], a[1][r], w1);
+            w1b = fma(v[r + 1], a[1][r + 1], w1b);
         }
         double s2 = s2a + s2b;
         w0 += w0b;
         w1 += w1b;
-        s2 += __shfl_xor_sync(F, s2, 8);
-        w0 += __shfl_xor_sync(F, w0, 8);
-        w1 += __shfl_xor_sync(F, w1, 8);
-        s2 += __shfl_xor_sync(F, s2, 16);
-        w0 += __shfl_xor_sync(F, w0, 16);
-        w1 += __shfl_xor_sync(F, w1, 16);
+        s2 += shfl_xor_d(s2, 8);
+        w0 += shfl_xor_d(w0, 8);
+        w1 += shfl_xor_d(w1, 8);
+        s2 += shfl_xor_d(s2, 16);
+        w0 += shfl_xor_d(w0, 16);
+        w1 += shfl_xor_d(w1, 16);
         // columns c < i hold their final reflector vectors, so w = v_c . v_i = G[c][i]
-        if (rg == 0) {
-            if (c0 < i) Gp[c0 * kNBW + i] = w0;
-            if (c1 < i) Gp[c1 * kNBW + i] = w1;
-        }
+        if (rg == 0 && c0 < i) g_row0[i] = w0;
+        if (rg == 0 && c1 < i) g_row0[kNBW + i] = w1;
         // ---- reflector of panel column i (make_reflector semantics): s2 == 0 or
         // t <= 1e-280 is H = I (|beta u0| lies in [t, 2t]); testing t also keeps a
         // subnormal t away from rsqrt.approx.ftz, which would flush it to 0 (NaN
-        // reflector) -- it occurs in deep noise cascades of rank-deficient partial R
-        // branch-free (every lane takes the same path anyway): evaluate on a safe t,
-        // then select H = I
+        // reflector) -- it occurs in deep noise cascades of rank-deficient partial R.
+        // Branch-free (every lane takes the same path): evaluate on a safe t, then
+        // select H = I.
         const double t = fma(x0, x0, s2);
         const bool refl_ok = s2 != 0.0 && t > 1e-280;
         const double ts = refl_ok ? t : 1.0;
@@ -630,41 +639,36 @@ __device__ __noinline__ void wy_panel(double* __restrict__ C, int LDC, int p, in
         const double uu = x0 - bt;
         const bool app = refl_ok && fabs(bt * uu) > 1e-280;
         const double gg = -rs * rs * rcp_nr(1.0 + fabs(x0) * rs);   // = 1 / (beta u0)
-        const double g = app ? gg : 0.0, u0 = app ? uu : 0.0, beta = app ? bt : 0.0;
-        // column i's coefficients are kept by lane i and stored after the loop
-        // (no divergent store branch on the per-column chain)
-        if (lane == i) {
-            my_g = g;
-            my_u0 = u0;
-            my_beta = beta;
+        const double g = app ? gg : 0.0, u0 = app ? uu : 0.0;
+        if (lane == 0) {   // coefficients and R_ii (off the chain: nothing reads them in this panel)
+            cgv[i] = g;
+            cuv[i] = u0;
+            if (app) Rd[i * (kNBW + 1)] = bt;
         }
-        {   // ---- apply H_i to the panel columns right of i: W_j = u0 R[i][j] + v^T a_j
-            // (unconditionally: f = 0 when H_i = I or the column is not right of i)
-            const bool l0 = c0 > i && c0 < nbp, l1 = c1 > i && c1 < nbp;
-            const double f0 = l0 ? g * fma(u0, rd0, w0) : 0.0;
-            const double f1 = l1 ? g * fma(u0, rd1, w1) : 0.0;
+        // ---- apply H_i to the panel columns right of i: W_j = u0 R[i][j] + v^T a_j
+        // (unconditionally: f = 0 when H_i = I or the column is not right of i)
+        const bool l0 = c0 > i && c0 < nbp, l1 = c1 > i && c1 < nbp;
+        const double f0 = l0 ? g * fma(u0, rd0, w0) : 0.0;
+        const double f1 = l1 ? g * fma(u0, rd1, w1) : 0.0;
 #pragma unroll
-            for (int r = 0; r < RPL; ++r) {
-                a0[r] = fma(f0, v[r], a0[r]);
-                a1[r] = fma(f1, v[r], a1[r]);
-            }
-            if (rg == 0 && g != 0.0) {
-                if (l0) Rd[i * kNBW + c0] = fma(f0, u0, rd0);
-                if (l1) Rd[i * kNBW + c1] = fma(f1, u0, rd1);
-            }
+        for (int r = 0; r < RPL; ++r) {
+            a[0][r] = fma(f0, v[r], a[0][r]);
+            a[1][r] = fma(f1, v[r], a[1][r]);
         }
+        if (rg == 0 && app && l0) rd_c[i * kNBW] = fma(f0, u0, rd0);
+        if (rg == 0 && app && l1) rd_c[i * kNBW + 1] = fma(f1, u0, rd1);
+    };
+#pragma unroll 1
+    for (int i = 0; i < nbp; i += 2) {
+        step(std::integral_constant<int, 0>{}, i);
+        if (i + 1 < nbp) step(std::integral_constant<int, 1>{}, i + 1);
     }
     // the reflector vectors: lane (rg, cp) holds final columns 2cp, 2cp+1 of its rows
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
         double* row = C + (size_t)(rg + 4 * r) * LDC + p;
-        if (c0 < nbp) row[c0] = a0[r];
-        if (c1 < nbp) row[c1] = a1[r];
-    }
-    if (lane < nbp) {
-        cgv[lane] = my_g;
-        cuv[lane] = my_u0;
-        if (my_g != 0.0) Rd[lane * kNBW + lane] = my_beta;
+        if (c0 < nbp) row[c0] = a[0][r];
+        if (c1 < nbp) row[c1] = a[1][r];
     }
     __syncwarp();
 }
