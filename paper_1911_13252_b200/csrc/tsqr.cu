@@ -1100,35 +1100,44 @@ static int wy_rows(const elmrnn* h, int n) {
             return r;
     }
     // 32-row tiles, 2-3 CTAs per SM (their panels overlap each other's trailing updates)
+    // n <= 160: 64-row tiles (measured M = 128 x 2M rows: 12.9 vs 14.3 ms with 32);
+    // larger n: 32-row tiles, 2-3 CTAs per SM (their panels overlap each other's
+    // trailing updates; 16/24-row tiles and 4-warp CTAs measured slower at
+    // n = 257, 513, 1025: tools/wy_variants.sh)
+    if (n <= 160) return 64;
     return wy_smem_bytes(32, n) <= 220 * 1024 ? 32 : 16;
 }
 // Leaf dynamic shared memory: the tile + coefficients.
 static size_t wy_leaf_smem(int rows, int n) { return std::min(wy_smem_bytes(rows, n), (size_t)227 * 1024); }
 static int wy_nw(int n) { return n <= 320 ? 4 : 8; }
 static int wy_threads(int n) { return 32 * wy_nw(n); }
+// leaf warps per CTA: by n, or the testing override
+static int wy_leaf_nw(const elmrnn* h, int n) { return (h->tune.wy_nw == 4 || h->tune.wy_nw == 8) ? h->tune.wy_nw : wy_nw(n); }
 template <int RW, class F>
-static auto wy_nw_dispatch(int n, F& f) {
-    if (wy_nw(n) == 4) return f(std::integral_constant<int, RW>{}, std::integral_constant<int, 4>{});
+static auto wy_nw_dispatch(int nw, F& f) {
+    if (nw == 4) return f(std::integral_constant<int, RW>{}, std::integral_constant<int, 4>{});
     return f(std::integral_constant<int, RW>{}, std::integral_constant<int, 8>{});
 }
 template <class F>
 static auto wy_dispatch(const elmrnn* h, int n, F&& f) {
+    const int nw = wy_leaf_nw(h, n);
     switch (wy_rows(h, n)) {
-    case 96: return wy_nw_dispatch<96>(n, f);
-    case 64: return wy_nw_dispatch<64>(n, f);
-    case 32: return wy_nw_dispatch<32>(n, f);
-    case 24: return wy_nw_dispatch<24>(n, f);
-    case 8: return wy_nw_dispatch<8>(n, f);
-    default: return wy_nw_dispatch<16>(n, f);
+    case 96: return wy_nw_dispatch<96>(nw, f);
+    case 64: return wy_nw_dispatch<64>(nw, f);
+    case 32: return wy_nw_dispatch<32>(nw, f);
+    case 24: return wy_nw_dispatch<24>(nw, f);
+    case 8: return wy_nw_dispatch<8>(nw, f);
+    default: return wy_nw_dispatch<16>(nw, f);
     }
 }
 
 template <class F>
 static auto wy_dispatch_merge(int n, F&& f) {
-    if (wy_smem_bytes(96, n) <= 220 * 1024) return wy_nw_dispatch<96>(n, f);
-    if (wy_smem_bytes(64, n) <= 220 * 1024) return wy_nw_dispatch<64>(n, f);
-    if (wy_smem_bytes(32, n) <= 220 * 1024) return wy_nw_dispatch<32>(n, f);
-    return wy_nw_dispatch<16>(n, f);
+    const int nw = wy_nw(n);
+    if (wy_smem_bytes(96, n) <= 220 * 1024) return wy_nw_dispatch<96>(nw, f);
+    if (wy_smem_bytes(64, n) <= 220 * 1024) return wy_nw_dispatch<64>(nw, f);
+    if (wy_smem_bytes(32, n) <= 220 * 1024) return wy_nw_dispatch<32>(nw, f);
+    return wy_nw_dispatch<16>(nw, f);
 }
 
 int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
@@ -1140,7 +1149,7 @@ int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
         const size_t sm = wy_leaf_smem(RW, n);
         cudaFuncSetAttribute(k_tsqr_leaf_wy<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         int ps = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_tsqr_leaf_wy<RW, NW>, wy_threads(n), sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_tsqr_leaf_wy<RW, NW>, 32 * NW, sm);
         return ps < 1 ? 1 : ps;
     }) : dispatch(v, [&](auto tr, auto p) {
         int ps = 0;
@@ -1255,7 +1264,7 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
             cudaFuncSetAttribute(k_tsqr_leaf_wy<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             int* slot = reinterpret_cast<int*>(h->sdev + 1);   // per-SM arrival counters (ensure_solve_ws)
             cudaMemsetAsync(slot, 0, 1024 * sizeof(int), h->stream);
-            k_tsqr_leaf_wy<RW, NW><<<(unsigned)slabs, wy_threads(n), sm, h->stream>>>(
+            k_tsqr_leaf_wy<RW, NW><<<(unsigned)slabs, 32 * NW, sm, h->stream>>>(
                 H, ldh, Y, ldy, h->nrhs, N, h->M, h->Rws, rows, h->flag, slot, wy_la_wait(n), h->tune.pw_mode);
             h->launches++;
             return cudaGetLastError();
