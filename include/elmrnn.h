@@ -83,6 +83,10 @@ typedef struct {
                          to the fp16 grid, 2 rounded to the tf32 grid (RNA)            */
     int fc_lags;      /* FC lags L; -1 -> Q (prose reading R9); 1 = first-order FC     */
     int force_path;   /* H-builder choice: 0 auto, 1 FP32-FMA kernels, 2 tensor cores */
+    int fused_train;  /* elmrnn_train route: 0 (default) build_H + solve, measured faster
+                         (C1 133 vs 238 us, C2 0.94 vs 1.08 ms: the per-column leaf
+                         has too few threads to also compute H); 1 the fused
+                         build -> TSQR leaf where supported (H never in memory) */
 } elmrnn_opts;
 
 /* Diagnostics of a solve (host struct). */
@@ -158,6 +162,29 @@ ELMRNN_API elmrnn_status elmrnn_error_windows(elmrnn_t h, const float* H, int64_
  * Errors: ARG, SHAPE, UNDERDETERMINED (N < M), NONFINITE, OOM, CUDA. */
 ELMRNN_API elmrnn_status elmrnn_solve_beta(elmrnn_t h, const float* H, int64_t ldh, const float* Y,
                                 int64_t N, double* beta, elmrnn_solve_info* info);
+
+/* Alg. 1 lines 2-3 in one call: H(Q) of the N windows (as
+ * elmrnn_build_H) and beta (as elmrnn_solve_beta) -- SURVEY 8(f) row 2, "the two
+ * CPU intensive operations" of P:246 fused.  For the cell-independent archs
+ * (Elman with Q <= 32, Jordan, NARMAX) whose solve takes the per-column
+ * TSQR (M + 1 <= 128), with opts.fused_train = 1, the TSQR leaf computes every
+ * H element where it would have loaded it, so H never exists in memory
+ * (elmrnn_train_fused(h) == 1); otherwise (the default, measured faster) H goes
+ * through a library workspace (N*M floats) between build_H and the solve.
+ *   X, Yfb as elmrnn_build_H; Y dev fp32 [N]; beta dev fp64 [M]; info as
+ *   elmrnn_solve_beta.
+ * Errors: ARG, SHAPE, UNDERDETERMINED (N < M), NONFINITE, OOM, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_train(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy,
+                           const float* Y, int64_t N, double* beta, elmrnn_solve_info* info);
+
+/* Row-sharded step 1 of elmrnn_train: this rank's packed R of [H | Y] (as
+ * elmrnn_solve_local) directly from its windows.  N may be 0.  Asynchronous.
+ * Errors: ARG, SHAPE, OOM, CUDA. */
+ELMRNN_API elmrnn_status elmrnn_train_local(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb,
+                                 int64_t ldy, const float* Y, int64_t N, double* Rpk);
+
+/* 1 when elmrnn_train / elmrnn_train_local run the fused build -> leaf on this handle. */
+ELMRNN_API int elmrnn_train_fused(elmrnn_t h);
 
 /* Multi-output least squares (the paper's future work,
  * P:655): B = argmin ||H B - Y||_F for P outputs at once, by one fp64

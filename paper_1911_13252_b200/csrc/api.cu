@@ -29,7 +29,7 @@ extern "C" {
 
 void elmrnn_opts_default(elmrnn_opts* o) {
     if (!o) return;
-    o->F = -1; o->R = -1; o->act = 0; o->rec_scale = 0; o->weight_grid = 0; o->fc_lags = -1; o->force_path = 0;
+    o->F = -1; o->R = -1; o->act = 0; o->rec_scale = 0; o->weight_grid = 0; o->fc_lags = -1; o->force_path = 0; o->fused_train = 0;
 }
 
 elmrnn_status elmrnn_init(elmrnn_t* out, int arch, int d, int M, int Q, uint64_t seed) {
@@ -48,7 +48,7 @@ elmrnn_status elmrnn_init_ex(elmrnn_t* out, int arch, int d, int M, int Q, uint6
     if (o.R < 0) o.R = Q;
     if (o.fc_lags < 0) o.fc_lags = Q;
     if (o.act < 0 || o.act > 1 || o.rec_scale < 0 || o.rec_scale > 1 || o.weight_grid < 0 || o.weight_grid > 2 ||
-        o.force_path < 0 || o.force_path > 2 || o.fc_lags < 1)
+        o.force_path < 0 || o.force_path > 2 || o.fc_lags < 1 || o.fused_train < 0 || o.fused_train > 1)
         return fail(nullptr, ELMRNN_ERR_ARG, "invalid option value");
     if ((arch == ELMRNN_ELMAN || arch == ELMRNN_FC_EQ8) && !elman_supported(Q))
         return fail(nullptr, ELMRNN_ERR_UNSUPPORTED, "Elman supports Q <= 128");
@@ -58,7 +58,7 @@ elmrnn_status elmrnn_init_ex(elmrnn_t* out, int arch, int d, int M, int Q, uint6
     if (!h) return fail(nullptr, ELMRNN_ERR_OOM, "host allocation failed");
     h->arch = arch; h->S = d; h->M = M; h->Q = Q; h->F = o.F; h->R = o.R; h->act = o.act;
     h->fc_lags = o.fc_lags; h->rec_scale = o.rec_scale; h->weight_grid = o.weight_grid;
-    h->force_path = o.force_path; h->seed = seed; h->G = gates_of(arch); h->stream = nullptr;
+    h->force_path = o.force_path; h->fused_train = o.fused_train; h->seed = seed; h->G = gates_of(arch); h->stream = nullptr;
     h->path = 1;
     h->nrhs = 1;
     if (const char* t = std::getenv("ELMRNN_TESTING"); t && std::atoi(t) == 1) {   // test overrides, read once
@@ -282,6 +282,74 @@ elmrnn_status elmrnn_sync(elmrnn_t h) {
     return ELMRNN_OK;
 }
 
+// Readout (Eq. 4) row chunk: H(Q) of a chunk is built into a workspace of at
+// most 32 MB that stays resident in the 126 MB L2 while the readout kernel
+// consumes it, so H never round-trips HBM and the workspace does not grow with N.
+static int64_t readout_chunk_rows(const elmrnn* h, int64_t N) {
+    int64_t rows = ((int64_t)32 << 20) / ((int64_t)4 * h->M);
+    rows = rows < 8192 ? 8192 : (rows / 128) * 128;
+    return rows < N ? rows : N;
+}
+
+static cudaError_t ensure_hws(elmrnn* h, int64_t N) {
+    if (N <= h->Hws_rows) return cudaSuccess;
+    if (h->Hws) cudaFree(h->Hws);
+    h->Hws = nullptr;
+    h->Hws_rows = 0;
+    cudaError_t e = cudaMalloc(&h->Hws, sizeof(float) * N * h->M);
+    if (!e) h->Hws_rows = N;
+    return e;
+}
+
+// Alg. 1 lines 2-3 in one call.  Cell-independent archs on
+// the per-column TSQR path: fused build -> leaf, H never exists.  Others: H in a
+// library workspace, then the solve.
+static elmrnn_status train_factor(elmrnn* h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy,
+                                  const float* Y, int64_t N) {
+    if (!X || !Y) return fail(h, ELMRNN_ERR_ARG, "NULL pointer");
+    if (ldx < (int64_t)h->Q * h->S) return fail(h, ELMRNN_ERR_SHAPE, "ldx < Q*d");
+    if (Yfb && ldy < h->Q) return fail(h, ELMRNN_ERR_SHAPE, "ldy < Q");
+    cudaError_t e;
+    if (h->fused_train && tsqr_fused_supported(h)) {
+        if ((e = tsqr_factor_fused(h, X, ldx, Yfb, ldy, Y, N))) return cuda_fail(h, e, "train (fused)");
+        return ELMRNN_OK;
+    }
+    if ((e = ensure_hws(h, N))) return cuda_fail(h, e, "train workspace");
+    elmrnn_status st = build_impl(h, X, ldx, Yfb, ldy, N, h->Hws, h->M);
+    if (st != ELMRNN_OK) return st;
+    if ((e = tsqr_factor(h, h->Hws, h->M, Y, 1, N))) return cuda_fail(h, e, "tsqr_factor");
+    return ELMRNN_OK;
+}
+
+elmrnn_status elmrnn_train(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy, const float* Y,
+                           int64_t N, double* beta, elmrnn_solve_info* info) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (!beta) return fail(h, ELMRNN_ERR_ARG, "NULL pointer");
+    if (N < h->M) return fail(h, ELMRNN_ERR_UNDERDETERMINED, "N < M");
+    elmrnn_status st = train_factor(h, X, ldx, Yfb, ldy, Y, N);
+    if (st != ELMRNN_OK) return st;
+    cudaError_t e;
+    if ((e = tsqr_solve(h, N, beta))) return cuda_fail(h, e, "tsqr_solve");
+    return finish_solve(h, info);
+}
+
+elmrnn_status elmrnn_train_local(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy,
+                                 const float* Y, int64_t N, double* Rpk) {
+    if (!h) return ELMRNN_ERR_ARG;
+    if (!Rpk || N < 0) return fail(h, ELMRNN_ERR_ARG, "bad argument");
+    cudaError_t e;
+    if (N == 0) {
+        if ((e = tsqr_factor(h, nullptr, h->M, nullptr, 1, 0))) return cuda_fail(h, e, "tsqr_factor");
+    } else {
+        elmrnn_status st = train_factor(h, X, ldx, Yfb, ldy, Y, N);
+        if (st != ELMRNN_OK) return st;
+    }
+    if ((e = tsqr_pack(h, Rpk))) return cuda_fail(h, e, "tsqr_pack");
+    return ELMRNN_OK;
+}
+
+int elmrnn_train_fused(elmrnn_t h) { return h && h->fused_train && tsqr_fused_supported(h) ? 1 : 0; }
+
 elmrnn_status elmrnn_solve_local_multi(elmrnn_t h, const float* H, int64_t ldh, const float* Y, int64_t ldy, int P,
                                        int64_t N, double* Rpk) {
     if (!h) return ELMRNN_ERR_ARG;
@@ -341,15 +409,6 @@ int64_t elmrnn_packed_r_len(elmrnn_t h) {
     return (int64_t)(h->M + 1) * (h->M + 2) / 2;
 }
 
-static cudaError_t ensure_hws(elmrnn* h, int64_t N) {
-    if (N <= h->Hws_rows) return cudaSuccess;
-    if (h->Hws) cudaFree(h->Hws);
-    h->Hws = nullptr;
-    h->Hws_rows = 0;
-    cudaError_t e = cudaMalloc(&h->Hws, sizeof(float) * N * h->M);
-    if (!e) h->Hws_rows = N;
-    return e;
-}
 
 elmrnn_status elmrnn_predict(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy, int64_t N,
                              const double* beta, float* Yhat) {
@@ -360,10 +419,14 @@ elmrnn_status elmrnn_predict(elmrnn_t h, const float* X, int64_t ldx, const floa
     if (ldx < (int64_t)h->Q * h->S) return fail(h, ELMRNN_ERR_SHAPE, "ldx < Q*d");
     if (Yfb && ldy < h->Q) return fail(h, ELMRNN_ERR_SHAPE, "ldy < Q");
     cudaError_t e;
-    if ((e = ensure_hws(h, N))) return cuda_fail(h, e, "predict workspace");
-    elmrnn_status st = build_impl(h, X, ldx, Yfb, ldy, N, h->Hws, h->M);
-    if (st != ELMRNN_OK) return st;
-    if ((e = launch_predict_gemv(h, h->Hws, h->M, N, beta, Yhat))) return cuda_fail(h, e, "predict");
+    const int64_t chunk = readout_chunk_rows(h, N);
+    if ((e = ensure_hws(h, chunk))) return cuda_fail(h, e, "predict workspace");
+    for (int64_t r0 = 0; r0 < N; r0 += chunk) {   // build a chunk into the L2-resident workspace, read it out
+        const int64_t nr = N - r0 < chunk ? N - r0 : chunk;
+        elmrnn_status st = build_impl(h, X + r0 * ldx, ldx, Yfb ? Yfb + r0 * ldy : nullptr, ldy, nr, h->Hws, h->M);
+        if (st != ELMRNN_OK) return st;
+        if ((e = launch_predict_gemv(h, h->Hws, h->M, nr, beta, Yhat + r0))) return cuda_fail(h, e, "predict");
+    }
     return ELMRNN_OK;
 }
 
@@ -388,13 +451,19 @@ elmrnn_status elmrnn_forecast(elmrnn_t h, const float* X, int64_t ldx, int64_t N
         if ((e = cudaMalloc(&h->fws, sizeof(float) * N * (ldw + 1)))) return cuda_fail(h, e, "forecast workspace");
         h->fws_rows = N;
     }
-    if ((e = ensure_hws(h, N))) return cuda_fail(h, e, "forecast workspace");
+    const int64_t chunk = readout_chunk_rows(h, N);
+    if ((e = ensure_hws(h, chunk))) return cuda_fail(h, e, "forecast workspace");
     if ((e = launch_window_init(h, X, ldx, N, h->fws, ldw))) return cuda_fail(h, e, "forecast");
-    for (int k = 0; k < K; ++k) {
-        elmrnn_status st = build_impl(h, h->fws, ldw, nullptr, 0, N, h->Hws, h->M);
-        if (st != ELMRNN_OK) return st;
-        if ((e = launch_predict_shift(h, h->Hws, h->M, N, beta, h->fws, ldw, Yhat + k, ldyh)))
-            return cuda_fail(h, e, "forecast");
+    // rows are independent: each chunk runs its K steps with H(Q) in the L2-resident workspace
+    for (int64_t r0 = 0; r0 < N; r0 += chunk) {
+        const int64_t nr = N - r0 < chunk ? N - r0 : chunk;
+        float* w = h->fws + r0 * ldw;
+        for (int k = 0; k < K; ++k) {
+            elmrnn_status st = build_impl(h, w, ldw, nullptr, 0, nr, h->Hws, h->M);
+            if (st != ELMRNN_OK) return st;
+            if ((e = launch_predict_shift(h, h->Hws, h->M, nr, beta, w, ldw, Yhat + r0 * ldyh + k, ldyh)))
+                return cuda_fail(h, e, "forecast");
+        }
     }
     return ELMRNN_OK;
 }

@@ -42,7 +42,7 @@ struct Tune {
 // (DESIGN.md "Data layout in HBM"); the logical blocks are regenerated on
 // demand by elmrnn_get_weights.
 struct elmrnn {
-    int arch, S, M, Q, F, R, act, fc_lags, rec_scale, weight_grid, force_path;
+    int arch, S, M, Q, F, R, act, fc_lags, rec_scale, weight_grid, force_path, fused_train;
     int G;                // gate blocks
     uint64_t seed;
     int device, sm_count;
@@ -128,6 +128,9 @@ cudaError_t launch_fc_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, floa
 // Fold [H | Y] rows into per-CTA R slabs and reduce them to slab 0 (full storage).
 cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t ldy, int64_t N);
 cudaError_t tsqr_pack(elmrnn* h, double* Rpk);
+bool tsqr_fused_supported(const elmrnn* h);
+cudaError_t tsqr_factor_fused(elmrnn* h, const float* X, int64_t ldx, const float* Yfb, int64_t ldyfb, const float* Y,
+                              int64_t N);
 cudaError_t tsqr_merge_packed(elmrnn* h, const double* Rpk_all, int P);
 cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta);
 cudaError_t ensure_solve_ws(elmrnn* h, int64_t slabs);

@@ -31,6 +31,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "cell.cuh"
 
 namespace elm {
 
@@ -205,9 +206,24 @@ __device__ void fold_tile(double (&a)[TR], int n, int k0, double* __restrict__ R
 }
 
 
-template <int TR, int P>
+// Leaf element sources: H loaded from memory, or computed per cell (fused
+// build -> leaf, elmrnn_train; cell.cuh).  KIND 0: H; 1: Elman (QMAX >= Q);
+// 2: Jordan / NARMAX teacher forced.
+template <int KIND, int QMAX>
+struct LeafSrc {
+    const float* H;
+    int64_t ldh;
+    CellSrc cell;
+    __device__ __forceinline__ float at(int64_t row, int j) const {
+        if constexpr (KIND == 0) return __ldg(H + row * ldh + j);
+        else if constexpr (KIND == 1) return cell_elman<QMAX>(cell, row, j);
+        else return cell_tf(cell, row, j);
+    }
+};
+
+template <int TR, int P, int KIND = 0, int QMAX = 1>
 __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
-    k_tsqr_leaf(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t ldy, int64_t N, int M,
+    k_tsqr_leaf(const LeafSrc<KIND, QMAX> src, const float* __restrict__ Y, int64_t ldy, int64_t N, int M,
                 double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag) {
     constexpr int ROWS = TR * P;
     __shared__ __align__(16) double vbuf[2 * ROWS];
@@ -225,7 +241,7 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
         for (int i = 0; i < TR; ++i) {
             const int64_t row = base + half * TR + i;
             float v = 0.0f;
-            if (row < r1 && j >= 0 && j < n) v = (j < M) ? __ldg(H + row * ldh + j) : __ldg(Y + row * ldy);
+            if (row < r1 && j >= 0 && j < n) v = (j < M) ? src.at(row, j) : __ldg(Y + row * ldy);
             bad |= !isfinite(v);
             a[i] = (double)v;
         }
@@ -1153,7 +1169,7 @@ int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
         return ps < 1 ? 1 : ps;
     }) : dispatch(v, [&](auto tr, auto p) {
         int ps = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_tsqr_leaf<decltype(tr)::value, decltype(p)::value>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_tsqr_leaf<decltype(tr)::value, decltype(p)::value, 0, 1>,
                                                       threads, 0);
         return ps < 1 ? 1 : ps;
     });
@@ -1273,8 +1289,53 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
         return tree(h, slabs);
     }
     e = dispatch(v, [&](auto tr, auto p) {
-        k_tsqr_leaf<decltype(tr)::value, decltype(p)::value>
-            <<<(unsigned)slabs, threads, 0, h->stream>>>(H, ldh, Y, ldy, N, h->M, h->Rws, rows, h->flag);
+        LeafSrc<0, 1> src{H, ldh, {}};
+        k_tsqr_leaf<decltype(tr)::value, decltype(p)::value, 0, 1>
+            <<<(unsigned)slabs, threads, 0, h->stream>>>(src, Y, ldy, N, h->M, h->Rws, rows, h->flag);
+        h->launches++;
+        return cudaGetLastError();
+    });
+    if (e) return e;
+    return tree(h, slabs);
+}
+
+// Fused build -> leaf (elmrnn_train): the per-column leaf
+// computes each H element of the cell-independent archs where it would load it.
+bool tsqr_fused_supported(const elmrnn* h) {
+    const int n = h->M + 1;
+    if (use_wy(h, n)) return false;   // the per-column fold's thread = column layout only
+    if (h->arch == kArchElman) return h->Q <= 32;
+    return h->arch == kArchJordan || h->arch == kArchNarmax;
+}
+
+cudaError_t tsqr_factor_fused(elmrnn* h, const float* X, int64_t ldx, const float* Yfb, int64_t ldyfb,
+                              const float* Y, int64_t N) {
+    const int n = h->M + 1;
+    const Var v = pick_var(n);
+    const int64_t slabs = tsqr_leaf_slabs(h, N);
+    cudaError_t e;
+    if ((e = ensure_solve_ws(h, slabs))) return e;
+    if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream))) return e;
+    int64_t rows = (N + slabs - 1) / slabs;
+    rows = (rows + var_rows(v) - 1) / var_rows(v) * var_rows(v);
+    const int threads = var_threads(v, n);
+    int nlag = h->Q - 1;
+    if (h->arch == kArchNarmax) nlag = h->F < h->Q - 1 ? h->F : h->Q - 1;
+    const CellSrc cs{X, ldx, Yfb, ldyfb, h->S, h->M, h->Q, h->act, nlag, h->W, h->b, h->rec};
+    e = dispatch(v, [&](auto tr, auto p) {
+        constexpr int TRv = decltype(tr)::value, Pv = decltype(p)::value;
+        if (h->arch == kArchElman) {
+            if (h->Q <= 16) {
+                LeafSrc<1, 16> src{nullptr, 0, cs};
+                k_tsqr_leaf<TRv, Pv, 1, 16><<<(unsigned)slabs, threads, 0, h->stream>>>(src, Y, 1, N, h->M, h->Rws, rows, h->flag);
+            } else {
+                LeafSrc<1, 32> src{nullptr, 0, cs};
+                k_tsqr_leaf<TRv, Pv, 1, 32><<<(unsigned)slabs, threads, 0, h->stream>>>(src, Y, 1, N, h->M, h->Rws, rows, h->flag);
+            }
+        } else {
+            LeafSrc<2, 1> src{nullptr, 0, cs};
+            k_tsqr_leaf<TRv, Pv, 2, 1><<<(unsigned)slabs, threads, 0, h->stream>>>(src, Y, 1, N, h->M, h->Rws, rows, h->flag);
+        }
         h->launches++;
         return cudaGetLastError();
     });

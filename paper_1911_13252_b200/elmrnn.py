@@ -27,6 +27,7 @@ EXPORTED = ("elmrnn_opts_default", "elmrnn_init", "elmrnn_init_ex", "elmrnn_set_
             "elmrnn_solve_beta_multi",
             "elmrnn_solve_beta", "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_sync", "elmrnn_packed_r_len",
             "elmrnn_solve_local_multi", "elmrnn_solve_merge_multi", "elmrnn_packed_r_len_multi",
+            "elmrnn_train", "elmrnn_train_local", "elmrnn_train_fused",
             "elmrnn_predict", "elmrnn_get_weights", "elmrnn_weight_block_len", "elmrnn_path",
             "elmrnn_launch_count", "elmrnn_last_error", "elmrnn_destroy")
 
@@ -39,7 +40,8 @@ class ElmrnnError(RuntimeError):
 
 class Opts(ctypes.Structure):
     _fields_ = [("F", ctypes.c_int), ("R", ctypes.c_int), ("act", ctypes.c_int), ("rec_scale", ctypes.c_int),
-                ("weight_grid", ctypes.c_int), ("fc_lags", ctypes.c_int), ("force_path", ctypes.c_int)]
+                ("weight_grid", ctypes.c_int), ("fc_lags", ctypes.c_int), ("force_path", ctypes.c_int),
+                ("fused_train", ctypes.c_int)]
 
 
 class _Info(ctypes.Structure):
@@ -86,6 +88,9 @@ def lib() -> ctypes.CDLL:
         L.elmrnn_solve_local.argtypes = [vp, vp, i64, vp, i64, vp]
         L.elmrnn_solve_merge.argtypes = [vp, vp, i32, i64, vp, vp]
         L.elmrnn_sync.argtypes = [vp]
+        L.elmrnn_train.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, vp]
+        L.elmrnn_train_local.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp]
+        L.elmrnn_train_fused.argtypes = [vp]
         L.elmrnn_solve_local_multi.argtypes = [vp, vp, i64, vp, i64, i32, i64, vp]
         L.elmrnn_solve_merge_multi.argtypes = [vp, vp, i32, i32, i64, vp, vp, vp]
         L.elmrnn_packed_r_len_multi.argtypes = [vp, i32]
@@ -107,7 +112,8 @@ def lib() -> ctypes.CDLL:
                   "elmrnn_error_windows", "elmrnn_forecast", "elmrnn_test_rmse", "elmrnn_solve_beta",
                   "elmrnn_solve_beta_multi",
                   "elmrnn_solve_local", "elmrnn_solve_merge", "elmrnn_sync", "elmrnn_predict", "elmrnn_get_weights",
-                  "elmrnn_solve_local_multi", "elmrnn_solve_merge_multi",
+                  "elmrnn_solve_local_multi", "elmrnn_solve_merge_multi", "elmrnn_train", "elmrnn_train_local",
+                  "elmrnn_train_fused",
                   "elmrnn_path"):
             getattr(L, f).restype = i32
         _lib = L
@@ -151,7 +157,7 @@ class ELMRNN:
     """Handle of one ELM-RNN (fixed random weights) on the current CUDA device.
 
     ELMRNN(arch, d, M, Q, seed, F=-1, R=-1, act=0, rec_scale=0, weight_grid=0,
-    fc_lags=-1, force_path=0) -- elmrnn_init_ex."""
+    fc_lags=-1, force_path=0, fused_train=0) -- elmrnn_init_ex."""
 
     def __init__(self, arch, d: int, M: int, Q: int, seed: int = 1, **opts):
         L = lib()
@@ -432,6 +438,51 @@ class ELMRNN:
         self._stream()
         self._check(lib().elmrnn_get_weights(self._h, block_id, out.data_ptr(), n))
         return out
+
+    @property
+    def train_fused(self) -> bool:
+        return bool(lib().elmrnn_train_fused(self._h))
+
+    def train_direct(self, X: torch.Tensor, Y: torch.Tensor, Yfb: torch.Tensor | None = None,
+                     beta: torch.Tensor | None = None, info: bool = True):
+        """elmrnn_train: beta (and SolveInfo) straight from the windows, without
+        returning H (fused build -> TSQR leaf where supported)."""
+        _dev_check(X, "X", torch.float32)
+        N = X.shape[0]
+        _vec(Y, "Y", torch.float32, N)
+        ldx = _rows(X, "X")[0] if N else self.Q * self.d
+        ldy = 0
+        if Yfb is not None:
+            _dev_check(Yfb, "Yfb", torch.float32)
+            ldy, ry = _rows(Yfb, "Yfb")
+            _need_rows(ry, N, "Yfb")
+        if beta is None:
+            beta = torch.empty(self.M, dtype=torch.float64, device=X.device)
+        _vec(beta, "beta", torch.float64, self.M)
+        self._stream()
+        inf = _Info()
+        st = self._check(lib().elmrnn_train(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, _ptr(Y), N, _ptr(beta),
+                                            ctypes.byref(inf) if info else None))
+        return beta, (self._info(inf, st) if info else None)
+
+    def train_local(self, X: torch.Tensor, Y: torch.Tensor, Yfb: torch.Tensor | None = None,
+                    Rpk: torch.Tensor | None = None):
+        """elmrnn_train_local: this shard's packed R of [H | Y] straight from its windows."""
+        _dev_check(X, "X", torch.float32)
+        N = X.shape[0]
+        _vec(Y, "Y", torch.float32, N)
+        ldx = _rows(X, "X")[0] if N else self.Q * self.d
+        ldy = 0
+        if Yfb is not None:
+            _dev_check(Yfb, "Yfb", torch.float32)
+            ldy, ry = _rows(Yfb, "Yfb")
+            _need_rows(ry, N, "Yfb")
+        if Rpk is None:
+            Rpk = torch.empty(self.packed_r_len, dtype=torch.float64, device=X.device)
+        _vec(Rpk, "Rpk", torch.float64, self.packed_r_len)
+        self._stream()
+        self._check(lib().elmrnn_train_local(self._h, _ptr(X), ldx, _ptr(Yfb), ldy, _ptr(Y), N, _ptr(Rpk)))
+        return Rpk
 
     def train(self, X, Y, Yfb=None):
         """Alg. 1 lines 2-3: H(Q) then beta."""

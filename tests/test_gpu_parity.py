@@ -397,6 +397,38 @@ def test_nonfinite_async_reported_by_sync():
             e.sync()
 
 
+@pytest.mark.parametrize("arch,N,S,M,Q,yfb,o", [("elman", 1000, 1, 20, 10, False, {}), ("jordan", 20000, 1, 64, 20, False, {}),
+                                                ("narmax", 5000, 1, 64, 20, True, {"F": 3, "R": 7}),
+                                                ("elman", 777, 2, 37, 25, False, {"act": 1}), ("gru", 3000, 1, 32, 10, False, {}),
+                                                ("lstm", 3000, 4, 128, 10, False, {})])
+def test_train_fused(arch, N, S, M, Q, yfb, o):
+    """elmrnn_train: the fused build -> TSQR leaf (H never in
+    memory) gives bitwise the beta of elmrnn_build_H + elmrnn_solve_beta; archs
+    without the fused path take the workspace route and agree as well; the
+    row-sharded elmrnn_train_local + merge equals the single call."""
+    X, Y, Yfb = inputs(N, Q, S, seed=N + M, kind="ar5" if arch in ("jordan", "narmax") else None)
+    e = E(arch, S, M, Q, 3, fused_train=1, **o)
+    assert e.train_fused == (arch in ("elman", "jordan", "narmax"))
+    assert not E(arch, S, M, Q, 3, **o).train_fused     # default route: build_H + solve (measured faster)
+    Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+    Yfbd = torch.from_numpy(Yfb).cuda() if yfb else None
+    b1, i1 = e.train_direct(Xd, Yd, Yfbd)
+    H = e.build_H(Xd, Yfbd)
+    b2, i2 = e.solve_beta(H, Yd)
+    assert torch.equal(b1, b2), float((b1 - b2).norm() / b2.norm())
+    assert i1.rmse == i2.rmse and i1.status == i2.status
+    cuts = [0, N // 3, N]
+    parts = [e.train_local(Xd[a:b], Yd[a:b], Yfbd[a:b] if yfb else None).clone() for a, b in zip(cuts[:-1], cuts[1:])]
+    b3, _ = e.solve_merge(torch.stack(parts), 2, N)
+    bo, io = orc.lstsq(H.double().cpu().numpy(), Y.astype(np.float64))
+    cond = np.linalg.cond(io.R[:M, :M])
+    assert float((b3 - b2).norm() / b2.norm()) <= 1e-12 * max(1.0, cond)
+    # and against the oracle's own H (R26 rule)
+    net = oracle_net(arch, S, M, Q, **o)
+    Ho = orc.build_H(net, orc.gen_weights(net, 3), X, Yfb if yfb else None, threads=8)
+    pr.check(f"train {arch} fused={e.train_fused}", b1.cpu().numpy(), i1.rmse, H.double().cpu().numpy(), Ho, Y)
+
+
 def test_predict_parity():
     N, S, M, Q = 700, 1, 32, 10
     X, Y, _ = inputs(N, Q, S)
@@ -685,6 +717,25 @@ def test_forecast_per_step_parity(arch, M, Q):
         W = np.concatenate([W[:, 1:], Yh[:, k:k + 1]], axis=1)
     full = orc.forecast(net, bl, X, beta, K, threads=8)
     assert np.abs(Yh - full).max() <= 10 * tol
+
+
+def test_predict_forecast_chunked_readout():
+    """Readout in L2-resident row chunks (elmrnn_predict / elmrnn_forecast build
+    H(Q) chunk by chunk, 131072 rows at M = 64): rows on both sides of the chunk
+    boundary against the oracle's Eq. 4 and free-running forecast."""
+    N, M, Q, K = 140000, 64, 10, 2
+    X, Y, _ = inputs(N, Q, 1, seed=5, kind="ar5")
+    beta = np.random.default_rng(2).standard_normal(M) / M
+    e = E("elman", 1, M, Q, 8)
+    Xd, bd = torch.from_numpy(X).cuda(), torch.from_numpy(beta).cuda()
+    yp = e.predict(Xd, bd).cpu().numpy()
+    Yh = e.forecast(Xd, bd, K).cpu().numpy()
+    rows = np.r_[0:50, 131000:131200, N - 50:N]
+    net = orc.Net("elman", S=1, M=M, Q=Q)
+    bl = orc.gen_weights(net, 8)
+    tol = 1e-5 * max(1.0, np.abs(beta).sum())
+    assert np.abs(yp[rows] - orc.predict(orc.build_H(net, bl, X[rows], threads=8), beta)).max() <= tol
+    assert np.abs(Yh[rows] - orc.forecast(net, bl, X[rows], beta, K, threads=8)).max() <= 10 * tol
 
 
 def test_forecast_errors_and_empty():
