@@ -34,6 +34,7 @@ struct Tune {
     int wy_rows = 0;    // ELMRNN_TSQR_WY_ROWS: WY leaf tile rows (8..96)
     int pw_mode = 1;    // ELMRNN_PW_MODE: WY leaf panel warp 0 rotate SMSPs per CTA, 1 pin to SMSP 0
     int wy_nw = 0;      // ELMRNN_WY_NW: WY leaf/merge warps per CTA (4 or 8; 0 = by n)
+    int max_slabs = 0;  // ELMRNN_TSQR_MAXSLABS: cap on the TSQR leaf count (0 = by size)
 };
 
 }  // namespace elm

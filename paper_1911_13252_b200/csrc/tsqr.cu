@@ -1174,6 +1174,7 @@ int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
         return ps < 1 ? 1 : ps;
     });
     int64_t maxc = (int64_t)per_sm * h->sm_count;
+    if (h->tune.max_slabs >= 1 && h->tune.max_slabs < maxc) maxc = h->tune.max_slabs;
     // at least n rows per leaf: a leaf R with fewer rows is rank deficient
     // and its noise rows only cost merges (and risk underflow cascades)
     int64_t byrows = N / n;
