@@ -976,7 +976,7 @@ __global__ void __launch_bounds__(32 * NW, (NW == 4 && ROWS <= 32) ? 3 : 1)
                 for (int b = 0; b < B; ++b) {
                     const int e = e0 + b * nt, r = e / M4, q = e - r * M4;
                     v[b] = (e < ROWS * M4 && base + r < r1)
-                               ? __ldg(reinterpret_cast<const float4*>(H + (base + r) * ldh) + q)
+                               ? __ldcs(reinterpret_cast<const float4*>(H + (base + r) * ldh) + q)
                                : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
 #pragma unroll
