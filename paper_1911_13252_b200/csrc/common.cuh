@@ -35,6 +35,7 @@ struct Tune {
     int pw_mode = 1;    // ELMRNN_PW_MODE: WY leaf panel warp 0 rotate SMSPs per CTA, 1 pin to SMSP 0
     int wy_nw = 0;      // ELMRNN_WY_NW: WY leaf/merge warps per CTA (4 or 8; 0 = by n)
     int max_slabs = 0;  // ELMRNN_TSQR_MAXSLABS: cap on the TSQR leaf count (0 = by size)
+    int wy_2phase = 1;  // ELMRNN_WY_2PHASE: 0 = single-chain WY leaf only; 2 = two-phase also for n <= 320
 };
 
 }  // namespace elm

@@ -831,13 +831,27 @@ __device__ __forceinline__ void wy_panel_rd(double* C, int LDC, int n, int p, do
     }
 }
 
+// A warp group that runs one fold: threads [base, base + threads) of the CTA,
+// its own named barriers (step barrier: 0 = the whole CTA via __syncthreads),
+// and the exclusive end of the panels it factors (p_end = n: the whole fold).
+struct WyGroup {
+    int base, threads, bar_step, bar_la, p_end;
+};
+__device__ __forceinline__ WyGroup wy_whole_cta(int n) { return WyGroup{0, (int)blockDim.x, 0, 1, n}; }
+
 template <int ROWS>
 __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* __restrict__ R, double* Gs,
                         double* Rd, double* cgv, double* cuv, int pw, const int* pred_prog = nullptr,
-                        int* my_prog = nullptr, bool la_wait = false) {
-    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+                        int* my_prog = nullptr, bool la_wait = false, WyGroup grp = WyGroup{0, 0, 0, 1, -1}) {
+    if (grp.threads == 0) grp = wy_whole_cta(n);
+    const int gtid = (int)threadIdx.x - grp.base;
+    const int warp = gtid >> 5, nw = grp.threads >> 5;
     const int tw = warp < pw ? warp : warp - 1;
-    const bool lane0 = (threadIdx.x & 31) == 0 && warp == pw;
+    const bool lane0 = (gtid & 31) == 0 && warp == pw;
+    auto step_sync = [&]() {
+        if (grp.bar_step == 0) __syncthreads();
+        else named_bar_sync(grp.bar_step, grp.threads);
+    };
     // Pipelined merge (k_tsqr_merge_wy_par): the fold of the previous row chunk into
     // the same R publishes the number of panel steps it has completed; step p of
     // this fold touches R rows p .. p+47 (trailing rows, look-ahead panel, diagonal
@@ -847,15 +861,19 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
     auto wait_pred = [&](int need) {
         if (!pred_prog) return;
         need = min(need, npan);
-        if (threadIdx.x == 0)
+        if (gtid == 0)
             while (ld_acquire_gpu(pred_prog) < need) __nanosleep(64);
-        __syncthreads();
+        step_sync();
     };
     auto publish = [&](int v) {
-        if (my_prog && threadIdx.x == 0) {
+        if (my_prog && gtid == 0) {
             __threadfence();
             st_release_gpu(my_prog, v);
         }
+    };
+    // the R diagonal block of panel q is read only for panels this group factors
+    auto rd_next = [&](int q, double (&rr)[8]) {
+        if (q < grp.p_end) rd_load(R, n, q, rr);
     };
     int p = k0, buf = 0;
     double rdn[8];   // panel warp: next panel's R diagonal block
@@ -863,13 +881,14 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
     if (warp == pw) {
         rd_load(R, n, p, rdn);
         rd_put(Rd, rdn);
-        rd_load(R, n, p + kNBW, rdn);
+        rd_next(p + kNBW, rdn);
         wy_panel_rd<ROWS>(C, LDC, n, p, R, Rd, cgv, cuv, Gs);
     }
-    __syncthreads();
+    step_sync();
     for (;;) {
         const int pe = p + min(kNBW, n - p);
         if (pe >= n) break;   // no trailing columns (so below nbp == kNBW)
+        const bool fact = pe < grp.p_end;   // does this group factor panel pe (look-ahead)?
         wait_pred(p / kNBW + 3);
         if (lane0) qr_ev(0, p);
         const int nbn = min(kNBW, n - pe);
@@ -877,31 +896,37 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
         if (nw == 1) {
             wy_trailing<ROWS>(C, LDC, n, p, pe, n, 0, 1, R, G0, g0, u0);
             __syncwarp();
-            rd_put(Rd, rdn);
-            rd_load(R, n, pe + kNBW, rdn);
-            wy_panel_rd<ROWS>(C, LDC, n, pe, R, Rd, cgv + (buf ^ 1) * kNBW, cuv + (buf ^ 1) * kNBW,
-                              Gs + (buf ^ 1) * kNBW * kNBW);
+            if (fact) {
+                rd_put(Rd, rdn);
+                rd_next(pe + kNBW, rdn);
+                wy_panel_rd<ROWS>(C, LDC, n, pe, R, Rd, cgv + (buf ^ 1) * kNBW, cuv + (buf ^ 1) * kNBW,
+                                  Gs + (buf ^ 1) * kNBW * kNBW);
+            }
         } else if (warp == pw) {
             // look-ahead: wait until panel p+1's columns carry panel p's update, factor it
-            rd_put(Rd, rdn);
-            rd_load(R, n, pe + kNBW, rdn);
-            named_bar_sync(1, nw * 32);
+            if (fact) {
+                rd_put(Rd, rdn);
+                rd_next(pe + kNBW, rdn);
+            }
+            named_bar_sync(grp.bar_la, grp.threads);
             if (lane0) qr_ev(1, p);
-            wy_panel_rd<ROWS>(C, LDC, n, pe, R, Rd, cgv + (buf ^ 1) * kNBW, cuv + (buf ^ 1) * kNBW,
-                              Gs + (buf ^ 1) * kNBW * kNBW);
+            if (fact)
+                wy_panel_rd<ROWS>(C, LDC, n, pe, R, Rd, cgv + (buf ^ 1) * kNBW, cuv + (buf ^ 1) * kNBW,
+                                  Gs + (buf ^ 1) * kNBW * kNBW);
             if (lane0) qr_ev(5, p);
         } else {
             wy_trailing<ROWS>(C, LDC, n, p, pe, pe + nbn, tw, nw - 1, R, G0, g0, u0);   // panel p+1's columns first
             __threadfence_block();
-            // warps without a look-ahead tile wait with the panel warp (ELMRNN_WY_LA_WAIT, testing
-            // aid) so the look-ahead chain is not slowed by their trailing work
-            if (la_wait && 8 * tw >= nbn) named_bar_sync(1, nw * 32);
-            else named_bar_arrive(1, nw * 32);
+            // warps without a look-ahead tile wait with the panel warp so the
+            // look-ahead chain is not slowed by their trailing work
+            if (la_wait && 8 * tw >= nbn) named_bar_sync(grp.bar_la, grp.threads);
+            else named_bar_arrive(grp.bar_la, grp.threads);
             wy_trailing<ROWS>(C, LDC, n, p, pe + nbn, n, tw, nw - 1, R, G0, g0, u0);
         }
-        __syncthreads();
+        step_sync();
         if (lane0) qr_ev(2, p);
         publish(p / kNBW + 1);
+        if (!fact) break;     // phase end: panels >= p_end belong to the next group
         p = pe;
         buf ^= 1;   // the panel warp wrote G of the new panel p with its reflectors
     }
@@ -1010,6 +1035,116 @@ __global__ void __launch_bounds__(32 * NW, (NW == 4 && ROWS <= 32) ? 3 : 1)
         }
         __syncthreads();
         wy_fold<ROWS>(C, LDC, n, 0, R, Gs, Rd, cgv, cuv, pw, nullptr, nullptr, la_wait != 0);
+    }
+    if (bad) atomicOr(flag, 1);
+}
+
+// ---- two-phase pipelined WY leaf ----------------------------------------------------
+// The fold of a tile is a chain of npan panel steps (the panel warp's dependency
+// latency); the trailing warps wait on it most of the time, and one 32-row fp64
+// tile per chain fills a third of shared memory.  Split the chain: group A
+// factors panels [0, p_split) of tile k (trailing updates over all columns)
+// while group B factors panels [p_split, n) of tile k-1 -- the two touch
+// disjoint R rows, so they need no synchronisation until the period ends.  A
+// tile past phase A only needs its columns >= p_split, so group B's buffer is
+// half the size: two chains for 1.5 tiles of shared memory.
+__host__ __device__ constexpr int wy2_split(int n) { return 16 * (((n + kNBW - 1) / kNBW + 1) / 2); }
+__host__ __device__ constexpr size_t wy2_aux_doubles() { return (size_t)kNBW * kNBW * 3 + 4 * kNBW; }
+__host__ __device__ constexpr size_t wy2_smem_bytes(int rows, int n) {
+    return ((size_t)rows * wy_ldc(n) + (size_t)rows * wy_ldc(n - wy2_split(n)) + 2 * wy2_aux_doubles()) * sizeof(double);
+}
+
+template <int ROWS, int NWA, int NWB>
+__global__ void __launch_bounds__(32 * (NWA + NWB), (NWA + NWB) * 32 * 168 * 2 <= 65536 ? 2 : 1)
+    k_tsqr_leaf_wy2(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t ldy, int P,
+                    int64_t N, int M, double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag,
+                    int la_wait) {
+    extern __shared__ __align__(16) double wsm[];
+    const int n = M + P, LDC = wy_ldc(n), ps = wy2_split(n), LDCB = wy_ldc(n - ps);
+    double* bufA = wsm;
+    double* auxA = bufA + (size_t)ROWS * LDC;
+    double* bufB = auxA + wy2_aux_doubles();
+    double* auxB = bufB + (size_t)ROWS * LDCB;
+    // aux: Gs [2][16][16] | Rd [16][16] | cgv [2][16] | cuv [2][16]
+    auto Gs = [](double* a) { return a; };
+    auto Rd = [](double* a) { return a + 2 * kNBW * kNBW; };
+    auto cg = [](double* a) { return a + 3 * kNBW * kNBW; };
+    auto cu = [](double* a) { return a + 3 * kNBW * kNBW + 2 * kNBW; };
+    constexpr int TA = 32 * NWA, TB = 32 * NWB;
+    const WyGroup gA{0, TA, 2, 1, ps}, gB{TA, TB, 4, 3, n};
+    const bool inA = (int)threadIdx.x < TA;
+    double* R = Rws + (size_t)blockIdx.x * n * n;
+    for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) R[e] = 0.0;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+    const int64_t r1 = min(N, r0 + rows_per_cta);
+    const int64_t ntiles = r1 > r0 ? (r1 - r0 + ROWS - 1) / ROWS : 0;
+    bool bad = false;
+    const bool vec = (M % 4 == 0) && (ldh % 4 == 0) && ((reinterpret_cast<uintptr_t>(H) & 15) == 0);
+    const int M4 = M / 4, tail = LDC - M;
+    __syncthreads();
+    for (int64_t k = 0; k <= ntiles; ++k) {
+        if (inA) {
+            if (k < ntiles) {
+                const int tid = threadIdx.x, nt = TA;
+                const int64_t base = r0 + k * ROWS;
+                if (vec) {   // 16-B evict-first loads, 8 in flight per thread
+                    constexpr int B = 8;
+                    for (int e0 = tid; e0 < ROWS * M4; e0 += nt * B) {
+                        float4 v[B];
+#pragma unroll
+                        for (int b = 0; b < B; ++b) {
+                            const int e = e0 + b * nt, r = e / M4, q = e - r * M4;
+                            v[b] = (e < ROWS * M4 && base + r < r1)
+                                       ? __ldcs(reinterpret_cast<const float4*>(H + (base + r) * ldh) + q)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+#pragma unroll
+                        for (int b = 0; b < B; ++b) {
+                            const int e = e0 + b * nt, r = e / M4, q = e - r * M4;
+                            if (e < ROWS * M4) {
+                                bad |= !(isfinite(v[b].x) && isfinite(v[b].y) && isfinite(v[b].z) && isfinite(v[b].w));
+                                double2* d = reinterpret_cast<double2*>(bufA + (size_t)r * LDC + 4 * q);
+                                d[0] = make_double2(v[b].x, v[b].y);
+                                d[1] = make_double2(v[b].z, v[b].w);
+                            }
+                        }
+                    }
+                    for (int e = tid; e < ROWS * tail; e += nt) {   // Y columns, zero padding
+                        const int r = e / tail, c = M + (e - r * tail);
+                        const int64_t row = base + r;
+                        const float x = (c < n && row < r1) ? __ldg(Y + row * ldy + (c - M)) : 0.0f;
+                        bad |= !isfinite(x);
+                        bufA[(size_t)r * LDC + c] = (double)x;
+                    }
+                } else {
+                    for (int r = 0; r < ROWS; ++r) {
+                        const int64_t row = base + r;
+                        for (int c = tid; c < LDC; c += nt) {
+                            float x = 0.0f;
+                            if (row < r1 && c < n) x = c < M ? __ldg(H + row * ldh + c) : __ldg(Y + row * ldy + (c - M));
+                            bad |= !isfinite(x);
+                            bufA[(size_t)r * LDC + c] = (double)x;
+                        }
+                    }
+                }
+                named_bar_sync(gA.bar_step, TA);
+                wy_fold<ROWS>(bufA, LDC, n, 0, R, Gs(auxA), Rd(auxA), cg(auxA), cu(auxA), 0, nullptr, nullptr,
+                              la_wait != 0, gA);
+            }
+        } else if (k >= 1) {
+            // columns >= ps of tile k-1 live in bufB (column c at bufB[r * LDCB + c - ps])
+            wy_fold<ROWS>(bufB - ps, LDCB, n, ps, R, Gs(auxB), Rd(auxB), cg(auxB), cu(auxB), 0, nullptr, nullptr,
+                          la_wait != 0, gB);
+        }
+        __syncthreads();
+        if (k < ntiles) {   // tile k moves on to phase B
+            const int w = LDC - ps;
+            for (int e = threadIdx.x; e < ROWS * w; e += blockDim.x) {
+                const int r = e / w, c = e - r * w;
+                bufB[(size_t)r * LDCB + c] = bufA[(size_t)r * LDC + ps + c];
+            }
+        }
+        __syncthreads();
     }
     if (bad) atomicOr(flag, 1);
 }
@@ -1156,11 +1291,41 @@ static auto wy_dispatch_merge(int n, F&& f) {
     return wy_nw_dispatch<16>(nw, f);
 }
 
+// Two-phase pipelined WY leaf (k_tsqr_leaf_wy2) for n > 160 when its two tile
+// buffers fit: (rows, warps of phase A, warps of phase B).  0 rows: not used.
+struct Wy2Cfg { int rows, nwa, nwb; };
+static Wy2Cfg wy2_cfg(const elmrnn* h, int n) {
+    // n <= 320: the single-chain leaf with 3 CTAs/SM measured faster (C4 shape 67.7
+    // vs 77.4 ms with 4+2-warp two-phase CTAs); n = 401: 46.6 vs 56.6 ms, n = 513:
+    // 135.5 vs 155.1, n = 1025: 789 vs 803 (tools/wy_variants.sh)
+    if (h->tune.wy_2phase == 0 || n <= 160 || h->tune.wy_rows) return {0, 0, 0};
+    if (n <= 320) return h->tune.wy_2phase == 2 ? Wy2Cfg{32, 4, 2} : Wy2Cfg{0, 0, 0};
+    if (wy2_smem_bytes(32, n) <= 220 * 1024) return {32, 8, 4};
+    if (wy2_smem_bytes(16, n) <= 220 * 1024) return {16, 8, 4};
+    return {0, 0, 0};
+}
+template <class F>
+static auto wy2_dispatch(const Wy2Cfg& c, F&& f) {
+    if (c.rows == 32 && c.nwa == 4) return f(std::integral_constant<int, 32>{}, std::integral_constant<int, 4>{},
+                                             std::integral_constant<int, 2>{});
+    if (c.rows == 32) return f(std::integral_constant<int, 32>{}, std::integral_constant<int, 8>{},
+                               std::integral_constant<int, 4>{});
+    return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 8>{}, std::integral_constant<int, 4>{});
+}
+
 int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N) {
     const int n = h->M + h->nrhs;
     const Var v = pick_var(n);
     const int threads = var_threads(v, n);
-    int per_sm = use_wy_h(h) ? wy_dispatch(h, n, [&](auto rows, auto nwc) {
+    const Wy2Cfg c2 = use_wy_h(h) ? wy2_cfg(h, n) : Wy2Cfg{0, 0, 0};
+    int per_sm = c2.rows ? wy2_dispatch(c2, [&](auto rows, auto na, auto nb) {
+        constexpr int RW = decltype(rows)::value, NA = decltype(na)::value, NB = decltype(nb)::value;
+        const size_t sm = wy2_smem_bytes(RW, n);
+        cudaFuncSetAttribute(k_tsqr_leaf_wy2<RW, NA, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        int ps = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_tsqr_leaf_wy2<RW, NA, NB>, 32 * (NA + NB), sm);
+        return ps < 1 ? 1 : ps;
+    }) : use_wy_h(h) ? wy_dispatch(h, n, [&](auto rows, auto nwc) {
         constexpr int RW = decltype(rows)::value, NW = decltype(nwc)::value;
         const size_t sm = wy_leaf_smem(RW, n);
         cudaFuncSetAttribute(k_tsqr_leaf_wy<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1270,10 +1435,24 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
     cudaError_t e;
     if ((e = ensure_solve_ws(h, wide_solve(h) && slabs < 2 ? 2 : slabs))) return e;   // wide solve: slab 1 = ridge rows
     if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream))) return e;
-    const int rows_tile = use_wy_h(h) ? wy_rows(h, n) : var_rows(v);
+    const Wy2Cfg c2 = use_wy_h(h) ? wy2_cfg(h, n) : Wy2Cfg{0, 0, 0};
+    const int rows_tile = c2.rows ? c2.rows : use_wy_h(h) ? wy_rows(h, n) : var_rows(v);
     int64_t rows = (N + slabs - 1) / slabs;
     rows = (rows + rows_tile - 1) / rows_tile * rows_tile;
     const int threads = var_threads(v, n);
+    if (c2.rows) {
+        e = wy2_dispatch(c2, [&](auto rws, auto na, auto nb) {
+            constexpr int RW = decltype(rws)::value, NA = decltype(na)::value, NB = decltype(nb)::value;
+            const size_t sm = wy2_smem_bytes(RW, n);
+            cudaFuncSetAttribute(k_tsqr_leaf_wy2<RW, NA, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_tsqr_leaf_wy2<RW, NA, NB><<<(unsigned)slabs, 32 * (NA + NB), sm, h->stream>>>(
+                H, ldh, Y, ldy, h->nrhs, N, h->M, h->Rws, rows, h->flag, wy_la_wait(n));
+            h->launches++;
+            return cudaGetLastError();
+        });
+        if (e) return e;
+        return tree(h, slabs);
+    }
     if (use_wy_h(h)) {
         e = wy_dispatch(h, n, [&](auto rws, auto nwc) {
             constexpr int RW = decltype(rws)::value, NW = decltype(nwc)::value;

@@ -319,7 +319,8 @@ def _packed_to_R(Rpk, n):
     return R
 
 
-@pytest.mark.parametrize("M,N", [(200, 1001), (256, 20011), (300, 5003), (511, 3001), (129, 777)])
+@pytest.mark.parametrize("M,N", [(200, 1001), (256, 20011), (300, 5003), (511, 3001), (129, 777), (256, 40),
+                                 (400, 70000), (1024, 9000)])
 def test_tsqr_wy_and_fold_agree(M, N, monkeypatch):
     """The blocked compact-WY TSQR (k_tsqr_leaf_wy, UT-transform trailing update on
     f64 tensor cores) and the per-column fold produce the same R of [H | Y] as
@@ -328,15 +329,20 @@ def test_tsqr_wy_and_fold_agree(M, N, monkeypatch):
     H = torch.rand(N, M, device="cuda", generator=g) - 0.5
     Y = torch.rand(N, device="cuda", generator=g) - 0.5
     n = M + 1
-    Rn = np.abs(np.linalg.qr(np.column_stack([H.double().cpu().numpy(), Y.double().cpu().numpy()]), mode="r"))
+    Rq = np.abs(np.linalg.qr(np.column_stack([H.double().cpu().numpy(), Y.double().cpu().numpy()]), mode="r"))
+    Rn = np.zeros((n, n))
+    Rn[: Rq.shape[0]] = Rq   # N < n: the trailing rows of R are zero
     scale = Rn.max()
-    for wy in ("1", "0"):
+    # blocked WY (two-phase pipelined leaf, forced for n <= 320 too, and the single-chain
+    # leaf), per-column fold
+    for wy, two in (("1", "2"), ("1", "0"), ("0", "1")):
         monkeypatch.setenv("ELMRNN_TESTING", "1")
         monkeypatch.setenv("ELMRNN_TSQR_WY", wy)
+        monkeypatch.setenv("ELMRNN_WY_2PHASE", two)
         e = E("lstm", 1, M, 4, 1, force_path=1)
         R = _packed_to_R(e.solve_local(H, Y).cpu().numpy(), n)
         assert np.isfinite(R).all()
-        assert np.abs(np.abs(R) - Rn).max() <= 1e-12 * scale, wy
+        assert np.abs(np.abs(R) - Rn).max() <= 1e-12 * scale, (wy, two)
 
 
 @pytest.mark.parametrize("rows,M,N", [("16", 511, 600), ("16", 300, 3001), ("32", 1000, 1500)])
