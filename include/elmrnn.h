@@ -247,7 +247,11 @@ ELMRNN_API elmrnn_status elmrnn_sync(elmrnn_t h);
 ELMRNN_API int64_t elmrnn_packed_r_len(elmrnn_t h);
 
 /* Eq. 4: Yhat[i] = sum_j beta_j H(Q)[i][j] (no output bias, R16),
- * building H(Q) internally with the same kernels as elmrnn_build_H.
+ * fused into the H builders: the same kernels as
+ * elmrnn_build_H run with a readout epilogue that writes no H(Q), only the fp64
+ * partial products of each thread's H(Q) row segment with beta (<= max(4,
+ * ceil(M/32)+1) doubles per row, a library workspace); a finish kernel sums each
+ * row's partials in a fixed order (bitwise repeatable) and rounds once to fp32.
  * X, Yfb as in elmrnn_build_H; beta dev fp64 [M]; Yhat dev fp32 [N].
  * Errors: ARG, SHAPE, OOM, CUDA. */
 ELMRNN_API elmrnn_status elmrnn_predict(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb,
@@ -260,8 +264,9 @@ ELMRNN_API elmrnn_status elmrnn_predict(elmrnn_t h, const float* X, int64_t ldx,
  * the prediction in as the next observation: w_{k+1} = (w_k[1:], fp32(yhat_k)).
  *   X dev fp32 [N][ldx], ldx >= Q; beta dev fp64 [M];
  *   Yhat dev fp32 [N][ldyh] output, Yhat[i][k] = yhat_k of window i, ldyh >= K.
- * Runs K (build_H, predict-and-shift) rounds on the handle's stream with a
- * library workspace of N*(Q+1) + N*M floats.  N == 0 or K == 0 is a no-op.
+ * Runs K (fused build -> readout, shift) rounds on the handle's stream with
+ * library workspaces of N*(Q+1) floats (windows) and the readout partials of
+ * elmrnn_predict.  N == 0 or K == 0 is a no-op.
  * Errors: ARG, SHAPE, UNSUPPORTED (d != 1, Q > 128), OOM, CUDA. */
 ELMRNN_API elmrnn_status elmrnn_forecast(elmrnn_t h, const float* X, int64_t ldx, int64_t N,
                               const double* beta, int K, float* Yhat, int64_t ldyh);

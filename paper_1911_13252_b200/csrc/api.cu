@@ -284,13 +284,33 @@ elmrnn_status elmrnn_sync(elmrnn_t h) {
     return ELMRNN_OK;
 }
 
-// Readout (Eq. 4) row chunk: H(Q) of a chunk is built into a workspace of at
-// most 32 MB that stays resident in the 126 MB L2 while the readout kernel
-// consumes it, so H never round-trips HBM and the workspace does not grow with N.
-static int64_t readout_chunk_rows(const elmrnn* h, int64_t N) {
-    int64_t rows = ((int64_t)32 << 20) / ((int64_t)4 * h->M);
-    rows = rows < 8192 ? 8192 : (rows / 128) * 128;
-    return rows < N ? rows : N;
+// Fused readout (Eq. 4): the builder runs with the
+// readout sink set, so it writes no H(Q) -- only the fp64 partial products of
+// its H(Q) row segments with beta (4 or fewer slots per row, elmrnn::ro_slots) --
+// and k_readout_finish sums each row's slots in a fixed order.  With w != null
+// the finish also shifts the forecast window (reading R31).
+static elmrnn_status readout_impl(elmrnn* h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy, int64_t N,
+                                  const double* beta, float* yout, int64_t ldyo, float* w = nullptr,
+                                  int64_t ldw = 0) {
+    cudaError_t e;
+    const int64_t need = (int64_t)elm::ro_max_slots(h->M) * N;
+    if (need > h->ypws_len) {
+        if (h->ypws) cudaFree(h->ypws);
+        h->ypws = nullptr;
+        h->ypws_len = 0;
+        if ((e = cudaMalloc(&h->ypws, sizeof(double) * need))) return cuda_fail(h, e, "readout workspace");
+        h->ypws_len = need;
+    }
+    h->ro_beta = beta;
+    h->ro_yp = h->ypws;
+    h->ro_slots = 0;
+    elmrnn_status st = build_impl(h, X, ldx, Yfb, ldy, N, nullptr, 0);
+    h->ro_beta = nullptr;
+    h->ro_yp = nullptr;
+    if (st != ELMRNN_OK) return st;
+    if (h->ro_slots == 0) return fail(h, ELMRNN_ERR_CUDA, "builder without a readout sink");
+    if ((e = launch_readout_finish(h, h->ypws, N, h->ro_slots, yout, ldyo, w, ldw))) return cuda_fail(h, e, "readout");
+    return ELMRNN_OK;
 }
 
 static cudaError_t ensure_hws(elmrnn* h, int64_t N) {
@@ -420,16 +440,7 @@ elmrnn_status elmrnn_predict(elmrnn_t h, const float* X, int64_t ldx, const floa
     if (!X || !beta || !Yhat) return fail(h, ELMRNN_ERR_ARG, "NULL pointer");
     if (ldx < (int64_t)h->Q * h->S) return fail(h, ELMRNN_ERR_SHAPE, "ldx < Q*d");
     if (Yfb && ldy < h->Q) return fail(h, ELMRNN_ERR_SHAPE, "ldy < Q");
-    cudaError_t e;
-    const int64_t chunk = readout_chunk_rows(h, N);
-    if ((e = ensure_hws(h, chunk))) return cuda_fail(h, e, "predict workspace");
-    for (int64_t r0 = 0; r0 < N; r0 += chunk) {   // build a chunk into the L2-resident workspace, read it out
-        const int64_t nr = N - r0 < chunk ? N - r0 : chunk;
-        elmrnn_status st = build_impl(h, X + r0 * ldx, ldx, Yfb ? Yfb + r0 * ldy : nullptr, ldy, nr, h->Hws, h->M);
-        if (st != ELMRNN_OK) return st;
-        if ((e = launch_predict_gemv(h, h->Hws, h->M, nr, beta, Yhat + r0))) return cuda_fail(h, e, "predict");
-    }
-    return ELMRNN_OK;
+    return readout_impl(h, X, ldx, Yfb, ldy, N, beta, Yhat, 1);
 }
 
 static int64_t forecast_ldw(const elmrnn* h) { return (h->Q + 3) & ~3; }   // 16-B aligned window rows
@@ -453,19 +464,11 @@ elmrnn_status elmrnn_forecast(elmrnn_t h, const float* X, int64_t ldx, int64_t N
         if ((e = cudaMalloc(&h->fws, sizeof(float) * N * (ldw + 1)))) return cuda_fail(h, e, "forecast workspace");
         h->fws_rows = N;
     }
-    const int64_t chunk = readout_chunk_rows(h, N);
-    if ((e = ensure_hws(h, chunk))) return cuda_fail(h, e, "forecast workspace");
     if ((e = launch_window_init(h, X, ldx, N, h->fws, ldw))) return cuda_fail(h, e, "forecast");
-    // rows are independent: each chunk runs its K steps with H(Q) in the L2-resident workspace
-    for (int64_t r0 = 0; r0 < N; r0 += chunk) {
-        const int64_t nr = N - r0 < chunk ? N - r0 : chunk;
-        float* w = h->fws + r0 * ldw;
-        for (int k = 0; k < K; ++k) {
-            elmrnn_status st = build_impl(h, w, ldw, nullptr, 0, nr, h->Hws, h->M);
-            if (st != ELMRNN_OK) return st;
-            if ((e = launch_predict_shift(h, h->Hws, h->M, nr, beta, w, ldw, Yhat + r0 * ldyh + k, ldyh)))
-                return cuda_fail(h, e, "forecast");
-        }
+    // per step: the fused readout of the current windows, then the window shift (in the finish)
+    for (int k = 0; k < K; ++k) {
+        elmrnn_status st = readout_impl(h, h->fws, ldw, nullptr, 0, N, beta, Yhat + k, ldyh, h->fws, ldw);
+        if (st != ELMRNN_OK) return st;
     }
     return ELMRNN_OK;
 }
@@ -527,7 +530,7 @@ const char* elmrnn_last_error(elmrnn_t h) { return h ? h->err.c_str() : g_init_e
 void elmrnn_destroy(elmrnn_t h) {
     if (!h) return;
     cudaFree(h->W); cudaFree(h->b); cudaFree(h->rec); cudaFree(h->tc_ops);
-    cudaFree(h->Rws); cudaFree(h->sdev); cudaFree(h->flag); cudaFree(h->Hws); cudaFree(h->prog); cudaFree(h->rho_multi); cudaFree(h->rws); cudaFree(h->fws); cudaFree(h->dscr); cudaFree(h->scratch);
+    cudaFree(h->Rws); cudaFree(h->sdev); cudaFree(h->flag); cudaFree(h->Hws); cudaFree(h->prog); cudaFree(h->rho_multi); cudaFree(h->rws); cudaFree(h->fws); cudaFree(h->dscr); cudaFree(h->scratch); cudaFree(h->ypws);
     if (h->shost) cudaFreeHost(h->shost);
     delete h;
 }

@@ -82,6 +82,16 @@ struct elmrnn {
     int64_t Hws_rows;
     float* scratch;       // builder scratch (FC history ring)
     size_t scratch_bytes;
+    // fused readout sink (Eq. 4): while ro_beta is set, a builder
+    // writes no H(Q) but the fp64 partial dot products of its H(Q) row segments with
+    // beta, slot s of row i at ro_yp[s * N + i]; the launcher reports the slot layout
+    // in ro_slots (K > 0: K slots per row; kRoCellSlots: the 32-cell warp groups a row
+    // spans) and elm::launch_readout_finish sums the slots in a fixed order
+    const double* ro_beta;
+    double* ro_yp;
+    int ro_slots;
+    double* ypws;         // readout slot workspace
+    int64_t ypws_len;
     int64_t launches;
     elm::Tune tune;
     std::string err;
@@ -101,8 +111,6 @@ cudaError_t launch_diag_gated(elmrnn* h, const float* X, int64_t ldx, int64_t N,
 cudaError_t launch_teacher_forced(elmrnn* h, const float* X, int64_t ldx, const float* Yfb, int64_t ldy,
                                   int64_t N, float* H, int64_t ldh, const float* Ef = nullptr, int64_t lde = 0);
 cudaError_t launch_window_init(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* w, int64_t ldw);
-cudaError_t launch_predict_shift(elmrnn* h, const float* H, int64_t ldh, int64_t N, const double* beta, float* w,
-                                 int64_t ldw, float* yout, int64_t ldyo);
 cudaError_t launch_rmse(elmrnn* h, const float* yhat, const float* y, int64_t N, double* out);
 cudaError_t launch_error_windows(elmrnn* h, const float* H, int64_t ldh, const float* Y, int64_t N,
                                  const double* beta, float* Ef, int64_t lde);
@@ -137,7 +145,14 @@ cudaError_t tsqr_merge_packed(elmrnn* h, const double* Rpk_all, int P);
 cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta);
 cudaError_t ensure_solve_ws(elmrnn* h, int64_t slabs);
 int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N);
-cudaError_t launch_predict_gemv(elmrnn* h, const float* H, int64_t ldh, int64_t N, const double* beta, float* yhat);
+
+// ---- fused readout (readout.cu) ---------------------------------------------------
+constexpr int kRoCellSlots = -1;   // slot = 32-cell group index - first group of the row
+inline int ro_max_slots(int M) { return 4 > (M + 31) / 32 + 1 ? 4 : (M + 31) / 32 + 1; }
+// yhat_i = fp32(sum of row i's slots, in slot order); with w != null also
+// w_i <- (w_i[1:], yhat_i) (the free-running forecast step, reading R31)
+cudaError_t launch_readout_finish(elmrnn* h, const double* yp, int64_t N, int slots, float* yout, int64_t ldyo,
+                                  float* w, int64_t ldw);
 
 }  // namespace elm
 
@@ -188,6 +203,24 @@ __device__ __forceinline__ float tanh_acc(float x) { return tanhf(x); }
 // 4.3 vs 3.8 floors with tanhf at 10% less build time (C3 GRU); the LSTM keeps
 // tanhf (2.1-2.3 vs 3.9-5.8 floors with this form).
 __device__ __forceinline__ float tanh_e2_sig(float a2) { return fmaf(2.0f, sig_e2(-a2), -1.0f); }
+
+// Fused readout of the flattened-cell builders (cell c = i*M + j, 32 consecutive
+// cells per warp): per row segment of the warp, sum v over its lanes (fixed
+// shuffle order: deterministic) and store it from the segment's first lane into
+// slot (c/32 - (i*M)/32) of row i (kRoCellSlots layout).  All 32 lanes must call.
+__device__ __forceinline__ void ro_cell_store(double v, int64_t cell, int64_t N, int M, double* yp) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = cell / M;
+    const int64_t last = min((i + 1) * (int64_t)M, N * (int64_t)M) - 1;   // last cell of row i
+    const int seg_end = (int)min((int64_t)31, (last - cell) + lane);       // lane of that cell in this warp
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const double t = __shfl_down_sync(0xffffffffu, v, off);
+        if (lane + off <= seg_end) v += t;
+    }
+    const bool head = lane == 0 || cell % M == 0;
+    if (head && cell < N * (int64_t)M) yp[(cell / 32 - (i * M) / 32) * N + i] = v;
+}
 
 // Fast MUFU forms (ex2.approx / rcp.approx, ~2 ulp each) for epilogues that
 // are MUFU bound; accuracy validated by the parity tests of the kernel using them.

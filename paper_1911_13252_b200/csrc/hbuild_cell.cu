@@ -8,6 +8,8 @@
 // Elman's lag history lives in registers (fully unrolled over a compile-time
 // bound QMAX >= Q) instead of the paper's global H[Row,Col,t] round trips.
 // Both kernels are bound by HBM (H stores) or by MUFU, never by FMA.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace elm {
@@ -25,9 +27,12 @@ template <int QMAX, typename T = double>
 __global__ void __launch_bounds__(256) k_elman(const float* __restrict__ X, int64_t ldx, int64_t N, int S, int M,
                                                int Q, int act, const float* __restrict__ W,
                                                const float* __restrict__ b, const float* __restrict__ alT,
-                                               float* __restrict__ H, int64_t ldh) {
-    int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (cell >= N * (int64_t)M) return;
+                                               float* __restrict__ H, int64_t ldh, const double* __restrict__ rbeta,
+                                               double* __restrict__ ryp) {
+    const int64_t cell0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool live = cell0 < N * (int64_t)M;
+    if (!live && !rbeta) return;   // the fused readout needs every lane of the warp
+    const int64_t cell = live ? cell0 : 0;
     int64_t i = cell / M;
     int j = (int)(cell - i * M);
     const float* xi = X + i * ldx;
@@ -72,7 +77,8 @@ __global__ void __launch_bounds__(256) k_elman(const float* __restrict__ X, int6
             last = h[t];
         }
     }
-    H[i * ldh + j] = (float)last;
+    if (rbeta) ro_cell_store(live ? (double)(float)last * __ldg(rbeta + j) : 0.0, cell0, N, M, ryp);   // Eq. 4
+    else H[i * ldh + j] = (float)last;
 }
 
 bool elman_supported(int Q) { return Q >= 1 && Q <= 128; }
@@ -87,10 +93,13 @@ bool elman_supported(int Q) { return Q >= 1 && Q <= 128; }
 template <bool IS_LSTM, int SS>
 __global__ void __launch_bounds__(256) k_diag_gated(const float* __restrict__ X, int64_t ldx, int64_t N, int S, int M,
                                                     int Q, const float* __restrict__ W, const float* __restrict__ b,
-                                                    const float* __restrict__ u, float* __restrict__ H, int64_t ldh) {
+                                                    const float* __restrict__ u, float* __restrict__ H, int64_t ldh,
+                                                    const double* __restrict__ rbeta, double* __restrict__ ryp) {
     constexpr int G = IS_LSTM ? 4 : 3;
-    const int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (cell >= N * (int64_t)M) return;
+    const int64_t cell0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool live = cell0 < N * (int64_t)M;
+    if (!live && !rbeta) return;   // the fused readout needs every lane of the warp
+    const int64_t cell = live ? cell0 : 0;
     const int64_t i = cell / M;
     const int j = (int)(cell - i * M), GM = G * M;
     const float* xi = X + i * ldx;
@@ -135,7 +144,8 @@ __global__ void __launch_bounds__(256) k_diag_gated(const float* __restrict__ X,
             h = fmaf(z, nn - h, h);   // (1 - z) h + z n
         }
     }
-    H[i * ldh + j] = h;
+    if (rbeta) ro_cell_store(live ? (double)h * __ldg(rbeta + j) : 0.0, cell0, N, M, ryp);   // Eq. 4
+    else H[i * ldh + j] = h;
 }
 
 cudaError_t launch_diag_gated(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh) {
@@ -144,8 +154,10 @@ cudaError_t launch_diag_gated(elmrnn* h, const float* X, int64_t ldx, int64_t N,
     const int64_t blocks = (cells + threads - 1) / threads;
     if (blocks > INT32_MAX) return cudaErrorInvalidConfiguration;
     auto go = [&](auto kern) {
-        kern<<<(unsigned)blocks, threads, 0, h->stream>>>(X, ldx, N, h->S, h->M, h->Q, h->W, h->b, h->rec, H, ldh);
+        kern<<<(unsigned)blocks, threads, 0, h->stream>>>(X, ldx, N, h->S, h->M, h->Q, h->W, h->b, h->rec, H, ldh,
+                                                         h->ro_beta, h->ro_yp);
     };
+    h->ro_slots = kRoCellSlots;
     const bool lstm = h->arch == kArchLSTMDiag;
     const int S = h->S;
     if (lstm) {
@@ -166,8 +178,9 @@ cudaError_t launch_elman(elmrnn* h, const float* X, int64_t ldx, int64_t N, floa
     if (blocks > INT32_MAX) return cudaErrorInvalidConfiguration;
     auto go = [&](auto kern) {
         kern<<<(unsigned)blocks, threads, 0, h->stream>>>(X, ldx, N, h->S, h->M, h->Q, h->act, h->W, h->b, h->rec, H,
-                                                         ldh);
+                                                         ldh, h->ro_beta, h->ro_yp);
     };
+    h->ro_slots = kRoCellSlots;
     const int Q = h->Q;
     if (h->arch == kArchFCEq8) {
         if (Q <= 8) go(k_elman<8, float>);
@@ -206,7 +219,8 @@ __global__ void __launch_bounds__(256) k_teacher_forced(const float* __restrict_
                                                         const float* __restrict__ W, const float* __restrict__ b,
                                                         const float* __restrict__ recT, float* __restrict__ H,
                                                         int64_t ldh, const float* __restrict__ Ef, int64_t lde,
-                                                        int nerr, const float* __restrict__ recE) {
+                                                        int nerr, const float* __restrict__ recE,
+                                                        const double* __restrict__ rbeta, double* __restrict__ ryp) {
     extern __shared__ __align__(16) float tf_sm[];
     float* ys = tf_sm;                          // [nlag][kTfRows]: ys[k-1][r] = y_r(Q-k)
     float* es = ys + nlag * kTfRows;            // [nerr][kTfRows]: es[l-1][r] = e_r(Q-l)
@@ -228,6 +242,9 @@ __global__ void __launch_bounds__(256) k_teacher_forced(const float* __restrict_
         xs[e] = r < rows ? __ldg(X + (r0 + r) * ldx + (int64_t)(Q - 1) * S + s) : 0.0f;
     }
     __syncthreads();
+    double yacc[kTfRows];   // fused readout (Eq. 4): this thread's neurons' share of each row's H . beta
+#pragma unroll
+    for (int r = 0; r < kTfRows; ++r) yacc[r] = 0.0;
     for (int j = threadIdx.x; j < M; j += blockDim.x) {
         float a[kTfRows];
         const float bj = __ldg(b + j);
@@ -269,9 +286,33 @@ __global__ void __launch_bounds__(256) k_teacher_forced(const float* __restrict_
                 a[4 * q + 3] = fmaf(w, v.w, a[4 * q + 3]);
             }
         }
+        if (rbeta) {
+            const double bj = __ldg(rbeta + j);
 #pragma unroll
-        for (int r = 0; r < kTfRows; ++r)
-            if (r < rows) H[(r0 + r) * ldh + j] = act_g(a[r], act);
+            for (int r = 0; r < kTfRows; ++r) yacc[r] = fma((double)act_g(a[r], act), bj, yacc[r]);
+        } else {
+#pragma unroll
+            for (int r = 0; r < kTfRows; ++r)
+                if (r < rows) H[(r0 + r) * ldh + j] = act_g(a[r], act);
+        }
+    }
+    if (rbeta) {   // reduce over the CTA's neurons in a fixed order: lanes (shuffle tree), then warps
+        __syncthreads();   // the staged windows are no longer read: reuse that shared memory
+        double* red = reinterpret_cast<double*>(tf_sm);   // [warp][row]
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = (int)(blockDim.x >> 5);
+#pragma unroll
+        for (int r = 0; r < kTfRows; ++r) {
+            double v = yacc[r];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == r) red[warp * kTfRows + r] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < rows) {
+            double v = 0.0;
+            for (int w = 0; w < nwarp; ++w) v += red[w * kTfRows + threadIdx.x];
+            ryp[r0 + threadIdx.x] = v;
+        }
     }
 }
 
@@ -283,7 +324,8 @@ cudaError_t launch_teacher_forced(elmrnn* h, const float* X, int64_t ldx, const 
     if (h->arch == kArchNarmax) nlag = h->F < h->Q - 1 ? h->F : h->Q - 1;
     const bool ef = Ef && h->arch == kArchNarmax;
     const int nerr = ef ? (h->R < h->Q - 1 ? h->R : h->Q - 1) : 0;
-    const size_t smem = sizeof(float) * kTfRows * (size_t)(nlag + nerr + h->S);
+    size_t smem = sizeof(float) * kTfRows * (size_t)(nlag + nerr + h->S);
+    if (h->ro_beta) smem = std::max(smem, sizeof(double) * kTfRows * 8);   // readout reduction: [8 warps][rows]
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_teacher_forced, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -293,7 +335,8 @@ cudaError_t launch_teacher_forced(elmrnn* h, const float* X, int64_t ldx, const 
     k_teacher_forced<<<(unsigned)blocks, threads, smem, h->stream>>>(X, ldx, Yfb, ldy, N, h->S, h->M, h->Q, nlag,
                                                                      h->act, h->W, h->b, h->rec, H, ldh,
                                                                      ef ? Ef : nullptr, lde, nerr,
-                                                                     h->rec + (size_t)h->F * h->M);
+                                                                     h->rec + (size_t)h->F * h->M, h->ro_beta, h->ro_yp);
+    h->ro_slots = 1;
     h->launches++;
     return cudaGetLastError();
 }

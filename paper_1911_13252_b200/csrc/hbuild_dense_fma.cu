@@ -29,6 +29,8 @@ struct DenseParams {
     float* H;
     int64_t ldh;
     float* ring_global;  // FC history ring in global memory (nullptr: shared)
+    const double* rbeta; // fused readout (Eq. 4): no H store, ryp[i] = H_i . beta
+    double* ryp;
     int T;               // rows per tile (= 8 * RT)
     int64_t ntiles;
 };
@@ -212,10 +214,21 @@ __global__ void __launch_bounds__(256) k_dense_fma(DenseParams p) {
             }
         }
         const float* hQ = ring + (size_t)(p.Q % nslots) * MT;
-        for (int e = tid; e < T * M; e += blockDim.x) {
-            int r = e / M, j = e - r * M;
-            int64_t i = row0 + r;
-            if (i < p.N) p.H[i * p.ldh + j] = hQ[(size_t)j * T + r];
+        if (p.rbeta) {   // one warp per row: lanes over neurons, fixed shuffle-tree order
+            const int lane = tid & 31;
+            for (int r = tid >> 5; r < T; r += (int)(blockDim.x >> 5)) {
+                double v = 0.0;
+                for (int j = lane; j < M; j += 32) v = fma((double)hQ[(size_t)j * T + r], __ldg(p.rbeta + j), v);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0 && row0 + r < p.N) p.ryp[row0 + r] = v;
+            }
+        } else {
+            for (int e = tid; e < T * M; e += blockDim.x) {
+                int r = e / M, j = e - r * M;
+                int64_t i = row0 + r;
+                if (i < p.N) p.H[i * p.ldh + j] = hQ[(size_t)j * T + r];
+            }
         }
         __syncthreads();
     }
@@ -270,6 +283,8 @@ cudaError_t launch_dense_fma(elmrnn* h, const float* X, int64_t ldx, int64_t N, 
     DenseParams p{};
     p.X = X; p.ldx = ldx; p.N = N; p.S = h->S; p.M = h->M; p.Q = h->Q; p.G = h->G; p.act = h->act;
     p.L = h->fc_lags; p.W = h->W; p.b = h->b; p.U = h->rec; p.H = H; p.ldh = ldh;
+    p.rbeta = h->ro_beta; p.ryp = h->ro_yp;
+    h->ro_slots = 1;
     int RT = 8;
     bool ring_smem = true;
     for (;;) {

@@ -42,7 +42,12 @@ namespace elm {
 namespace {
 
 constexpr int kTcRows = 128;
-constexpr int kTcStages = 3;
+#ifndef ELM_TC256_STAGES
+#define ELM_TC256_STAGES 3
+#endif
+#ifndef ELM_TC_HOLD
+#define ELM_TC_HOLD 1   // hold the last K-slice of h(t) in registers (0: stage it like the others)
+#endif
 constexpr int kTcSliceBytes = 128 * 64 * 2;      // one 128 x 64 fp16 SW128 tile
 constexpr int kTcStageBytes = 2 * kTcSliceBytes;  // hi + lo
 constexpr int kTcEpiWarps = 16;                 // 4 per TMEM lane quadrant, 8 neurons per chunk each
@@ -61,6 +66,9 @@ struct TcParams {
     int two_pass;          // 1: U on the fp16 grid (weight_grid = 1), U_lo = 0 -> hi.hi + lo.hi only
     int debug_no_u;        // ELMRNN_DEBUG_NO_U: skip U streaming after step 0 (timing experiment only)
     int64_t ntiles;
+    uint32_t xbytes;       // a1: bytes of a tile's X block staged by cp.async.bulk (0: x(t) via L1)
+    const double* rbeta;   // fused readout (Eq. 4): no H store; ryp[u * N + row] = H[row][u's neurons] . beta
+    double* ryp;
     float k_sig, k_tanh;   // -log2(e) 2^-sigma, 2 log2(e) 2^-sigma
     unsigned long long* trace;   // optional event trace of CTA 0 (ELMRNN_TRACE), else null
     int trace_cap;
@@ -69,11 +77,17 @@ struct TcParams {
 
 template <int M>
 struct TcCfg {
+    static constexpr int STAGES = M == 256 ? ELM_TC256_STAGES : 3;   // U ring depth
     static constexpr int NCH = M / 32;
     static constexpr int KS = M / 64;
-    static constexpr int ITEMS = NCH * 8;                  // staged words per epilogue thread
+    // staged words per epilogue thread: h(t) hi|lo of chunks 0 .. NCH-3.  The last
+    // K-slice bypasses the staging area (chunk NCH-2 waits in 8 registers for the
+    // last chunk's MMAs to finish, chunk NCH-1 goes straight into TMEM), which
+    // leaves room for the tile's X block next to a 3-stage U ring at M = 256
+    static constexpr int HOLD = ELM_TC_HOLD ? 2 : 0;   // chunks held in registers
+    static constexpr int ITEMS = (NCH - HOLD) * 8;
     static constexpr int STG_BYTES = kTcEpiWarps * ITEMS * 32 * 4;
-    static constexpr int SMEM = 1024 + kTcStages * kTcStageBytes + STG_BYTES + 256;
+    static constexpr int SMEM = 1024 + STAGES * kTcStageBytes + STG_BYTES + 256;   // + the X block
     static constexpr int TMEM_COLS = 512;
     static constexpr int A_HI = 256;                       // TMEM columns of A = h(t-1): hi parts
     static constexpr int A_LO = 256 + M / 2;               //   lo parts (2 fp16 per 32-bit column)
@@ -118,16 +132,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
     using C = TcCfg<M>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int kTcStages = C::STAGES;
     uint8_t* stages = smem;                                                     // U ring
     uint32_t* stg = reinterpret_cast<uint32_t*>(stages + kTcStages * kTcStageBytes);  // h(t) hi|lo staging
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + C::STG_BYTES);
+    float* xbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);   // the tile's X block
     uint64_t* full = bars;                       // [kTcStages]
     uint64_t* empty = bars + kTcStages;          // [kTcStages]
     uint64_t* acc_full = bars + 2 * kTcStages;   // [2]
     uint64_t* acc_empty = acc_full + 2;          // [2]
     uint64_t* a_ready = acc_empty + 2;           // [KS]: K-slice ks of A = h(t-1) is in TMEM
     uint64_t* a_free = a_ready + C::KS;          // [KS]: the last chunk's MMAs no longer read A slice ks
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_free + C::KS);
+    uint64_t* x_full = a_free + C::KS;           // the tile's X block has landed
+    uint64_t* x_empty = x_full + 1;              // every epilogue warp has read its last x(t)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 1);
     uint32_t* trace_cnt = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -142,6 +160,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
         }
         for (int i = 0; i < C::KS; ++i) ptx::mbar_init(a_ready + i, kTcEpiWarps);
         for (int i = 0; i < C::KS; ++i) ptx::mbar_init(a_free + i, 1);
+        ptx::mbar_init(x_full, 1);
+        ptx::mbar_init(x_empty, kTcEpiWarps);
         *trace_cnt = 0;
         ptx::fence_mbar_init();
     }
@@ -159,9 +179,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
         // ---------------- producer: stream U slices (chunk, K-slice) from L2.
         // The whole warp runs the loop (warp-uniform state lives in uniform
         // registers); one elected lane issues.
-        uint32_t st = 0, ph = 0;
+        uint32_t st = 0, ph = 0, xph = 0;
         const uint32_t bytes = p.two_pass ? kTcSliceBytes : kTcStageBytes;   // hi only when U_lo = 0
         for (int64_t s = 0; s < steps_total; ++s) {
+            if (s % p.Q == 0) {   // a new tile: its X block (a1)
+                const int64_t tile = blockIdx.x + (s / p.Q) * gridDim.x;
+                if (ptx::xstage_tile(p.xbytes, tile, p.N))
+                    ptx::xstage_issue(xbuf, p.X, p.ldx, tile, p.xbytes, x_full, x_empty, xph);
+            }
             for (int c = 0; c < C::NCH * C::KS; ++c) {
                 ptx::mbar_wait(empty + st, ph ^ 1);
                 if (ptx::elect_one()) {
@@ -236,8 +261,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
         const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
         const float kS = p.k_sig, kT = p.k_tanh;     // -log2e 2^-sigma, 2 log2e 2^-sigma
         float c[C::NCH * 8];                         // c(t) of neurons n*32 + 8u + 0..7
-        uint32_t ach = 0, aph = 0, afph = 0;
+        uint32_t ach = 0, aph = 0, afph = 0, xph = 0;
         uint32_t* my_stg = stg + (size_t)e * C::ITEMS * 32 + lane;   // [item][lane]
+        uint32_t hold[8];                                             // h(t) hi|lo of chunk NCH-2
         {   // h(0) = 0 for the first tile
             const uint32_t z[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
@@ -275,14 +301,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             const int64_t row = tile * kTcRows + r;
             const bool valid = row < p.N;
-            const float* xrow = p.X + (valid ? row : 0) * p.ldx;
+            const bool xst = ptx::xstage_tile(p.xbytes, tile, p.N);
+            const float* xrow = xst ? xbuf + (int64_t)r * p.ldx : p.X + (valid ? row : 0) * p.ldx;
+            if (xst) {
+                ptx::mbar_wait(x_full, xph);
+                xph ^= 1;
+            }
 #pragma unroll
             for (int i = 0; i < C::NCH * 8; ++i) c[i] = 0.0f;
+            double yacc = 0.0;   // fused readout partial
             for (int t = 1; t <= p.Q; ++t) {
                 float xs[SS];
 #pragma unroll
                 for (int s = 0; s < SS; ++s)
-                    xs[s] = (valid && s < p.S) ? __ldg(xrow + (int64_t)(t - 1) * p.S + s) : 0.0f;
+                    xs[s] = (valid && s < p.S) ? (xst ? xrow[(t - 1) * p.S + s] : __ldg(xrow + (int64_t)(t - 1) * p.S + s))
+                                               : 0.0f;
+                if (xst && t == p.Q) {   // last x(t) of this tile read: the block may be replaced
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(x_empty);
+                }
 #pragma unroll
                 for (int n = 0; n < C::NCH; ++n) {
                     if (n == C::NCH - 1) {
@@ -298,6 +335,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                     }
                     ptx::mbar_wait(acc_full + ach, aph);
                     ptx::tc_fence_after();
+                    if (C::HOLD && n == C::NCH - 1) {
+                        // the last chunk's MMAs are done with A: chunk NCH-2's h(t), held in
+                        // registers since its epilogue, goes into the last K-slice now
+                        uint32_t hi[4], lo[4];
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) {
+                            hi[w] = t == p.Q ? 0u : hold[w];
+                            lo[w] = t == p.Q ? 0u : hold[4 + w];
+                        }
+                        ptx::tmem_st4(lane_base + C::A_HI + (C::NCH - 2) * 16 + 4 * u, hi);
+                        ptx::tmem_st4(lane_base + C::A_LO + (C::NCH - 2) * 16 + 4 * u, lo);
+                    }
                     if (e == 0 && lane == 0) trace_ev(p, trace_cnt, 4, t, n);
                     float a[2][16];   // 2 groups x 4 neurons x (o, c, lambda, in), scaled domain
                     tmem_ld16(lane_base + ach * 128 + (8 * u) * 4, a[0]);
@@ -340,13 +389,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                     {
                         uint32_t hi[4], lo[4];
                         split_h8(hv, hi, lo);
+                        if (C::HOLD && n == C::NCH - 1) {   // A is free: straight into TMEM (zeros after step Q)
 #pragma unroll
-                        for (int w = 0; w < 4; ++w) {
-                            my_stg[(n * 8 + w) * 32] = hi[w];
-                            my_stg[(n * 8 + 4 + w) * 32] = lo[w];
+                            for (int w = 0; w < 4; ++w)
+                                if (t == p.Q) hi[w] = lo[w] = 0u;
+                            ptx::tmem_st4(lane_base + C::A_HI + n * 16 + 4 * u, hi);
+                            ptx::tmem_st4(lane_base + C::A_LO + n * 16 + 4 * u, lo);
+                        } else if (C::HOLD && n == C::NCH - 2) {
+#pragma unroll
+                            for (int w = 0; w < 4; ++w) {
+                                hold[w] = hi[w];
+                                hold[4 + w] = lo[w];
+                            }
+                        } else {
+#pragma unroll
+                            for (int w = 0; w < 4; ++w) {
+                                my_stg[(n * 8 + w) * 32] = hi[w];
+                                my_stg[(n * 8 + 4 + w) * 32] = lo[w];
+                            }
                         }
                     }
-                    if (t == p.Q && valid) {
+                    if (t == p.Q && valid && p.rbeta) {
+                        const double* bj = p.rbeta + n * 32 + 8 * u;
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) yacc = fma((double)hv[i], __ldg(bj + i), yacc);
+                    } else if (t == p.Q && valid) {
                         float* d1 = p.H + row * p.ldh + n * 32 + 8 * u;
                         if (((p.ldh | (int64_t)(reinterpret_cast<uintptr_t>(p.H) >> 2)) & 3) == 0) {
                             float4* dst = reinterpret_cast<float4*>(d1);
@@ -360,9 +427,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                     if (e == 0 && lane == 0) trace_ev(p, trace_cnt, 5, t, n);
                     if (++ach == 2) { ach = 0; aph ^= 1; }
                 }
-                publish(C::KS - 1, C::KS, t == p.Q);
+                if (C::HOLD) {   // the last K-slice is in TMEM: release it
+                    ptx::tmem_wait_st();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(a_ready + C::KS - 1);
+                } else {
+                    publish(C::KS - 1, C::KS, t == p.Q);
+                }
                 if (e == 0 && lane == 0) trace_ev(p, trace_cnt, 6, t, 0);
             }
+            if (p.rbeta && valid) p.ryp[u * p.N + row] = yacc;
         }
     }
     ptx::tc_fence_before();
@@ -404,11 +479,16 @@ cudaError_t launch_lstm_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, fl
     p.two_pass = h->weight_grid == 1;
     p.debug_no_u = std::getenv("ELMRNN_DEBUG_NO_U") != nullptr;
     p.ntiles = (N + kTcRows - 1) / kTcRows;
+    // a1: stage each full tile's X block when X is 16-byte aligned and it fits
+    p.xbytes = ptx::xstage_host(X, ldx, C::SMEM);   // a1: stage each full tile's X block when it fits
+    p.rbeta = h->ro_beta; p.ryp = h->ro_yp;
+    h->ro_slots = 4;
+    const int smem = C::SMEM + (int)p.xbytes;
     p.k_sig = -1.4426950408889634f * h->tc_inv_scale;
     p.k_tanh = 2.8853900817779268f * h->tc_inv_scale;
     std::copy(h->tc_wb.begin(), h->tc_wb.end(), p.wb);   // W | b captured at init
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_lstm_tc<M, SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(k_lstm_tc<M, SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
     int grid = (int)std::min<int64_t>(p.ntiles, h->sm_count);
     const char* tpath = std::getenv("ELMRNN_TRACE");
     unsigned long long* tbuf = nullptr;
@@ -420,7 +500,7 @@ cudaError_t launch_lstm_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, fl
         cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * p.trace_cap, h->stream);
         p.trace = tbuf;
     }
-    k_lstm_tc<M, SS><<<grid, kTcThreads, C::SMEM, h->stream>>>(p);
+    k_lstm_tc<M, SS><<<grid, kTcThreads, smem, h->stream>>>(p);
     h->launches++;
     if ((e = cudaGetLastError())) return e;
     if (tbuf) {   // debug path: synchronous dump of CTA 0's event trace

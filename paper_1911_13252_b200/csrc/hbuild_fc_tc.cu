@@ -57,6 +57,9 @@ struct FcParams {
     int S, Q, L, NS, act;
     int two_pass;          // 1: A_k on the fp16 grid (weight_grid = 1), A_lo = 0 -> hi.hi + lo.hi only
     int64_t ntiles;
+    uint32_t xbytes;       // a1: bytes of a tile's X block staged by cp.async.bulk (0: x(t) via L1)
+    const double* rbeta;   // fused readout (Eq. 4): no H store; ryp[u * N + row] = H[row][u's neurons] . beta
+    double* ryp;
     float k_act;           // sigmoid: -log2(e) 2^-sigma; tanh: 2 log2(e) 2^-sigma
     float wb[kFWbMax];     // per neuron j: [b, W_0..W_{S-1}] x 2^sigma
 };
@@ -86,7 +89,10 @@ __global__ void __launch_bounds__(kFThreads, 1) k_fc_tc(const __grid_constant__ 
     uint64_t* acc_full = bars + 2 * kFStages;     // [2]
     uint64_t* acc_empty = acc_full + 2;           // [2]
     uint64_t* hist_ready = acc_empty + 2;         // h(t) is in the ring (t < Q)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hist_ready + 1);
+    uint64_t* x_full = hist_ready + 1;            // the tile's X block has landed
+    uint64_t* x_empty = x_full + 1;               // every epilogue warp has read its last x(t)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 1);
+    float* xbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);   // the tile's X block
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -99,6 +105,8 @@ __global__ void __launch_bounds__(kFThreads, 1) k_fc_tc(const __grid_constant__ 
             ptx::mbar_init(acc_empty + i, kFEpiWarps);
         }
         ptx::mbar_init(hist_ready, kFEpiWarps);
+        ptx::mbar_init(x_full, 1);
+        ptx::mbar_init(x_empty, kFEpiWarps);
         ptx::fence_mbar_init();
     }
     if (warp == kFProdWarp) {
@@ -113,8 +121,10 @@ __global__ void __launch_bounds__(kFThreads, 1) k_fc_tc(const __grid_constant__ 
 
     if (warp == kFProdWarp) {
         // ---------------- producer: per step t >= 2, lags min(t-1,L)..1
-        uint32_t st = 0, ph = 0, hph = 0;
+        uint32_t st = 0, ph = 0, hph = 0, xph = 0;
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+            if (ptx::xstage_tile(p.xbytes, tile, p.N))   // the tile's X block (a1)
+                ptx::xstage_issue(xbuf, p.X, p.ldx, tile, p.xbytes, x_full, x_empty, xph);
             for (int t = 2; t <= p.Q; ++t) {
                 const int nl = min(t - 1, p.L);
                 for (int k = nl; k >= 1; --k) {
@@ -184,16 +194,26 @@ __global__ void __launch_bounds__(kFThreads, 1) k_fc_tc(const __grid_constant__ 
         const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
         const float kA = p.k_act;
         const bool is_tanh = p.act == 1;
-        uint32_t ach = 0, aph = 0;
+        uint32_t ach = 0, aph = 0, xph = 0;
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             const int64_t row = tile * kFRows + r;
             const bool valid = row < p.N;
-            const float* xrow = p.X + (valid ? row : 0) * p.ldx;
+            const bool xst = ptx::xstage_tile(p.xbytes, tile, p.N);
+            const float* xrow = xst ? xbuf + (int64_t)r * p.ldx : p.X + (valid ? row : 0) * p.ldx;
+            if (xst) {
+                ptx::mbar_wait(x_full, xph);
+                xph ^= 1;
+            }
             for (int t = 1; t <= p.Q; ++t) {
                 float xs[SS];
 #pragma unroll
                 for (int s = 0; s < SS; ++s)
-                    xs[s] = (valid && s < p.S) ? __ldg(xrow + (int64_t)(t - 1) * p.S + s) : 0.0f;
+                    xs[s] = (valid && s < p.S) ? (xst ? xrow[(t - 1) * p.S + s] : __ldg(xrow + (int64_t)(t - 1) * p.S + s))
+                                               : 0.0f;
+                if (xst && t == p.Q) {   // last x(t) of this tile read: the block may be replaced
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(x_empty);
+                }
                 float a[2][16];
                 if (t >= 2) {
                     ptx::mbar_wait(acc_full + ach, aph);
@@ -247,6 +267,11 @@ __global__ void __launch_bounds__(kFThreads, 1) k_fc_tc(const __grid_constant__ 
                     fence_proxy_async_global();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(hist_ready);
+                } else if (valid && p.rbeta) {   // fused readout: this thread's 32 neurons
+                    double yacc = 0.0;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) yacc = fma((double)hv[i], __ldg(p.rbeta + 32 * u + i), yacc);
+                    p.ryp[u * p.N + row] = yacc;
                 } else if (valid) {
                     float* dst = p.H + row * p.ldh + 32 * u;
                     if (((p.ldh | (int64_t)(reinterpret_cast<uintptr_t>(p.H) >> 2)) & 3) == 0) {
@@ -300,6 +325,10 @@ cudaError_t launch_fc_ss(elmrnn* h, const float* X, int64_t ldx, int64_t N, floa
     p.S = h->S; p.Q = h->Q; p.L = fc_leff(h); p.NS = p.L + 1; p.act = h->act;
     p.two_pass = h->weight_grid == 1;
     p.ntiles = (N + kFRows - 1) / kFRows;
+    p.xbytes = ptx::xstage_host(X, ldx, kFSmem);   // a1: stage each full tile's X block when it fits
+    p.rbeta = h->ro_beta; p.ryp = h->ro_yp;
+    h->ro_slots = 4;
+    const int smem = kFSmem + (int)p.xbytes;
     p.k_act = (h->act == 1 ? 2.8853900817779268f : -1.4426950408889634f) * h->tc_inv_scale;
     std::copy(h->tc_wb.begin(), h->tc_wb.end(), p.wb);
     const int grid = (int)std::min<int64_t>(p.ntiles, h->sm_count);
@@ -313,8 +342,8 @@ cudaError_t launch_fc_ss(elmrnn* h, const float* X, int64_t ldx, int64_t N, floa
         h->scratch_bytes = need;
     }
     p.hist = reinterpret_cast<uint8_t*>(h->scratch);
-    if ((e = cudaFuncSetAttribute(k_fc_tc<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmem))) return e;
-    k_fc_tc<SS><<<grid, kFThreads, kFSmem, h->stream>>>(p);
+    if ((e = cudaFuncSetAttribute(k_fc_tc<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+    k_fc_tc<SS><<<grid, kFThreads, smem, h->stream>>>(p);
     h->launches++;
     return cudaGetLastError();
 }

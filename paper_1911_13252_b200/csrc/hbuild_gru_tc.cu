@@ -41,7 +41,7 @@ constexpr int kGStagesPerStep = kGChunks * kGKS;
 constexpr int kGWbMax = 7168;
 constexpr uint32_t kAcc = 0, kAH = 256, kARH = 384;   // TMEM column bases (hi at +0, lo at +64)
 constexpr int kZBytes = kGEpiWarps * 32 * 32 * 4;     // z of 32 neurons per thread
-constexpr int kGSmem = 1024 + kGStages * kGStageBytes + kZBytes + 256;
+constexpr int kGSmem = 1024 + kGStages * kGStageBytes + kZBytes + 256;   // + the X block
 
 struct GruParams {
     const float* X;
@@ -52,6 +52,9 @@ struct GruParams {
     int S, Q;
     int two_pass;          // 1: U on the fp16 grid (weight_grid = 1), U_lo = 0 -> hi.hi + lo.hi only
     int64_t ntiles;
+    uint32_t xbytes;       // a1: bytes of a tile's X block staged by cp.async.bulk (0: x(t) via L1)
+    const double* rbeta;   // fused readout (Eq. 4): no H store; ryp[u * N + row] = H[row][u's neurons] . beta
+    double* ryp;
     float k_sig, k_tanh;   // -log2(e) 2^-sigma, 2 log2(e) 2^-sigma
     float wb[kGWbMax];     // per neuron j, gate g in (z, r, f): [b, W_0..W_{S-1}] x 2^sigma
 };
@@ -98,7 +101,10 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
     uint64_t* acc_empty = acc_full + 2;
     uint64_t* a_ready = acc_empty + 2;   // [KS]: K-slice ks of h(t-1) is in TMEM
     uint64_t* rh_ready = a_ready + kGKS; // [KS]: K-slice ks of r o h(t-1) is in TMEM
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rh_ready + kGKS);
+    uint64_t* x_full = rh_ready + kGKS;  // the tile's X block has landed
+    uint64_t* x_empty = x_full + 1;      // every epilogue warp has read its last x(t)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 1);
+    float* xbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);   // the tile's X block
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -112,6 +118,8 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
         }
         for (int i = 0; i < kGKS; ++i) ptx::mbar_init(a_ready + i, kGEpiWarps);
         for (int i = 0; i < kGKS; ++i) ptx::mbar_init(rh_ready + i, kGEpiWarps);
+        ptx::mbar_init(x_full, 1);
+        ptx::mbar_init(x_empty, kGEpiWarps);
         ptx::fence_mbar_init();
     }
     if (warp == kGProdWarp) {
@@ -125,9 +133,14 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
     const int64_t steps_total = ((p.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x) * p.Q;
 
     if (warp == kGProdWarp) {
-        uint32_t st = 0, ph = 0;
+        uint32_t st = 0, ph = 0, xph = 0;
         const uint32_t bytes = p.two_pass ? kGSliceBytes : kGStageBytes;   // hi only when U_lo = 0
         for (int64_t s = 0; s < steps_total; ++s) {
+            if (s % p.Q == 0) {   // a new tile: its X block (a1)
+                const int64_t tile = blockIdx.x + (s / p.Q) * gridDim.x;
+                if (ptx::xstage_tile(p.xbytes, tile, p.N))
+                    ptx::xstage_issue(xbuf, p.X, p.ldx, tile, p.xbytes, x_full, x_empty, xph);
+            }
             for (int c = 0; c < kGStagesPerStep; ++c) {
                 ptx::mbar_wait(empty + st, ph ^ 1);
                 if (ptx::elect_one()) {
@@ -190,7 +203,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
         const float kS = p.k_sig, kT = p.k_tanh;
         float* my_z = zs + (size_t)warp * 32 * 32 + lane;      // [item][lane]
         float h[32];                                            // h of neurons 16u+i, 64+16u+i
-        uint32_t ach = 0, aph = 0;
+        uint32_t ach = 0, aph = 0, xph = 0;
         // write h (or zero) of this thread's neurons into A_h hi/lo and publish both K-slices
         // K-slice `half` of this thread's h (or zeros) into A_h, then release it
         auto publish_h = [&](int half, bool zero) {
@@ -214,14 +227,25 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             const int64_t row = tile * kGRows + r;
             const bool valid = row < p.N;
-            const float* xrow = p.X + (valid ? row : 0) * p.ldx;
+            const bool xst = ptx::xstage_tile(p.xbytes, tile, p.N);
+            const float* xrow = xst ? xbuf + (int64_t)r * p.ldx : p.X + (valid ? row : 0) * p.ldx;
+            if (xst) {
+                ptx::mbar_wait(x_full, xph);
+                xph ^= 1;
+            }
 #pragma unroll
             for (int i = 0; i < 32; ++i) h[i] = 0.0f;
+            double yacc = 0.0;   // fused readout partial
             for (int t = 1; t <= p.Q; ++t) {
                 float xs[SS];
 #pragma unroll
                 for (int s = 0; s < SS; ++s)
-                    xs[s] = (valid && s < p.S) ? __ldg(xrow + (int64_t)(t - 1) * p.S + s) : 0.0f;
+                    xs[s] = (valid && s < p.S) ? (xst ? xrow[(t - 1) * p.S + s] : __ldg(xrow + (int64_t)(t - 1) * p.S + s))
+                                               : 0.0f;
+                if (xst && t == p.Q) {   // last x(t) of this tile read: the block may be replaced
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(x_empty);
+                }
                 // ---- phase 1: z, r for neurons 64c + 16u + i; r o h -> A_rh
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
@@ -293,7 +317,11 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                         h0 = fmaf(z0, n0 - h0, h0);   // (1 - z) h + z n
                         h1 = fmaf(z1, n1 - h1, h1);
                     }
-                    if (t == p.Q && valid) {
+                    if (t == p.Q && valid && p.rbeta) {
+                        const double* bj = p.rbeta + 64 * c + 16 * u;
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) yacc = fma((double)h[c * 16 + i], __ldg(bj + i), yacc);
+                    } else if (t == p.Q && valid) {
                         float* d1 = p.H + row * p.ldh + 64 * c + 16 * u;
                         if (((p.ldh | (int64_t)(reinterpret_cast<uintptr_t>(p.H) >> 2)) & 3) == 0) {
                             float4* dst = reinterpret_cast<float4*>(d1);
@@ -309,6 +337,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                     publish_h(c, t == p.Q);   // next step's A slice c (or h(0) = 0 of the next tile)
                 }
             }
+            if (p.rbeta && valid) p.ryp[u * p.N + row] = yacc;
         }
     }
     ptx::tc_fence_before();
@@ -351,13 +380,17 @@ cudaError_t launch_gru(elmrnn* h, const float* X, int64_t ldx, int64_t N, float*
     p.S = h->S; p.Q = h->Q;
     p.two_pass = h->weight_grid == 1;
     p.ntiles = (N + kGRows - 1) / kGRows;
+    p.xbytes = ptx::xstage_host(X, ldx, kGSmem);   // a1: stage each full tile's X block when it fits
+    p.rbeta = h->ro_beta; p.ryp = h->ro_yp;
+    h->ro_slots = 4;
+    const int smem = kGSmem + (int)p.xbytes;
     p.k_sig = -1.4426950408889634f * h->tc_inv_scale;
     p.k_tanh = 2.8853900817779268f * h->tc_inv_scale;
     std::copy(h->tc_wb.begin(), h->tc_wb.end(), p.wb);
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_gru_tc<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGSmem))) return e;
+    if ((e = cudaFuncSetAttribute(k_gru_tc<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
     const int grid = (int)std::min<int64_t>(p.ntiles, h->sm_count);
-    k_gru_tc<SS><<<grid, kGThreads, kGSmem, h->stream>>>(p);
+    k_gru_tc<SS><<<grid, kGThreads, smem, h->stream>>>(p);
     h->launches++;
     return cudaGetLastError();
 }

@@ -52,6 +52,9 @@ struct GruWideParams {
     int M, S, Q, NC1, NC2, KS;
     int two_pass;
     int64_t ntiles;
+    uint32_t xbytes;       // a1: bytes of a tile's X block staged by cp.async.bulk (0: x(t) via L1)
+    const double* rbeta;   // fused readout (Eq. 4): no H store; ryp[u * N + row] = H[row][u's neurons] . beta
+    double* ryp;
     float k_sig, k_tanh;
 };
 
@@ -107,7 +110,10 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
     uint64_t* acc_empty = acc_full + 2;         // [2]
     uint64_t* hist_ready = acc_empty + 2;       // h(t) image complete (t < Q)
     uint64_t* rh_ready = hist_ready + 1;        // r o h(t-1) image complete (t >= 2)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rh_ready + 1);
+    uint64_t* x_full = rh_ready + 1;            // the tile's X block has landed
+    uint64_t* x_empty = x_full + 1;             // every epilogue warp has read its last x(t)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 1);
+    float* xbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);   // the tile's X block
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -121,6 +127,8 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
         }
         ptx::mbar_init(hist_ready, kQEpiWarps);
         ptx::mbar_init(rh_ready, kQEpiWarps);
+        ptx::mbar_init(x_full, 1);
+        ptx::mbar_init(x_empty, kQEpiWarps);
         ptx::fence_mbar_init();
     }
     if (warp == kQProdWarp) {
@@ -137,7 +145,7 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
     uint8_t* rh_img = img + 2 * img_bytes;
 
     if (warp == kQProdWarp) {
-        uint32_t st = 0, ph = 0, hph = 0, rph = 0;
+        uint32_t st = 0, ph = 0, hph = 0, rph = 0, xph = 0;
         const uint32_t bbytes = p.two_pass ? kQTile : kQPair;
         auto load = [&](const uint8_t* a_img, int chunk) {
             for (int ks = 0; ks < KS; ++ks) {
@@ -153,6 +161,8 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
             }
         };
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+            if (ptx::xstage_tile(p.xbytes, tile, p.N))   // the tile's X block (a1)
+                ptx::xstage_issue(xbuf, p.X, p.ldx, tile, p.xbytes, x_full, x_empty, xph);
             for (int t = 2; t <= p.Q; ++t) {
                 ptx::mbar_wait(hist_ready, hph);
                 hph ^= 1;
@@ -208,16 +218,27 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
         float* hst = p.hst + (size_t)blockIdx.x * M * 128;
         float* zst = p.zst + (size_t)blockIdx.x * M * 128;
         auto sidx = [&](int j) { return ((size_t)(j >> 3) * 128 + r) * 8; };   // 8 consecutive neurons j..j+7
-        uint32_t ach = 0, aph = 0;
+        uint32_t ach = 0, aph = 0, xph = 0;
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             const int64_t row = tile * kQRows + r;
             const bool valid = row < p.N;
-            const float* xrow = p.X + (valid ? row : 0) * p.ldx;
+            const bool xst = ptx::xstage_tile(p.xbytes, tile, p.N);
+            const float* xrow = xst ? xbuf + (int64_t)r * p.ldx : p.X + (valid ? row : 0) * p.ldx;
+            if (xst) {
+                ptx::mbar_wait(x_full, xph);
+                xph ^= 1;
+            }
+            double yacc = 0.0;   // fused readout partial
             for (int t = 1; t <= p.Q; ++t) {
                 float xs[SS];
 #pragma unroll
                 for (int s = 0; s < SS; ++s)
-                    xs[s] = (valid && s < p.S) ? __ldg(xrow + (int64_t)(t - 1) * p.S + s) : 0.0f;
+                    xs[s] = (valid && s < p.S) ? (xst ? xrow[(t - 1) * p.S + s] : __ldg(xrow + (int64_t)(t - 1) * p.S + s))
+                                               : 0.0f;
+                if (xst && t == p.Q) {   // last x(t) of this tile read: the block may be replaced
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(x_empty);
+                }
                 // ---- phase 1: z, r of neurons 64 c + 16 u + 0..15; r o h(t-1) -> image
                 for (int c = 0; c < NC1; ++c) {
                     float a[2][16];   // 16 neurons x (z, r) interleaved
@@ -313,6 +334,9 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
                         if (t < p.Q) {
                             st8(hst + sidx(j0), hp);
                             put_hilo8(img + (size_t)(t & 1) * img_bytes, r, j0, hp);
+                        } else if (valid && p.rbeta) {
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) yacc = fma((double)hp[i], __ldg(p.rbeta + j0 + i), yacc);
                         } else if (valid) {
                             float* d1 = p.H + row * p.ldh + j0;
                             if (((p.ldh | (int64_t)(reinterpret_cast<uintptr_t>(p.H) >> 2)) & 3) == 0) st8(d1, hp);
@@ -329,6 +353,7 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
                     if (lane == 0) ptx::mbar_arrive(hist_ready);
                 }
             }
+            if (p.rbeta && valid) p.ryp[u * p.N + row] = yacc;
         }
     }
     ptx::tc_fence_before();
@@ -370,6 +395,10 @@ cudaError_t launch_gw(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* 
     p.M = h->M; p.S = h->S; p.Q = h->Q; p.NC1 = h->M / 64; p.NC2 = h->M / 128; p.KS = h->M / 64;
     p.two_pass = h->weight_grid == 1;
     p.ntiles = (N + kQRows - 1) / kQRows;
+    p.xbytes = ptx::xstage_host(X, ldx, kQSmem);   // a1: stage each full tile's X block when it fits
+    p.rbeta = h->ro_beta; p.ryp = h->ro_yp;
+    h->ro_slots = 4;
+    const int smem = kQSmem + (int)p.xbytes;
     p.k_sig = -1.4426950408889634f * h->tc_inv_scale;
     p.k_tanh = 2.8853900817779268f * h->tc_inv_scale;
     p.Uimg = static_cast<const uint8_t*>(h->tc_ops);
@@ -389,8 +418,8 @@ cudaError_t launch_gw(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* 
     p.img = base;
     p.hst = reinterpret_cast<float*>(base + img);
     p.zst = reinterpret_cast<float*>(base + img + st);
-    if ((e = cudaFuncSetAttribute(k_gru_wide<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQSmem))) return e;
-    k_gru_wide<SS><<<grid, kQThreads, kQSmem, h->stream>>>(p);
+    if ((e = cudaFuncSetAttribute(k_gru_wide<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+    k_gru_wide<SS><<<grid, kQThreads, smem, h->stream>>>(p);
     h->launches++;
     return cudaGetLastError();
 }

@@ -59,6 +59,9 @@ struct WideParams {
     int M, S, Q, NCH, KS;
     int two_pass;
     int64_t ntiles;
+    uint32_t xbytes;       // a1: bytes of a tile's X block staged by cp.async.bulk (0: x(t) via L1)
+    const double* rbeta;   // fused readout (Eq. 4): no H store; ryp[u * N + row] = H[row][u's neurons] . beta
+    double* ryp;
     float k_sig, k_tanh;   // -log2(e) 2^-sigma, 2 log2(e) 2^-sigma
 };
 
@@ -87,7 +90,10 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
     uint64_t* acc_full = bars + 2 * kWStages;     // [2]
     uint64_t* acc_empty = acc_full + 2;           // [2]
     uint64_t* hist_ready = acc_empty + 2;         // all of h(t) is in the image (t < Q)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hist_ready + 1);
+    uint64_t* x_full = hist_ready + 1;            // the tile's X block has landed
+    uint64_t* x_empty = x_full + 1;               // every epilogue warp has read its last x(t)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 1);
+    float* xbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);   // the tile's X block
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -100,6 +106,8 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
             ptx::mbar_init(acc_empty + i, kWEpiWarps);
         }
         ptx::mbar_init(hist_ready, kWEpiWarps);
+        ptx::mbar_init(x_full, 1);
+        ptx::mbar_init(x_empty, kWEpiWarps);
         ptx::fence_mbar_init();
     }
     if (warp == kWProdWarp) {
@@ -117,9 +125,11 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
     if (warp == kWProdWarp) {
         // ---------------- producer: per step t >= 2, (chunk n, K-slice ks) pairs of
         // [h(t-1) slice ks | U_cat chunk n slice ks]; whole warp loops, one lane issues
-        uint32_t st = 0, ph = 0, hph = 0;
+        uint32_t st = 0, ph = 0, hph = 0, xph = 0;
         const uint32_t bbytes = p.two_pass ? kWTile : kWPair;   // U hi only when U_lo = 0
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+            if (ptx::xstage_tile(p.xbytes, tile, p.N))   // the tile's X block (a1)
+                ptx::xstage_issue(xbuf, p.X, p.ldx, tile, p.xbytes, x_full, x_empty, xph);
             for (int t = 2; t <= p.Q; ++t) {
                 const uint8_t* slot = hist + (size_t)((t - 1) & 1) * slot_bytes;
                 ptx::mbar_wait(hist_ready, hph);   // h(t-1) fully written by the epilogue
@@ -183,16 +193,27 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
         const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
         const float kS = p.k_sig, kT = p.k_tanh;
         float* cbase = p.cst + (size_t)blockIdx.x * NCH * 4 * 128 * 8;
-        uint32_t ach = 0, aph = 0;
+        uint32_t ach = 0, aph = 0, xph = 0;
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             const int64_t row = tile * kWRows + r;
             const bool valid = row < p.N;
-            const float* xrow = p.X + (valid ? row : 0) * p.ldx;
+            const bool xst = ptx::xstage_tile(p.xbytes, tile, p.N);
+            const float* xrow = xst ? xbuf + (int64_t)r * p.ldx : p.X + (valid ? row : 0) * p.ldx;
+            if (xst) {
+                ptx::mbar_wait(x_full, xph);
+                xph ^= 1;
+            }
+            double yacc = 0.0;   // fused readout partial
             for (int t = 1; t <= p.Q; ++t) {
                 float xs[SS];
 #pragma unroll
                 for (int s = 0; s < SS; ++s)
-                    xs[s] = (valid && s < p.S) ? __ldg(xrow + (int64_t)(t - 1) * p.S + s) : 0.0f;
+                    xs[s] = (valid && s < p.S) ? (xst ? xrow[(t - 1) * p.S + s] : __ldg(xrow + (int64_t)(t - 1) * p.S + s))
+                                               : 0.0f;
+                if (xst && t == p.Q) {   // last x(t) of this tile read: the block may be replaced
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(x_empty);
+                }
                 uint8_t* slot = hist + (size_t)(t & 1) * slot_bytes;
                 for (int n = 0; n < NCH; ++n) {
                     float a[2][16];   // 2 groups x 4 neurons x (o, c, lambda, in), scaled domain
@@ -264,6 +285,9 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
                         const uint32_t off = ptx::sw128_offset((uint32_t)r, (uint32_t)(K & 63));
                         *reinterpret_cast<uint4*>(sl + off) = hi;
                         *reinterpret_cast<uint4*>(sl + kWTile + off) = lo;
+                    } else if (valid && p.rbeta) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) yacc = fma((double)hv[i], __ldg(p.rbeta + n * 32 + 8 * u + i), yacc);
                     } else if (valid) {
                         float* d1 = p.H + row * p.ldh + n * 32 + 8 * u;
                         if (((p.ldh | (int64_t)(reinterpret_cast<uintptr_t>(p.H) >> 2)) & 3) == 0) {
@@ -282,6 +306,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
                     if (lane == 0) ptx::mbar_arrive(hist_ready);
                 }
             }
+            if (p.rbeta && valid) p.ryp[u * p.N + row] = yacc;
         }
     }
     ptx::tc_fence_before();
@@ -299,6 +324,10 @@ cudaError_t launch_wide_ss(elmrnn* h, const float* X, int64_t ldx, int64_t N, fl
     p.M = h->M; p.S = h->S; p.Q = h->Q; p.NCH = h->M / 32; p.KS = h->M / 64;
     p.two_pass = h->weight_grid == 1;
     p.ntiles = (N + kWRows - 1) / kWRows;
+    p.xbytes = ptx::xstage_host(X, ldx, kWSmem);   // a1: stage each full tile's X block when it fits
+    p.rbeta = h->ro_beta; p.ryp = h->ro_yp;
+    h->ro_slots = 4;
+    const int smem = kWSmem + (int)p.xbytes;
     p.k_sig = -1.4426950408889634f * h->tc_inv_scale;
     p.k_tanh = 2.8853900817779268f * h->tc_inv_scale;
     const size_t img_bytes = (size_t)p.NCH * p.KS * kWPair;
@@ -317,8 +346,8 @@ cudaError_t launch_wide_ss(elmrnn* h, const float* X, int64_t ldx, int64_t N, fl
     }
     p.hist = reinterpret_cast<uint8_t*>(h->scratch);
     p.cst = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(h->scratch) + hist_bytes);
-    if ((e = cudaFuncSetAttribute(k_lstm_wide<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem))) return e;
-    k_lstm_wide<SS><<<grid, kWThreads, kWSmem, h->stream>>>(p);
+    if ((e = cudaFuncSetAttribute(k_lstm_wide<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+    k_lstm_wide<SS><<<grid, kWThreads, smem, h->stream>>>(p);
     h->launches++;
     return cudaGetLastError();
 }

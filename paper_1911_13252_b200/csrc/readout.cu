@@ -46,43 +46,14 @@ cudaError_t launch_error_windows(elmrnn* h, const float* H, int64_t ldh, const f
 
 // ---- free-running forecast (reading R31) ------------------------------------------------
 // Window buffer w [N][ldw] (fp32, d = 1).  One step: yhat_i = H_i . beta (Eq. 4,
-// fp64 accumulation), Yhat[i][k] = fp32(yhat_i), then w_i <- (w_i[1:], fp32(yhat_i)).
-// One warp per row: the lanes read the window into registers before any write.
+// the fused readout of the builders), Yhat[i][k] = fp32(yhat_i), then
+// w_i <- (w_i[1:], fp32(yhat_i)) in k_readout_finish.
 __global__ void k_window_init(const float* __restrict__ X, int64_t ldx, int64_t N, int Q, float* __restrict__ w,
                               int64_t ldw) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N * Q; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / Q;
         const int t = (int)(e - i * Q);
         w[i * ldw + t] = X[i * ldx + t];
-    }
-}
-
-__global__ void k_predict_shift(const float* __restrict__ H, int64_t ldh, int64_t N, int M,
-                                const double* __restrict__ beta, float* __restrict__ w, int64_t ldw, int Q,
-                                float* __restrict__ yout, int64_t ldyo) {
-    const int lane = threadIdx.x & 31;
-    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (row >= N) return;
-    double s = 0.0;
-    for (int j = lane; j < M; j += 32) s = fma((double)H[row * ldh + j], beta[j], s);
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const float y = (float)s;
-    float* wr = w + row * ldw;
-    float v[4];   // Q <= 128 (checked by the caller)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int t = lane + 32 * q;
-        v[q] = (t >= 1 && t < Q) ? wr[t] : 0.0f;
-    }
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int t = lane + 32 * q;
-        if (t >= 1 && t < Q) wr[t - 1] = v[q];
-    }
-    if (lane == 0) {
-        wr[Q - 1] = y;
-        yout[row * ldyo] = y;
     }
 }
 
@@ -93,11 +64,44 @@ cudaError_t launch_window_init(elmrnn* h, const float* X, int64_t ldx, int64_t N
     return cudaGetLastError();
 }
 
-cudaError_t launch_predict_shift(elmrnn* h, const float* H, int64_t ldh, int64_t N, const double* beta, float* w,
-                                 int64_t ldw, float* yout, int64_t ldyo) {
+// ---- fused readout finish (Eq. 4) ---------------------------------
+// The builders ran with a readout sink (elmrnn::ro_beta): row i's partial dot
+// products H_i[segment] . beta sit in its slots; sum them in slot order (fixed:
+// deterministic), round once to fp32.  Forecast (w != null, reading R31): the
+// row's warp then shifts its window and appends yhat.
+__global__ void k_readout_finish(const double* __restrict__ yp, int64_t N, int M, int slots, float* __restrict__ yout,
+                                 int64_t ldyo, float* __restrict__ w, int64_t ldw, int Q) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (row >= N) return;
+    const int ns = slots > 0 ? slots : (int)(((row + 1) * M - 1) / 32 - (row * M) / 32 + 1);
+    double s = 0.0;
+    for (int k = 0; k < ns; ++k) s += yp[k * N + row];
+    const float y = (float)s;
+    if (w) {
+        float* wr = w + row * ldw;
+        float v[4];   // Q <= 128 (checked by the caller)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = lane + 32 * q;
+            v[q] = (t >= 1 && t < Q) ? wr[t] : 0.0f;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = lane + 32 * q;
+            if (t >= 1 && t < Q) wr[t - 1] = v[q];
+        }
+        if (lane == 0) wr[Q - 1] = y;
+    }
+    if (lane == 0) yout[row * ldyo] = y;
+}
+
+cudaError_t launch_readout_finish(elmrnn* h, const double* yp, int64_t N, int slots, float* yout, int64_t ldyo,
+                                  float* w, int64_t ldw) {
     const int64_t blocks = (N * 32 + 255) / 256;
     if (blocks > INT32_MAX) return cudaErrorInvalidConfiguration;
-    k_predict_shift<<<(unsigned)blocks, 256, 0, h->stream>>>(H, ldh, N, h->M, beta, w, ldw, h->Q, yout, ldyo);
+    k_readout_finish<<<(unsigned)blocks, 256, 0, h->stream>>>(yp, N, h->M, slots, yout, ldyo, w, ldw, h->Q);
     h->launches++;
     return cudaGetLastError();
 }

@@ -75,6 +75,38 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
         : "memory");
 }
 
+// ---- window staging ----------------------------------------------
+// A 128-row sample tile's windows X[row0 .. row0+127][0 .. ldx) are ONE contiguous
+// block of X (rows are consecutive), so a single cp.async.bulk moves the whole
+// tile's Q-step input into shared memory; the epilogue then reads x(t) from there.
+// Staged only for full tiles of a 16-byte aligned X whose block fits the kernel's
+// spare shared memory (host: xstage_bytes); otherwise x(t) is read through L1.
+__host__ __device__ __forceinline__ uint32_t xstage_bytes(int64_t ldx) { return (uint32_t)(128 * ldx * 4); }
+// host: bytes to stage per tile for a kernel whose other dynamic shared memory is
+// smem_base bytes (227 KB opt-in limit), or 0 (X not 16-byte aligned / does not fit)
+inline uint32_t xstage_host(const float* X, int64_t ldx, int smem_base) {
+#ifdef ELM_NO_XSTAGE   // A/B timing variant only
+    return 0;
+#endif
+    const int64_t xb = 128 * ldx * 4;
+    return ((reinterpret_cast<uintptr_t>(X) & 15) == 0 && smem_base + xb <= 232448) ? (uint32_t)xb : 0;
+}
+__device__ __forceinline__ bool xstage_tile(uint32_t xbytes, int64_t tile, int64_t N) {
+    return xbytes != 0 && (tile + 1) * 128 <= N;
+}
+// producer warp (warp-uniform): wait until the previous tile's epilogue warps have
+// read their last x(t) (x_empty), then one elected lane brings this tile's block in
+__device__ __forceinline__ void xstage_issue(float* xbuf, const float* X, int64_t ldx, int64_t tile, uint32_t xbytes,
+                                             uint64_t* x_full, uint64_t* x_empty, uint32_t& xph) {
+    mbar_wait(x_empty, xph ^ 1);
+    if (elect_one()) {
+        mbar_arrive_expect_tx(x_full, xbytes);
+        bulk_g2s(xbuf, X + tile * 128 * ldx, xbytes, x_full);
+    }
+    __syncwarp();
+    xph ^= 1;
+}
+
 // generic-proxy smem writes -> visible to the async proxy (tensor core reads)
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

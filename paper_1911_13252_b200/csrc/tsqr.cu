@@ -916,12 +916,14 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
             if (lane0) qr_ev(5, p);
         } else {
             wy_trailing<ROWS>(C, LDC, n, p, pe, pe + nbn, tw, nw - 1, R, G0, g0, u0);   // panel p+1's columns first
+            if (tw == 0 && (gtid & 31) == 0) qr_ev(3, p);
             __threadfence_block();
             // warps without a look-ahead tile wait with the panel warp so the
             // look-ahead chain is not slowed by their trailing work
             if (la_wait && 8 * tw >= nbn) named_bar_sync(grp.bar_la, grp.threads);
             else named_bar_arrive(grp.bar_la, grp.threads);
             wy_trailing<ROWS>(C, LDC, n, p, pe + nbn, n, tw, nw - 1, R, G0, g0, u0);
+            if (tw == 0 && (gtid & 31) == 0) qr_ev(4, p);
         }
         step_sync();
         if (lane0) qr_ev(2, p);
@@ -1460,9 +1462,39 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
             cudaFuncSetAttribute(k_tsqr_leaf_wy<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             int* slot = reinterpret_cast<int*>(h->sdev + 1);   // per-SM arrival counters (ensure_solve_ws)
             cudaMemsetAsync(slot, 0, 1024 * sizeof(int), h->stream);
+#ifdef ELM_QR_TRACE   // tracing build: per panel step clocks of CTA 0's last tile -> $ELMRNN_TRACE_QR
+            const char* tpath = std::getenv("ELMRNN_TRACE_QR");
+            unsigned long long* tb = nullptr;
+            if (tpath) {
+                cudaMalloc(&tb, 4096 * 8 * sizeof(unsigned long long));
+                cudaMemset(tb, 0, 4096 * 8 * sizeof(unsigned long long));
+                cudaMemcpyToSymbol(g_qr_trace, &tb, sizeof(tb));
+            }
+#endif
             k_tsqr_leaf_wy<RW, NW><<<(unsigned)slabs, 32 * NW, sm, h->stream>>>(
                 H, ldh, Y, ldy, h->nrhs, N, h->M, h->Rws, rows, h->flag, slot, wy_la_wait(n), h->tune.pw_mode);
             h->launches++;
+#ifdef ELM_QR_TRACE
+            if (tb) {
+                std::vector<unsigned long long> hb(4096 * 8);
+                cudaStreamSynchronize(h->stream);
+                cudaMemcpy(hb.data(), tb, hb.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+                unsigned long long* z = nullptr;
+                cudaMemcpyToSymbol(g_qr_trace, &z, sizeof(z));
+                cudaFree(tb);
+                if (FILE* f = std::fopen(tpath, "w")) {
+                    for (int k = 0; k < 4096; ++k) {
+                        bool any = false;
+                        for (int c = 0; c < 8; ++c) any |= hb[k * 8 + c] != 0;
+                        if (!any) continue;
+                        std::fprintf(f, "%d", k);
+                        for (int c = 0; c < 8; ++c) std::fprintf(f, ",%llu", hb[k * 8 + c]);
+                        std::fprintf(f, "\n");
+                    }
+                    std::fclose(f);
+                }
+            }
+#endif
             return cudaGetLastError();
         });
         if (e) return e;
@@ -1577,26 +1609,6 @@ cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta) {
         h->launches++;
         return cudaGetLastError();
     });
-}
-
-// ---- predict: Eq. 4, yhat_i = sum_j beta_j H[i][j] ------------------------
-__global__ void k_predict_gemv(const float* __restrict__ H, int64_t ldh, int64_t N, int M,
-                               const double* __restrict__ beta, float* __restrict__ yhat) {
-    const int lane = threadIdx.x & 31;
-    int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (row >= N) return;
-    double s = 0.0;
-    for (int j = lane; j < M; j += 32) s = fma((double)H[row * ldh + j], beta[j], s);
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) yhat[row] = (float)s;
-}
-
-cudaError_t launch_predict_gemv(elmrnn* h, const float* H, int64_t ldh, int64_t N, const double* beta, float* yhat) {
-    int64_t threads = N * 32;
-    int64_t blocks = (threads + 255) / 256;
-    k_predict_gemv<<<(unsigned)blocks, 256, 0, h->stream>>>(H, ldh, N, h->M, beta, yhat);
-    h->launches++;
-    return cudaGetLastError();
 }
 
 }  // namespace elm

@@ -725,10 +725,38 @@ def test_forecast_per_step_parity(arch, M, Q):
     assert np.abs(Yh - full).max() <= 10 * tol
 
 
-def test_predict_forecast_chunked_readout():
-    """Readout in L2-resident row chunks (elmrnn_predict / elmrnn_forecast build
-    H(Q) chunk by chunk, 131072 rows at M = 64): rows on both sides of the chunk
-    boundary against the oracle's Eq. 4 and free-running forecast."""
+READOUT_CASES = [  # (arch, M, Q, S, force_path): one per builder kernel and its readout-slot layout
+    ("lstm", 256, 12, 1, 0), ("lstm", 128, 12, 2, 0), ("lstm", 512, 4, 1, 0), ("gru", 128, 12, 4, 0),
+    ("gru", 256, 6, 1, 0), ("fc", 128, 10, 4, 0), ("lstm", 48, 10, 1, 0), ("gru", 40, 10, 2, 0), ("fc", 50, 10, 1, 0),
+    ("elman", 20, 10, 1, 0), ("elman", 64, 40, 1, 0), ("jordan", 64, 20, 1, 0), ("narmax", 33, 20, 1, 0),
+    ("lstm_diag", 33, 10, 2, 0), ("gru_diag", 96, 10, 1, 0), ("fc_eq8", 20, 12, 1, 0)]
+
+
+@pytest.mark.parametrize("arch,M,Q,S,fp", READOUT_CASES)
+def test_fused_readout_every_builder(arch, M, Q, S, fp):
+    """elmrnn_predict through the fused readout epilogue (no H(Q) is written:
+    each builder emits fp64 partial products H_i . beta per row segment, summed
+    in a fixed slot order) against the oracle's Eq. 4 on every row of a ragged N
+    (partial last tile / warp group), and bitwise repeatable."""
+    N = 1000 + 37
+    X, Y, _ = inputs(N, Q, S, seed=M + Q + S, kind="ar5")
+    beta = np.random.default_rng(M + Q).standard_normal(M) / np.sqrt(M)
+    e = E(arch, S, M, Q, 4, force_path=fp)
+    Xd, bd = torch.from_numpy(X).cuda(), torch.from_numpy(beta).cuda()
+    y1 = e.predict(Xd, bd)
+    y2 = e.predict(Xd, bd)
+    assert torch.equal(y1, y2)
+    net = orc.Net(arch, S=S, M=M, Q=Q)
+    ref = orc.predict(orc.build_H(net, orc.gen_weights(net, 4), X, threads=8), beta)
+    tol = 1e-5 * max(1.0, np.abs(beta).sum())
+    err = np.abs(y1.cpu().numpy() - ref).max()
+    assert err <= tol, (arch, M, e.path, err, tol)
+
+
+def test_fused_readout_large_n():
+    """Fused readout / forecast at 140000 rows (M = 64, Elman: a row spans up to
+    three 32-cell warp groups, slot layout kRoCellSlots): first, middle and last
+    rows against the oracle's Eq. 4 and free-running forecast."""
     N, M, Q, K = 140000, 64, 10, 2
     X, Y, _ = inputs(N, Q, 1, seed=5, kind="ar5")
     beta = np.random.default_rng(2).standard_normal(M) / M
