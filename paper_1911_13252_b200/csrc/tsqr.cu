@@ -703,94 +703,137 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 //   solve   W' = T'^T W (16-step forward substitution across the 8 lanes of a column)
 //   R[p+i][j] += u0_i W'_i
 //   GEMM 2  C (ROWS x 8) += V W'                        (K = 16)
-// The V fragments of both GEMMs are loaded once per panel and stay in registers.
-template <int ROWS>
-__device__ __forceinline__ void wy_trailing(double* __restrict__ C, int LDC, int n, int p, int pe, int jend,
-                                            int warp, int nw, double* __restrict__ R, const double* Gs,
-                                            const double* cgv, const double* cuv) {
+// A warp with two or more tiles left runs two of them in lockstep (NT = 2): each
+// tile is a latency-bound chain (8 dependent MMA k-steps, the 16-step
+// substitution, 4 more), so two interleaved chains nearly double the warp's
+// throughput (measured: the first panel steps of a fold are trailing bound).
+template <int ROWS, int NT>
+__device__ __forceinline__ void wy_trailing_tiles(double* __restrict__ C, int LDC, int n, int p, const int (&j0)[NT],
+                                                  const bool (&ok)[NT], double* __restrict__ R, const double* Gs,
+                                                  const double* cgv, const double (&u0r)[2]) {
     constexpr int KS1 = ROWS / 4, MT2 = ROWS / 8;
     const int lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
-    const double u0r[2] = {cuv[gid], cuv[8 + gid]};
     const double* Vt = C + p;   // V[r][i] = Vt[r * LDC + i]
-    // R rows p.. of the warp's first tile, then prefetched one tile ahead
-    auto ldR = [&](int j0, double (&rr)[2][2]) {
+    double rcur[NT][2][2], d[NT][2][2];
+#pragma unroll
+    for (int q = 0; q < NT; ++q)
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int j = j0 + 2 * tig + e;
-                rr[mt][e] = (j0 < jend && j < n) ? __ldcg(R + (size_t)(p + 8 * mt + gid) * n + j) : 0.0;
+                const int j = j0[q] + 2 * tig + e;
+                rcur[q][mt][e] = (ok[q] && j < n) ? __ldcg(R + (size_t)(p + 8 * mt + gid) * n + j) : 0.0;
+                d[q][mt][e] = 0.0;   // the R term joins after GEMM 1: its L2 latency overlaps the MMAs
             }
-    };
-    double rn[2][2];
-    ldR(pe + 8 * warp, rn);
-    for (int j0 = pe + 8 * warp; j0 < jend; j0 += 8 * nw) {
-        double d[2][2];
+#pragma unroll 4
+    for (int ks = 0; ks < KS1; ++ks) {
+        const double va = Vt[(size_t)(4 * ks + tig) * LDC + gid], vb = Vt[(size_t)(4 * ks + tig) * LDC + 8 + gid];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-            d[mt][0] = u0r[mt] * rn[mt][0];
-            d[mt][1] = u0r[mt] * rn[mt][1];
+        for (int q = 0; q < NT; ++q) {
+            const double b = C[(size_t)(4 * ks + tig) * LDC + j0[q] + gid];
+            dmma(d[q][0], va, b);
+            dmma(d[q][1], vb, b);
         }
-        const double rcur[2][2] = {{rn[0][0], rn[0][1]}, {rn[1][0], rn[1][1]}};
-        ldR(j0 + 8 * nw, rn);
-#pragma unroll 8
-        for (int ks = 0; ks < KS1; ++ks) {
-            const double* row = C + (size_t)(4 * ks + tig) * LDC;
-            const double b = row[j0 + gid];
-            dmma(d[0], Vt[(size_t)(4 * ks + tig) * LDC + gid], b);
-            dmma(d[1], Vt[(size_t)(4 * ks + tig) * LDC + 8 + gid], b);
-        }
-        // W'_l = g_l (W_l + sum_{m<l} G[m][l] W'_m): finalise row l, push it down
+    }
 #pragma unroll
-        for (int l = 0; l < kNBW; ++l) {
-            const int mt = l >> 3;
-            if (gid == (l & 7)) {
-                const double gl = lds_nohoist(cgv + l);
-                d[mt][0] *= gl;
-                d[mt][1] *= gl;
+    for (int q = 0; q < NT; ++q)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) d[q][mt][e] = fma(u0r[mt], rcur[q][mt][e], d[q][mt][e]);
+    // W'_l = g_l (W_l + sum_{m<l} G[m][l] W'_m): finalise row l, push it down
+#pragma unroll
+    for (int l = 0; l < kNBW; ++l) {
+        const int mt = l >> 3;
+        if (gid == (l & 7)) {
+            const double gl = lds_nohoist(cgv + l);
+#pragma unroll
+            for (int q = 0; q < NT; ++q) {
+                d[q][mt][0] *= gl;
+                d[q][mt][1] *= gl;
             }
-            if (l + 1 < kNBW) {
-                const double w0 = __shfl_sync(0xffffffffu, d[mt][0], (l & 7) * 4 + tig);
-                const double w1 = __shfl_sync(0xffffffffu, d[mt][1], (l & 7) * 4 + tig);
+        }
+        if (l + 1 < kNBW) {
+            double w0[NT], w1[NT];
 #pragma unroll
-                for (int m2 = mt; m2 < 2; ++m2) {
-                    const int i = 8 * m2 + gid;
-                    if (i > l) {
-                        const double gg = lds_nohoist(Gs + l * kNBW + i);
-                        d[m2][0] = fma(gg, w0, d[m2][0]);
-                        d[m2][1] = fma(gg, w1, d[m2][1]);
+            for (int q = 0; q < NT; ++q) {
+                w0[q] = __shfl_sync(0xffffffffu, d[q][mt][0], (l & 7) * 4 + tig);
+                w1[q] = __shfl_sync(0xffffffffu, d[q][mt][1], (l & 7) * 4 + tig);
+            }
+#pragma unroll
+            for (int m2 = mt; m2 < 2; ++m2) {
+                const int i = 8 * m2 + gid;
+                if (i > l) {
+                    const double gg = lds_nohoist(Gs + l * kNBW + i);
+#pragma unroll
+                    for (int q = 0; q < NT; ++q) {
+                        d[q][m2][0] = fma(gg, w0[q], d[q][m2][0]);
+                        d[q][m2][1] = fma(gg, w1[q], d[q][m2][1]);
                     }
                 }
             }
         }
+    }
+#pragma unroll
+    for (int q = 0; q < NT; ++q)
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int j = j0 + 2 * tig + e;
-                if (j < n) R[(size_t)(p + 8 * mt + gid) * n + j] = fma(u0r[mt], d[mt][e], rcur[mt][e]);
+                const int j = j0[q] + 2 * tig + e;
+                if (ok[q] && j < n) R[(size_t)(p + 8 * mt + gid) * n + j] = fma(u0r[mt], d[q][mt][e], rcur[q][mt][e]);
             }
-        // B fragments of W': B[k][n] = W'[4 kt + k][n], lane (k = tig, n = gid); W' row
-        // i = 4 kt + tig lives in D tile kt/2 on lanes (i % 8) * 4 + n / 2, element n % 2
-        double b2[4];
+    // B fragments of W': B[k][n] = W'[4 kt + k][n], lane (k = tig, n = gid); W' row
+    // i = 4 kt + tig lives in D tile kt/2 on lanes (i % 8) * 4 + n / 2, element n % 2
+    double b2[NT][4];
 #pragma unroll
-        for (int kt = 0; kt < 4; ++kt) {
-            const int srcl = ((4 * kt + tig) & 7) * 4 + (gid >> 1);
-            const double x0 = __shfl_sync(0xffffffffu, d[kt >> 1][0], srcl);
-            const double x1 = __shfl_sync(0xffffffffu, d[kt >> 1][1], srcl);
-            b2[kt] = (gid & 1) ? x1 : x0;
+    for (int kt = 0; kt < 4; ++kt) {
+        const int srcl = ((4 * kt + tig) & 7) * 4 + (gid >> 1);
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+            const double x0 = __shfl_sync(0xffffffffu, d[q][kt >> 1][0], srcl);
+            const double x1 = __shfl_sync(0xffffffffu, d[q][kt >> 1][1], srcl);
+            b2[q][kt] = (gid & 1) ? x1 : x0;
         }
-#pragma unroll 4
-        for (int mt = 0; mt < MT2; ++mt) {
-            double2* cp2 = reinterpret_cast<double2*>(C + (size_t)(8 * mt + gid) * LDC + j0 + 2 * tig);
-            const double* vrow = Vt + (size_t)(8 * mt + gid) * LDC + tig;
+    }
+#pragma unroll 2
+    for (int mt = 0; mt < MT2; ++mt) {
+        const double* vrow = Vt + (size_t)(8 * mt + gid) * LDC + tig;
+        double vk[4];
+#pragma unroll
+        for (int kt = 0; kt < 4; ++kt) vk[kt] = vrow[4 * kt];
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+            if (!ok[q]) continue;
+            double2* cp2 = reinterpret_cast<double2*>(C + (size_t)(8 * mt + gid) * LDC + j0[q] + 2 * tig);
             const double2 cv = *cp2;
             double acc[2] = {cv.x, cv.y};
 #pragma unroll
-            for (int kt = 0; kt < 4; ++kt) dmma(acc, vrow[4 * kt], b2[kt]);
+            for (int kt = 0; kt < 4; ++kt) dmma(acc, vk[kt], b2[q][kt]);
             *cp2 = make_double2(acc[0], acc[1]);
         }
+    }
+}
+
+template <int ROWS, bool ILP2>
+__device__ __forceinline__ void wy_trailing(double* __restrict__ C, int LDC, int n, int p, int pe, int jend,
+                                            int warp, int nw, double* __restrict__ R, const double* Gs,
+                                            const double* cgv, const double* cuv) {
+    const int gid = (threadIdx.x & 31) >> 2;
+    const double u0r[2] = {cuv[gid], cuv[8 + gid]};
+    int j0 = pe + 8 * warp;
+    if constexpr (ILP2) {
+        for (; j0 + 8 * nw < jend; j0 += 16 * nw) {   // two tiles in lockstep
+            const int jj[2] = {j0, j0 + 8 * nw};
+            const bool ok[2] = {true, true};
+            wy_trailing_tiles<ROWS, 2>(C, LDC, n, p, jj, ok, R, Gs, cgv, u0r);
+        }
+    }
+    for (; j0 < jend; j0 += 8 * nw) {
+        const int jj[1] = {j0};
+        const bool ok[1] = {true};
+        wy_trailing_tiles<ROWS, 1>(C, LDC, n, p, jj, ok, R, Gs, cgv, u0r);
     }
 }
 
@@ -839,7 +882,10 @@ struct WyGroup {
 };
 __device__ __forceinline__ WyGroup wy_whole_cta(int n) { return WyGroup{0, (int)blockDim.x, 0, 1, n}; }
 
-template <int ROWS>
+// ILP2: two trailing tiles per warp in lockstep (measured per kernel shape: faster
+// for the 32-row single-chain leaf (C4 77.1 -> 76.0 ms) and the 16-row two-phase
+// leaf (2M x 1025: 918 -> 854 ms); slower for 32-row two-phase CTAs and 64/96-row tiles)
+template <int ROWS, bool ILP2 = false>
 __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* __restrict__ R, double* Gs,
                         double* Rd, double* cgv, double* cuv, int pw, const int* pred_prog = nullptr,
                         int* my_prog = nullptr, bool la_wait = false, WyGroup grp = WyGroup{0, 0, 0, 1, -1}) {
@@ -894,7 +940,7 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
         const int nbn = min(kNBW, n - pe);
         double *G0 = Gs + buf * kNBW * kNBW, *g0 = cgv + buf * kNBW, *u0 = cuv + buf * kNBW;
         if (nw == 1) {
-            wy_trailing<ROWS>(C, LDC, n, p, pe, n, 0, 1, R, G0, g0, u0);
+            wy_trailing<ROWS, ILP2>(C, LDC, n, p, pe, n, 0, 1, R, G0, g0, u0);
             __syncwarp();
             if (fact) {
                 rd_put(Rd, rdn);
@@ -915,14 +961,14 @@ __device__ void wy_fold(double* __restrict__ C, int LDC, int n, int k0, double* 
                                   Gs + (buf ^ 1) * kNBW * kNBW);
             if (lane0) qr_ev(5, p);
         } else {
-            wy_trailing<ROWS>(C, LDC, n, p, pe, pe + nbn, tw, nw - 1, R, G0, g0, u0);   // panel p+1's columns first
+            wy_trailing<ROWS, ILP2>(C, LDC, n, p, pe, pe + nbn, tw, nw - 1, R, G0, g0, u0);   // panel p+1's columns first
             if (tw == 0 && (gtid & 31) == 0) qr_ev(3, p);
             __threadfence_block();
             // warps without a look-ahead tile wait with the panel warp so the
             // look-ahead chain is not slowed by their trailing work
             if (la_wait && 8 * tw >= nbn) named_bar_sync(grp.bar_la, grp.threads);
             else named_bar_arrive(grp.bar_la, grp.threads);
-            wy_trailing<ROWS>(C, LDC, n, p, pe + nbn, n, tw, nw - 1, R, G0, g0, u0);
+            wy_trailing<ROWS, ILP2>(C, LDC, n, p, pe + nbn, n, tw, nw - 1, R, G0, g0, u0);
             if (tw == 0 && (gtid & 31) == 0) qr_ev(4, p);
         }
         step_sync();
@@ -1036,7 +1082,7 @@ __global__ void __launch_bounds__(32 * NW, (NW == 4 && ROWS <= 32) ? 3 : 1)
             }
         }
         __syncthreads();
-        wy_fold<ROWS>(C, LDC, n, 0, R, Gs, Rd, cgv, cuv, pw, nullptr, nullptr, la_wait != 0);
+        wy_fold<ROWS, ROWS == 32>(C, LDC, n, 0, R, Gs, Rd, cgv, cuv, pw, nullptr, nullptr, la_wait != 0);
     }
     if (bad) atomicOr(flag, 1);
 }
@@ -1130,12 +1176,12 @@ __global__ void __launch_bounds__(32 * (NWA + NWB), (NWA + NWB) * 32 * 168 * 2 <
                     }
                 }
                 named_bar_sync(gA.bar_step, TA);
-                wy_fold<ROWS>(bufA, LDC, n, 0, R, Gs(auxA), Rd(auxA), cg(auxA), cu(auxA), 0, nullptr, nullptr,
+                wy_fold<ROWS, ROWS == 16>(bufA, LDC, n, 0, R, Gs(auxA), Rd(auxA), cg(auxA), cu(auxA), 0, nullptr, nullptr,
                               la_wait != 0, gA);
             }
         } else if (k >= 1) {
             // columns >= ps of tile k-1 live in bufB (column c at bufB[r * LDCB + c - ps])
-            wy_fold<ROWS>(bufB - ps, LDCB, n, ps, R, Gs(auxB), Rd(auxB), cg(auxB), cu(auxB), 0, nullptr, nullptr,
+            wy_fold<ROWS, ROWS == 16>(bufB - ps, LDCB, n, ps, R, Gs(auxB), Rd(auxB), cg(auxB), cu(auxB), 0, nullptr, nullptr,
                           la_wait != 0, gB);
         }
         __syncthreads();
