@@ -330,16 +330,23 @@ __device__ double block_max(double v, double* red) { return -block_min(-v, red);
 // before a ridge refactorisation so rho is measured on the unregularised R.
 template <int TR, int P>
 __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
-    k_tsqr_solve(double* __restrict__ R, double* __restrict__ Rorig, int M, long long n_total,
-                 const int* __restrict__ flag, double* __restrict__ beta, SolveDev* __restrict__ out) {
+    k_tsqr_solve(double* __restrict__ Rg, double* __restrict__ Rorig, int M, long long n_total,
+                 const int* __restrict__ flag, double* __restrict__ beta, SolveDev* __restrict__ out, int r_smem) {
     constexpr int ROWS = TR * P;
     __shared__ __align__(16) double vbuf[2 * ROWS];
     __shared__ double coefs[4];
     __shared__ double red[32];
-    __shared__ double bk;
-    extern __shared__ __align__(16) double zs[];   // [n] signs / rhs / beta
+    extern __shared__ __align__(16) double zs[];   // [3][n] signs / rhs, R_kk, beta; then R when r_smem
     const int n = M + 1, j = col_of<P>(n), half = threadIdx.x % P;
     const bool own = j >= 0 && j < n && half == 0;
+    // small n: the whole R in shared memory (one coalesced copy in and out), so the
+    // column walks below (sign flips, norms, the ridge fold) are not chains of L2 loads
+    double* R = Rg;
+    if (r_smem) {
+        R = zs + 3 * ((n + 1) & ~1);
+        for (int e = threadIdx.x; e < n * n; e += blockDim.x) R[e] = Rg[e];
+        __syncthreads();
+    }
     // sign normalisation: flip row k when R_kk < 0 (signs read into smem first)
     if (own) zs[j] = R[(size_t)j * n + j] < 0.0 ? -1.0 : 1.0;
     __syncthreads();
@@ -356,8 +363,7 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
     const double fro2 = block_sum(f2, red);
     const bool ridge = !(dmin > DBL_EPSILON * (double)M * dmax);
     double lambda = 0.0;
-    if (own)
-        for (int k = 0; k < n; ++k) Rorig[(size_t)k * n + j] = R[(size_t)k * n + j];
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) Rorig[e] = R[e];   // sign-normalised, pre-ridge
     if (ridge) {
         lambda = 1e-8 * fro2 / (double)M;
         const double sl = sqrt(lambda);
@@ -376,24 +382,40 @@ __global__ void __launch_bounds__(Fold<TR, P>::MAX_THREADS, 1)
             for (int k = 0; k <= j; ++k) R[(size_t)k * n + j] *= zs[k];
         __syncthreads();
     }
-    // back substitution: thread (i, 0) holds z_i
-    if (diag) zs[j] = R[(size_t)j * n + M];
+    // back substitution, one barrier per step: thread (i, 0) owns z_i and reads
+    // row i of R (R[i][k] at step k) through a 4-deep register prefetch queue, so
+    // the L2 latency of R is off the step chain; the diagonal sits in shared
+    // memory and every thread forms b_k = z_k / R_kk itself (no broadcast step).
+    double* rdg = zs + n;       // [n] R_kk
+    double* bs = zs + 2 * n;    // [n] beta
+    if (diag) {
+        zs[j] = R[(size_t)j * n + M];
+        rdg[j] = R[(size_t)j * n + j];
+    }
     __syncthreads();
+    auto rowv = [&](int k) { return (diag && k > j) ? R[(size_t)j * n + k] : 0.0; };
+    double q0 = rowv(M - 1), q1 = rowv(M - 2), q2 = rowv(M - 3), q3 = rowv(M - 4);
     for (int k = M - 1; k >= 0; --k) {
-        if (threadIdx.x == 0) bk = zs[k] / R[(size_t)k * n + k];
-        __syncthreads();
-        if (own && j < k) zs[j] -= R[(size_t)j * n + k] * bk;
-        if (own && j == k) zs[k] = bk;
+        const double rjk = q0;
+        q0 = q1;
+        q1 = q2;
+        q2 = q3;
+        q3 = rowv(k - 4);
+        const double b = zs[k] / rdg[k];   // zs[k] is final: its last update was in step k+1
+        if (diag && j < k) zs[j] -= rjk * b;
+        if (diag && j == k) bs[k] = b;
         __syncthreads();
     }
-    if (diag) beta[j] = zs[j];
+    if (diag) beta[j] = bs[j];
     // rho = || R_orig [beta; -1] ||
     double s = 0.0;
     if (own) {
-        for (int c = j; c < M; ++c) s += Rorig[(size_t)j * n + c] * zs[c];
+        for (int c = j; c < M; ++c) s += Rorig[(size_t)j * n + c] * bs[c];
         s -= Rorig[(size_t)j * n + M];
     }
     const double rho2 = block_sum(own ? s * s : 0.0, red);
+    if (r_smem)
+        for (int e = threadIdx.x; e < n * n; e += blockDim.x) Rg[e] = R[e];
     if (threadIdx.x == 0) {
         out->rho = sqrt(rho2);
         out->rmse = sqrt(rho2) / sqrt((double)n_total);
@@ -1648,10 +1670,13 @@ cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta) {
         h->launches++;
         return cudaGetLastError();
     }
-    const size_t smem = ((n + 1) & ~1) * sizeof(double);
+    size_t smem = 3 * ((n + 1) & ~1) * sizeof(double);   // z, R_kk, beta
+    const int r_smem = smem + (size_t)n * n * sizeof(double) <= 160 * 1024 ? 1 : 0;   // R resident (n <= ~140)
+    if (r_smem) smem += (size_t)n * n * sizeof(double);
     return dispatch(v, [&](auto tr, auto p) {
-        k_tsqr_solve<decltype(tr)::value, decltype(p)::value><<<1, threads, smem, h->stream>>>(
-            h->Rws, Rorig, h->M, (long long)n_total, h->flag, beta, h->sdev);
+        auto kern = k_tsqr_solve<decltype(tr)::value, decltype(p)::value>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<1, threads, smem, h->stream>>>(h->Rws, Rorig, h->M, (long long)n_total, h->flag, beta, h->sdev, r_smem);
         h->launches++;
         return cudaGetLastError();
     });

@@ -182,6 +182,29 @@ def test_H_written_once_and_ld_respected():
     assert np.abs(H[:, :M].cpu().numpy() - ref).max() <= H_TOL
 
 
+@pytest.mark.parametrize("arch,M,Q,S", [("lstm", 256, 12, 1), ("lstm", 128, 10, 2), ("gru", 128, 10, 4),
+                                        ("lstm", 512, 4, 1), ("gru", 256, 4, 1), ("fc", 128, 6, 1)])
+def test_x_staging_layouts_bitwise(arch, M, Q, S):
+    """a1 window staging (one cp.async.bulk of each full tile's X block): a padded
+    row stride (ldx > Q*d, the padding travels with the block) and an X that is not
+    16-byte aligned (staging off, x(t) through L1) give bitwise the H of the
+    contiguous, aligned X; N is ragged so the partial last tile is read directly."""
+    N = 3 * 128 + 45
+    X, _, _ = inputs(N, Q, S, seed=M + Q)
+    e = E(arch, S, M, Q, 6)
+    assert e.path == 2
+    Xd = torch.from_numpy(X).cuda()
+    H0 = e.build_H(Xd)
+    pad = torch.full((N, Q * S + 5), float("nan"), device="cuda")
+    pad[:, :Q * S] = Xd.reshape(N, Q * S)
+    H1 = e.build_H(pad[:, :Q * S])
+    flat = torch.zeros(N * Q * S + 1, device="cuda")
+    flat[1:] = Xd.reshape(-1)
+    H2 = e.build_H(flat[1:].view(N, Q * S))
+    torch.cuda.synchronize()
+    assert torch.equal(H0, H1) and torch.equal(H0, H2)
+
+
 @pytest.mark.parametrize("arch,M", [("lstm", 128), ("gru", 32), ("elman", 20)])
 def test_build_H_from_host_chunked(arch, M):
     """The chunked, copy-overlapped build from pinned host X equals build_H."""
