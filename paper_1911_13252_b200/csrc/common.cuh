@@ -36,6 +36,7 @@ struct Tune {
     int wy_nw = 0;      // ELMRNN_WY_NW: WY leaf/merge warps per CTA (4 or 8; 0 = by n)
     int max_slabs = 0;  // ELMRNN_TSQR_MAXSLABS: cap on the TSQR leaf count (0 = by size)
     int wy_2phase = 1;  // ELMRNN_WY_2PHASE: 0 = single-chain WY leaf only; 2 = two-phase also for n <= 320
+    int merge_small = 1; // ELMRNN_MERGE_SMALL: 0 = top tree levels keep the tall merge tiles
 };
 
 }  // namespace elm

@@ -1445,6 +1445,42 @@ cudaError_t ensure_solve_ws(elmrnn* h, int64_t slabs) {
     return cudaSuccess;
 }
 
+// One tree level of the WY merge: P CTAs per pair (pipelined chunks, cooperative
+// launch) when P >= 2, else one CTA per pair.
+template <int RW, int NW>
+static cudaError_t wy_merge_level(elmrnn* h, int64_t slabs, int64_t stride, int n, int64_t pairs, int P) {
+    const size_t sm = wy_smem_bytes(RW, n);
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_tsqr_merge_wy<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_tsqr_merge_wy_par<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)))
+        return e;
+    if (P >= 2) {
+        if ((e = cudaMemsetAsync(h->prog, 0, sizeof(int) * pairs * kMaxChunks, h->stream))) return e;
+        double* rws = h->Rws;
+        int64_t sl = slabs, sd = stride;
+        int nn = n;
+        int* pg = h->prog;
+        void* args[] = {&rws, &sl, &sd, &nn, &P, &pg};
+        e = cudaLaunchCooperativeKernel((const void*)k_tsqr_merge_wy_par<RW, NW>, dim3((unsigned)(pairs * P)),
+                                        dim3(32 * NW), args, sm, h->stream);
+    } else {
+        k_tsqr_merge_wy<RW, NW><<<(unsigned)pairs, 32 * NW, sm, h->stream>>>(h->Rws, slabs, stride, n);
+        e = cudaGetLastError();
+    }
+    h->launches++;
+    return e;
+}
+
+template <int RW, int NW>
+static int64_t wy_merge_resident(const elmrnn* h, int n) {
+    const size_t sm = wy_smem_bytes(RW, n);
+    cudaFuncSetAttribute(k_tsqr_merge_wy_par<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tsqr_merge_wy_par<RW, NW>, 32 * NW, sm);
+    return (int64_t)occ * h->sm_count;
+}
+
 static cudaError_t tree(elmrnn* h, int64_t slabs) {
     const int n = h->M + h->nrhs;
     const Var v = pick_var(n);
@@ -1454,37 +1490,33 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
         // merges are latency-bound (few pairs at the top of the tree): the
         // tallest tile that fits means the fewest panel steps per fold, and the
         // SMs a level leaves idle pipeline each pair's row chunks
-        // (k_tsqr_merge_wy_par)
-        const bool par_ok = true;
+        // (k_tsqr_merge_wy_par).  Levels with so few pairs that every pair can
+        // pipeline ALL its short chunks (32 rows; 16 when n > 320) on its own CTAs
+        // take those instead: a chunk trails its predecessor by two panel steps,
+        // so a chunk's fold is shorter (measured at n = 257: 0.46-0.47 -> 0.41 ms
+        // per top level; the lag between chunks compounds, DESIGN 6.4b)
+        const bool small32 = wy_smem_bytes(32, n) <= 220 * 1024;
+        const int rws = small32 ? 32 : 16, nchs = (n + rws - 1) / rws;
+        const int64_t res_s = small32 ? wy_merge_resident<32, 4>(h, n) : wy_merge_resident<16, 8>(h, n);
         return wy_dispatch_merge(n, [&](auto rows, auto nwc) {
             constexpr int RW = decltype(rows)::value, NW = decltype(nwc)::value;
-            const size_t sm = wy_smem_bytes(RW, n);
-            cudaFuncSetAttribute(k_tsqr_merge_wy<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            cudaFuncSetAttribute(k_tsqr_merge_wy_par<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            int occ = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tsqr_merge_wy_par<RW, NW>, wy_threads(n), sm);
-            const int64_t resident = (int64_t)occ * h->sm_count;
+            const int64_t resident = wy_merge_resident<RW, NW>(h, n);
             const int nch = (n + RW - 1) / RW;
             for (int64_t stride = 1; stride < slabs && stride < max_stride; stride *= 2) {
-                int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
-                int P = (int)std::min<int64_t>(nch, resident / std::max<int64_t>(pairs, 1));
-                if (par_ok && P >= 2 && nch <= kMaxChunks && pairs <= h->prog_pairs) {
-                    cudaError_t e = cudaMemsetAsync(h->prog, 0, sizeof(int) * pairs * kMaxChunks, h->stream);
-                    if (e) return e;
-                    double* rws = h->Rws;
-                    int64_t sl = slabs, sd = stride;
-                    int nn = n;
-                    int* pg = h->prog;
-                    void* args[] = {&rws, &sl, &sd, &nn, &P, &pg};
-                    e = cudaLaunchCooperativeKernel((const void*)k_tsqr_merge_wy_par<RW, NW>, dim3((unsigned)(pairs * P)),
-                                                    dim3(wy_threads(n)), args, sm, h->stream);
-                    if (e) return e;
+                const int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
+                cudaError_t e;
+                if (h->tune.merge_small != 0 && RW > rws && nchs <= kMaxChunks && pairs <= h->prog_pairs &&
+                    pairs * nchs <= res_s) {
+                    e = small32 ? wy_merge_level<32, 4>(h, slabs, stride, n, pairs, nchs)
+                                : wy_merge_level<16, 8>(h, slabs, stride, n, pairs, nchs);
                 } else {
-                    k_tsqr_merge_wy<RW, NW><<<(unsigned)pairs, wy_threads(n), sm, h->stream>>>(h->Rws, slabs, stride, n);
+                    int P = (int)std::min<int64_t>(nch, resident / std::max<int64_t>(pairs, 1));
+                    if (!(P >= 2 && nch <= kMaxChunks && pairs <= h->prog_pairs)) P = 1;
+                    e = wy_merge_level<RW, NW>(h, slabs, stride, n, pairs, P);
                 }
-                h->launches++;
+                if (e) return e;
             }
-            return cudaGetLastError();
+            return cudaSuccess;
         });
     }
     return dispatch(v, [&](auto tr, auto p) {
