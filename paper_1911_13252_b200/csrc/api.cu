@@ -69,6 +69,7 @@ elmrnn_status elmrnn_init_ex(elmrnn_t* out, int arch, int d, int M, int Q, uint6
         if (const char* e = std::getenv("ELMRNN_TSQR_MAXSLABS")) h->tune.max_slabs = std::atoi(e);
         if (const char* e = std::getenv("ELMRNN_WY_2PHASE")) h->tune.wy_2phase = std::atoi(e);
         if (const char* e = std::getenv("ELMRNN_MERGE_SMALL")) h->tune.merge_small = std::atoi(e);
+        if (const char* e = std::getenv("ELMRNN_WIDE_PAIR")) h->tune.wide_pair = std::atoi(e);
     }
     cudaError_t e;
     if ((e = cudaGetDevice(&h->device))) { elmrnn_destroy(h); return cuda_fail(nullptr, e, "cudaGetDevice"); }

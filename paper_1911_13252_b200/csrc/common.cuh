@@ -37,6 +37,7 @@ struct Tune {
     int max_slabs = 0;  // ELMRNN_TSQR_MAXSLABS: cap on the TSQR leaf count (0 = by size)
     int wy_2phase = 1;  // ELMRNN_WY_2PHASE: 0 = single-chain WY leaf only; 2 = two-phase also for n <= 320
     int merge_small = 1; // ELMRNN_MERGE_SMALL: 0 = top tree levels keep the tall merge tiles
+    int wide_pair = 1;   // ELMRNN_WIDE_PAIR: 0 = wide LSTM MMA units of one 32-neuron chunk (N = 128)
 };
 
 }  // namespace elm
@@ -126,6 +127,7 @@ bool gru_tc_supported(const elmrnn* h);
 cudaError_t gru_tc_prepare(elmrnn* h);
 cudaError_t launch_gru_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);
 bool lstm_wide_supported(const elmrnn* h);
+bool lstm_wide_pair(const elmrnn* h);
 bool gru_wide_supported(const elmrnn* h);
 cudaError_t gru_wide_prepare(elmrnn* h);
 cudaError_t launch_gru_wide(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh);

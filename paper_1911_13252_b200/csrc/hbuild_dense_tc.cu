@@ -450,7 +450,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
 
 // Build the pre-swizzled fp16 hi/lo images of U_cat (scaled by 2^sigma):
 // image[(n*KS + s)*2 + part][sw128(nrow = jj*4 + g, kk)] for neuron n*32+jj, gate g, K = 64s + kk.
-__global__ void k_pack_u(const float* __restrict__ U, int M, float scale, uint8_t* __restrict__ img) {
+// pair = 1 (wide LSTM with N = 256 MMA units): chunks 2m, 2m+1 of a K-slice are adjacent
+// 16 KB tiles, i.e. one 256-row SW128 tile: image[((m*KS + s)*2 + part)][chunk % 2][16 KB]
+__global__ void k_pack_u(const float* __restrict__ U, int M, float scale, uint8_t* __restrict__ img, int pair) {
     const int KS = M / 64, NCH = M / 32;
     const int64_t total = (int64_t)NCH * KS * 128 * 64;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -462,10 +464,11 @@ __global__ void k_pack_u(const float* __restrict__ U, int M, float scale, uint8_
         float v = U[(size_t)(64 * s + kk) * (4 * M) + g * M + n * 32 + jj] * scale;
         __half hi = __float2half_rn(v);
         __half lo = __float2half_rn(v - __half2float(hi));
-        uint8_t* base = img + (size_t)((n * KS + s) * 2) * kTcSliceBytes;
+        uint8_t* base = pair ? img + (size_t)(((n >> 1) * KS + s) * 2) * 2 * kTcSliceBytes + (size_t)(n & 1) * kTcSliceBytes
+                             : img + (size_t)((n * KS + s) * 2) * kTcSliceBytes;
         uint32_t off = ptx::sw128_offset(nrow, kk);
         *reinterpret_cast<__half*>(base + off) = hi;
-        *reinterpret_cast<__half*>(base + kTcSliceBytes + off) = lo;
+        *reinterpret_cast<__half*>(base + (pair ? 2 : 1) * kTcSliceBytes + off) = lo;
     }
 }
 
@@ -572,7 +575,8 @@ cudaError_t tc_prepare(elmrnn* h) {
         return e;
     int64_t total = (int64_t)(M / 32) * (M / 64) * 128 * 64;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
-    k_pack_u<<<blocks, 256, 0, h->stream>>>(h->rec, M, scale, static_cast<uint8_t*>(h->tc_ops));
+    k_pack_u<<<blocks, 256, 0, h->stream>>>(h->rec, M, scale, static_cast<uint8_t*>(h->tc_ops),
+                                            wide && lstm_wide_pair(h) ? 1 : 0);
     h->launches++;
     return cudaGetLastError();
 }

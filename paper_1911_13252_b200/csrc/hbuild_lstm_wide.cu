@@ -38,21 +38,31 @@ namespace elm {
 namespace {
 
 constexpr int kWRows = 128;
-constexpr int kWStages = 3;
 constexpr int kWTile = 128 * 64 * 2;          // one 128 x 64 fp16 SW128 tile (16 KB)
 constexpr int kWPair = 2 * kWTile;            // hi + lo
-constexpr int kWStageBytes = 2 * kWPair;      // A pair + B pair
 constexpr int kWEpiWarps = 16;
 constexpr int kWProdWarp = kWEpiWarps, kWMmaWarp = kWEpiWarps + 1;
 constexpr int kWThreads = (kWEpiWarps + 2) * 32;
-constexpr int kWSmem = 1024 + kWStages * kWStageBytes + 256;
+// PAIR: one MMA unit = two 32-neuron chunks (N = 256 accumulator columns, 128 x 256 x 16
+// MMAs): h(t-1) is streamed once per chunk PAIR instead of once per chunk, and each
+// stage carries 32 KB of A for 64 KB of B (the SS operand bytes per MMA flop drop by a
+// quarter); 2 stages of 96 KB.  Else 3 stages of 64 KB, N = 128.
+template <bool PAIR>
+struct WCfg {
+    static constexpr int STAGES = PAIR ? 2 : 3;
+    static constexpr int BTILE = PAIR ? 2 * kWTile : kWTile;    // B hi (or lo) bytes per stage
+    static constexpr int STAGE = kWPair + 2 * BTILE;              // A hi|lo + B hi|lo
+    static constexpr int SMEM = 1024 + STAGES * STAGE + 256;      // + the X block
+    static constexpr int ACC = PAIR ? 256 : 128;                  // accumulator columns per unit
+    static constexpr int TMEM_COLS = 2 * ACC;
+};
 
 struct WideParams {
     const float* X;
     int64_t ldx, N;
     float* H;
     int64_t ldh;
-    const uint8_t* Uimg;   // [NCH][KS][hi|lo][16 KB] (hbuild_dense_tc.cu k_pack_u layout)
+    const uint8_t* Uimg;   // [units][KS][hi|lo][16 KB per chunk of the unit] (hbuild_dense_tc.cu k_pack_u)
     const float* wb;       // [M][4][SS+1]: k_g (b, W_0..W_{S-1})
     uint8_t* hist;         // [grid][2][KS][hi|lo][16 KB]: A images of h(t)
     float* cst;            // [grid][NCH][4][128][8]: c(t)
@@ -79,8 +89,10 @@ __device__ __forceinline__ void fence_proxy_async_global_w() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-template <int SS>
+template <int SS, bool PAIR>
 __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constant__ WideParams p) {
+    using CF = WCfg<PAIR>;
+    constexpr int kWStages = CF::STAGES, kWStageBytes = CF::STAGE;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stages = smem;
@@ -111,14 +123,14 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
         ptx::fence_mbar_init();
     }
     if (warp == kWProdWarp) {
-        ptx::tmem_alloc(tmem_slot, 256);
+        ptx::tmem_alloc(tmem_slot, CF::TMEM_COLS);
         ptx::tmem_relinquish();
     }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const int NCH = p.NCH, KS = p.KS;
+    const int NCH = p.NCH, KS = p.KS, NU = PAIR ? NCH / 2 : NCH;   // MMA units per step
     const size_t slot_bytes = (size_t)KS * kWPair;
     uint8_t* hist = p.hist + (size_t)blockIdx.x * 2 * slot_bytes;
 
@@ -126,7 +138,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
         // ---------------- producer: per step t >= 2, (chunk n, K-slice ks) pairs of
         // [h(t-1) slice ks | U_cat chunk n slice ks]; whole warp loops, one lane issues
         uint32_t st = 0, ph = 0, hph = 0, xph = 0;
-        const uint32_t bbytes = p.two_pass ? kWTile : kWPair;   // U hi only when U_lo = 0
+        const uint32_t bbytes = p.two_pass ? CF::BTILE : 2 * CF::BTILE;   // U hi only when U_lo = 0
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             if (ptx::xstage_tile(p.xbytes, tile, p.N))   // the tile's X block (a1)
                 ptx::xstage_issue(xbuf, p.X, p.ldx, tile, p.xbytes, x_full, x_empty, xph);
@@ -135,14 +147,15 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
                 ptx::mbar_wait(hist_ready, hph);   // h(t-1) fully written by the epilogue
                 hph ^= 1;
                 fence_proxy_async_global_w();
-                for (int n = 0; n < NCH; ++n) {
+                for (int n = 0; n < NU; ++n) {
                     for (int ks = 0; ks < KS; ++ks) {
                         ptx::mbar_wait(empty + st, ph ^ 1);
                         if (ptx::elect_one()) {
                             uint8_t* sb = stages + st * kWStageBytes;
                             ptx::mbar_arrive_expect_tx(full + st, kWPair + bbytes);
                             ptx::bulk_g2s(sb, slot + (size_t)ks * kWPair, kWPair, full + st);
-                            ptx::bulk_g2s(sb + kWPair, p.Uimg + (size_t)(n * KS + ks) * kWPair, bbytes, full + st);
+                            ptx::bulk_g2s(sb + kWPair, p.Uimg + (size_t)(n * KS + ks) * 2 * CF::BTILE, bbytes,
+                                          full + st);
                         }
                         __syncwarp();
                         if (++st == kWStages) { st = 0; ph ^= 1; }
@@ -152,23 +165,23 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
         }
     } else if (warp == kWMmaWarp) {
         // ---------------- MMA issuer: 12 SS MMAs (4 K-steps x 3 passes) per stage
-        constexpr uint32_t idesc = ptx::idesc_f16(128, 128);
+        constexpr uint32_t idesc = ptx::idesc_f16(128, CF::ACC);
         const uint64_t dbase = ptx::desc_sw128_kmajor(ptx::smem_u32(stages));
         const bool two = p.two_pass != 0;
         uint32_t st = 0, ph = 0, ach = 0, aph = 0;
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             for (int t = 2; t <= p.Q; ++t) {
-                for (int n = 0; n < NCH; ++n) {
+                for (int n = 0; n < NU; ++n) {
                     ptx::mbar_wait(acc_empty + ach, aph ^ 1);
                     ptx::tc_fence_after();
-                    const uint32_t d = tmem + ach * 128;
+                    const uint32_t d = tmem + ach * CF::ACC;
                     for (int ks = 0; ks < KS; ++ks) {
                         ptx::mbar_wait(full + st, ph);
                         ptx::tc_fence_after();
                         const uint64_t ah = dbase + (uint64_t)((st * kWStageBytes) >> 4);
                         const uint64_t al = ah + (uint64_t)(kWTile >> 4);
                         const uint64_t bh = ah + (uint64_t)(kWPair >> 4);
-                        const uint64_t bl = bh + (uint64_t)(kWTile >> 4);
+                        const uint64_t bl = bh + (uint64_t)(CF::BTILE >> 4);
                         if (ptx::elect_one()) {
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk) {
@@ -218,15 +231,22 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
                 for (int n = 0; n < NCH; ++n) {
                     float a[2][16];   // 2 groups x 4 neurons x (o, c, lambda, in), scaled domain
                     if (t >= 2) {
-                        ptx::mbar_wait(acc_full + ach, aph);
-                        ptx::tc_fence_after();
-                        tmem_ld16w(lane_base + ach * 128 + (8 * u) * 4, a[0]);
-                        tmem_ld16w(lane_base + ach * 128 + (8 * u + 4) * 4, a[1]);
+                        // PAIR: chunks 2m, 2m+1 are the two 128-column halves of one accumulator
+                        const bool first = !PAIR || (n & 1) == 0, last = !PAIR || (n & 1) == 1;
+                        if (first) {
+                            ptx::mbar_wait(acc_full + ach, aph);
+                            ptx::tc_fence_after();
+                        }
+                        const uint32_t acol = ach * CF::ACC + (PAIR ? (n & 1) * 128 : 0);
+                        tmem_ld16w(lane_base + acol + (8 * u) * 4, a[0]);
+                        tmem_ld16w(lane_base + acol + (8 * u + 4) * 4, a[1]);
                         ptx::tmem_wait_ld();
-                        ptx::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(acc_empty + ach);
-                        if (++ach == 2) { ach = 0; aph ^= 1; }
+                        if (last) {
+                            ptx::tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) ptx::mbar_arrive(acc_empty + ach);
+                            if (++ach == 2) { ach = 0; aph ^= 1; }
+                        }
                     } else {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) a[0][i] = a[1][i] = 0.0f;
@@ -313,12 +333,14 @@ __global__ void __launch_bounds__(kWThreads, 1) k_lstm_wide(const __grid_constan
     __syncthreads();
     if (warp == kWProdWarp) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem, 256);
+        ptx::tmem_dealloc(tmem, CF::TMEM_COLS);
     }
 }
 
-template <int SS>
+template <int SS, bool PAIR>
 cudaError_t launch_wide_ss(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh) {
+    using CF = WCfg<PAIR>;
+    constexpr int kWSmem = CF::SMEM;
     WideParams p{};
     p.X = X; p.ldx = ldx; p.N = N; p.H = H; p.ldh = ldh;
     p.M = h->M; p.S = h->S; p.Q = h->Q; p.NCH = h->M / 32; p.KS = h->M / 64;
@@ -346,13 +368,16 @@ cudaError_t launch_wide_ss(elmrnn* h, const float* X, int64_t ldx, int64_t N, fl
     }
     p.hist = reinterpret_cast<uint8_t*>(h->scratch);
     p.cst = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(h->scratch) + hist_bytes);
-    if ((e = cudaFuncSetAttribute(k_lstm_wide<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-    k_lstm_wide<SS><<<grid, kWThreads, smem, h->stream>>>(p);
+    if ((e = cudaFuncSetAttribute(k_lstm_wide<SS, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+    k_lstm_wide<SS, PAIR><<<grid, kWThreads, smem, h->stream>>>(p);
     h->launches++;
     return cudaGetLastError();
 }
 
 }  // namespace
+
+// chunk pairs (N = 256 MMA units): every wide M has an even chunk count (M % 64 == 0)
+bool lstm_wide_pair(const elmrnn* h) { return h->tune.wide_pair != 0; }
 
 bool lstm_wide_supported(const elmrnn* h) {
     return h->arch == kArchLSTM && h->M > 256 && h->M <= 1024 && h->M % 64 == 0 && h->S <= 4;
@@ -362,9 +387,9 @@ size_t lstm_wide_wb_offset(const elmrnn* h) { return (size_t)(h->M / 32) * (h->M
 
 cudaError_t launch_lstm_wide(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh) {
     switch (h->S <= 1 ? 1 : (h->S <= 2 ? 2 : 4)) {
-    case 1: return launch_wide_ss<1>(h, X, ldx, N, H, ldh);
-    case 2: return launch_wide_ss<2>(h, X, ldx, N, H, ldh);
-    case 4: return launch_wide_ss<4>(h, X, ldx, N, H, ldh);
+    case 1: return lstm_wide_pair(h) ? launch_wide_ss<1, true>(h, X, ldx, N, H, ldh) : launch_wide_ss<1, false>(h, X, ldx, N, H, ldh);
+    case 2: return lstm_wide_pair(h) ? launch_wide_ss<2, true>(h, X, ldx, N, H, ldh) : launch_wide_ss<2, false>(h, X, ldx, N, H, ldh);
+    case 4: return lstm_wide_pair(h) ? launch_wide_ss<4, true>(h, X, ldx, N, H, ldh) : launch_wide_ss<4, false>(h, X, ldx, N, H, ldh);
     }
     return cudaErrorNotSupported;
 }
