@@ -30,14 +30,22 @@ namespace elm {
 namespace {
 
 constexpr int kQRows = 128;
-constexpr int kQStages = 3;
 constexpr int kQTile = 128 * 64 * 2;
 constexpr int kQPair = 2 * kQTile;
-constexpr int kQStageBytes = 2 * kQPair;
 constexpr int kQEpiWarps = 16;
 constexpr int kQProdWarp = kQEpiWarps, kQMmaWarp = kQEpiWarps + 1;
 constexpr int kQThreads = (kQEpiWarps + 2) * 32;
-constexpr int kQSmem = 1024 + kQStages * kQStageBytes + 256;
+// PAIR (M % 256 == 0): MMA units of two chunks of the same phase (N = 256), as in
+// hbuild_lstm_wide.cu: the A image is streamed once per chunk pair; 2 stages of 96 KB.
+template <bool PAIR>
+struct QCfg {
+    static constexpr int STAGES = PAIR ? 2 : 3;
+    static constexpr int BTILE = PAIR ? 2 * kQTile : kQTile;
+    static constexpr int STAGE = kQPair + 2 * BTILE;
+    static constexpr int SMEM = 1024 + STAGES * STAGE + 256;   // + the X block
+    static constexpr int ACC = PAIR ? 256 : 128;
+    static constexpr int TMEM_COLS = 2 * ACC;
+};
 
 struct GruWideParams {
     const float* X;
@@ -98,8 +106,10 @@ __device__ __forceinline__ void st8(float* p, const float* v) {
     reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
 }
 
-template <int SS>
+template <int SS, bool PAIR>
 __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant__ GruWideParams p) {
+    using CF = QCfg<PAIR>;
+    constexpr int kQStages = CF::STAGES, kQStageBytes = CF::STAGE;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stages = smem;
@@ -132,7 +142,7 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
         ptx::fence_mbar_init();
     }
     if (warp == kQProdWarp) {
-        ptx::tmem_alloc(tmem_slot, 256);
+        ptx::tmem_alloc(tmem_slot, CF::TMEM_COLS);
         ptx::tmem_relinquish();
     }
     ptx::tc_fence_before();
@@ -146,15 +156,15 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
 
     if (warp == kQProdWarp) {
         uint32_t st = 0, ph = 0, hph = 0, rph = 0, xph = 0;
-        const uint32_t bbytes = p.two_pass ? kQTile : kQPair;
-        auto load = [&](const uint8_t* a_img, int chunk) {
+        const uint32_t bbytes = p.two_pass ? CF::BTILE : 2 * CF::BTILE;
+        auto load = [&](const uint8_t* a_img, int chunk) {   // chunk = MMA unit index
             for (int ks = 0; ks < KS; ++ks) {
                 ptx::mbar_wait(empty + st, ph ^ 1);
                 if (ptx::elect_one()) {
                     uint8_t* sb = stages + st * kQStageBytes;
                     ptx::mbar_arrive_expect_tx(full + st, kQPair + bbytes);
                     ptx::bulk_g2s(sb, a_img + (size_t)ks * kQPair, kQPair, full + st);
-                    ptx::bulk_g2s(sb + kQPair, p.Uimg + (size_t)(chunk * KS + ks) * kQPair, bbytes, full + st);
+                    ptx::bulk_g2s(sb + kQPair, p.Uimg + (size_t)(chunk * KS + ks) * 2 * CF::BTILE, bbytes, full + st);
                 }
                 __syncwarp();
                 if (++st == kQStages) { st = 0; ph ^= 1; }
@@ -168,31 +178,33 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
                 hph ^= 1;
                 fence_proxy_async_global_q();
                 const uint8_t* hslot = img + (size_t)((t - 1) & 1) * img_bytes;
-                for (int c = 0; c < NC1; ++c) load(hslot, c);
+                const int U1 = PAIR ? NC1 / 2 : NC1, U2 = PAIR ? NC2 / 2 : NC2;
+                for (int c = 0; c < U1; ++c) load(hslot, c);
                 ptx::mbar_wait(rh_ready, rph);
                 rph ^= 1;
                 fence_proxy_async_global_q();
-                for (int c = 0; c < NC2; ++c) load(rh_img, NC1 + c);
+                for (int c = 0; c < U2; ++c) load(rh_img, U1 + c);
             }
         }
     } else if (warp == kQMmaWarp) {
-        constexpr uint32_t idesc = ptx::idesc_f16(128, 128);
+        constexpr uint32_t idesc = ptx::idesc_f16(128, CF::ACC);
         const uint64_t dbase = ptx::desc_sw128_kmajor(ptx::smem_u32(stages));
         const bool two = p.two_pass != 0;
         uint32_t st = 0, ph = 0, ach = 0, aph = 0;
+        const int NU = PAIR ? (NC1 + NC2) / 2 : NC1 + NC2;
         for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             for (int t = 2; t <= p.Q; ++t) {
-                for (int n = 0; n < NC1 + NC2; ++n) {
+                for (int n = 0; n < NU; ++n) {
                     ptx::mbar_wait(acc_empty + ach, aph ^ 1);
                     ptx::tc_fence_after();
-                    const uint32_t d = tmem + ach * 128;
+                    const uint32_t d = tmem + ach * CF::ACC;
                     for (int ks = 0; ks < KS; ++ks) {
                         ptx::mbar_wait(full + st, ph);
                         ptx::tc_fence_after();
                         const uint64_t ah = dbase + (uint64_t)((st * kQStageBytes) >> 4);
                         const uint64_t al = ah + (uint64_t)(kQTile >> 4);
                         const uint64_t bh = ah + (uint64_t)(kQPair >> 4);
-                        const uint64_t bl = bh + (uint64_t)(kQTile >> 4);
+                        const uint64_t bl = bh + (uint64_t)(CF::BTILE >> 4);
                         if (ptx::elect_one()) {
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk) {
@@ -243,15 +255,21 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
                 for (int c = 0; c < NC1; ++c) {
                     float a[2][16];   // 16 neurons x (z, r) interleaved
                     if (t >= 2) {
-                        ptx::mbar_wait(acc_full + ach, aph);
-                        ptx::tc_fence_after();
-                        tmem_ld16q(lane_base + ach * 128 + 32 * u, a[0]);
-                        tmem_ld16q(lane_base + ach * 128 + 32 * u + 16, a[1]);
+                        const bool first = !PAIR || (c & 1) == 0, last = !PAIR || (c & 1) == 1;
+                        if (first) {
+                            ptx::mbar_wait(acc_full + ach, aph);
+                            ptx::tc_fence_after();
+                        }
+                        const uint32_t acol = ach * CF::ACC + (PAIR ? (c & 1) * 128 : 0);
+                        tmem_ld16q(lane_base + acol + 32 * u, a[0]);
+                        tmem_ld16q(lane_base + acol + 32 * u + 16, a[1]);
                         ptx::tmem_wait_ld();
-                        ptx::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(acc_empty + ach);
-                        if (++ach == 2) { ach = 0; aph ^= 1; }
+                        if (last) {
+                            ptx::tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) ptx::mbar_arrive(acc_empty + ach);
+                            if (++ach == 2) { ach = 0; aph ^= 1; }
+                        }
                     } else {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) a[0][i] = a[1][i] = 0.0f;
@@ -292,15 +310,21 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
                 for (int c = 0; c < NC2; ++c) {
                     float a2[2][16];
                     if (t >= 2) {
-                        ptx::mbar_wait(acc_full + ach, aph);
-                        ptx::tc_fence_after();
-                        tmem_ld16q(lane_base + ach * 128 + 32 * u, a2[0]);
-                        tmem_ld16q(lane_base + ach * 128 + 32 * u + 16, a2[1]);
+                        const bool first = !PAIR || (c & 1) == 0, last = !PAIR || (c & 1) == 1;
+                        if (first) {
+                            ptx::mbar_wait(acc_full + ach, aph);
+                            ptx::tc_fence_after();
+                        }
+                        const uint32_t acol = ach * CF::ACC + (PAIR ? (c & 1) * 128 : 0);
+                        tmem_ld16q(lane_base + acol + 32 * u, a2[0]);
+                        tmem_ld16q(lane_base + acol + 32 * u + 16, a2[1]);
                         ptx::tmem_wait_ld();
-                        ptx::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(acc_empty + ach);
-                        if (++ach == 2) { ach = 0; aph ^= 1; }
+                        if (last) {
+                            ptx::tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) ptx::mbar_arrive(acc_empty + ach);
+                            if (++ach == 2) { ach = 0; aph ^= 1; }
+                        }
                     } else {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) a2[0][i] = a2[1][i] = 0.0f;
@@ -360,13 +384,15 @@ __global__ void __launch_bounds__(kQThreads, 1) k_gru_wide(const __grid_constant
     __syncthreads();
     if (warp == kQProdWarp) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem, 256);
+        ptx::tmem_dealloc(tmem, CF::TMEM_COLS);
     }
 }
 
 // U images: phase-1 chunk q < NC1 rows nrow = 2 jj + g (neuron 64 q + jj, gate z|r),
 // phase-2 chunk q2 rows = neuron 128 q2 + nrow (gate f); K-major SW128, hi | lo, x 2^sigma.
-__global__ void k_pack_u_gru_wide(const float* __restrict__ U, int M, float scale, uint8_t* __restrict__ img) {
+// pair = 1: chunks 2m, 2m+1 adjacent (one 256-row tile per K-slice and part), as k_pack_u
+__global__ void k_pack_u_gru_wide(const float* __restrict__ U, int M, float scale, uint8_t* __restrict__ img,
+                                  int pair) {
     const int KS = M / 64, NC1 = M / 64, NC = NC1 + M / 128;
     const int64_t total = (int64_t)NC * KS * 128 * 64;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -378,18 +404,22 @@ __global__ void k_pack_u_gru_wide(const float* __restrict__ U, int M, float scal
         const float v = U[(size_t)(64 * ks + kk) * (3 * M) + col] * scale;
         const __half hi = __float2half_rn(v);
         const __half lo = __float2half_rn(v - __half2float(hi));
-        uint8_t* base = img + (size_t)((q * KS + ks) * 2) * kQTile;
+        uint8_t* base = pair ? img + (size_t)(((q >> 1) * KS + ks) * 2) * 2 * kQTile + (size_t)(q & 1) * kQTile
+                             : img + (size_t)((q * KS + ks) * 2) * kQTile;
         const uint32_t off = ptx::sw128_offset(nrow, kk);
         *reinterpret_cast<__half*>(base + off) = hi;
-        *reinterpret_cast<__half*>(base + kQTile + off) = lo;
+        *reinterpret_cast<__half*>(base + (pair ? 2 : 1) * kQTile + off) = lo;
     }
 }
 
 int gw_padded_s(int S) { return S <= 1 ? 1 : (S <= 2 ? 2 : 4); }
 size_t gw_img_bytes(int M) { return (size_t)(M / 64 + M / 128) * (M / 64) * kQPair; }
 
-template <int SS>
+bool gw_pair(const elmrnn* h) { return h->tune.wide_pair != 0 && h->M % 256 == 0; }
+
+template <int SS, bool PAIR>
 cudaError_t launch_gw(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh) {
+    constexpr int kQSmem = QCfg<PAIR>::SMEM;
     GruWideParams p{};
     p.X = X; p.ldx = ldx; p.N = N; p.H = H; p.ldh = ldh;
     p.M = h->M; p.S = h->S; p.Q = h->Q; p.NC1 = h->M / 64; p.NC2 = h->M / 128; p.KS = h->M / 64;
@@ -418,8 +448,8 @@ cudaError_t launch_gw(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* 
     p.img = base;
     p.hst = reinterpret_cast<float*>(base + img);
     p.zst = reinterpret_cast<float*>(base + img + st);
-    if ((e = cudaFuncSetAttribute(k_gru_wide<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-    k_gru_wide<SS><<<grid, kQThreads, smem, h->stream>>>(p);
+    if ((e = cudaFuncSetAttribute(k_gru_wide<SS, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+    k_gru_wide<SS, PAIR><<<grid, kQThreads, smem, h->stream>>>(p);
     h->launches++;
     return cudaGetLastError();
 }
@@ -457,16 +487,16 @@ cudaError_t gru_wide_prepare(elmrnn* h) {
         return e;
     const int64_t total = (int64_t)(M / 64 + M / 128) * (M / 64) * 128 * 64;
     k_pack_u_gru_wide<<<(int)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, h->stream>>>(
-        h->rec, M, scale, static_cast<uint8_t*>(h->tc_ops));
+        h->rec, M, scale, static_cast<uint8_t*>(h->tc_ops), gw_pair(h) ? 1 : 0);
     h->launches++;
     return cudaGetLastError();
 }
 
 cudaError_t launch_gru_wide(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh) {
     switch (gw_padded_s(h->S)) {
-    case 1: return launch_gw<1>(h, X, ldx, N, H, ldh);
-    case 2: return launch_gw<2>(h, X, ldx, N, H, ldh);
-    default: return launch_gw<4>(h, X, ldx, N, H, ldh);
+    case 1: return gw_pair(h) ? launch_gw<1, true>(h, X, ldx, N, H, ldh) : launch_gw<1, false>(h, X, ldx, N, H, ldh);
+    case 2: return gw_pair(h) ? launch_gw<2, true>(h, X, ldx, N, H, ldh) : launch_gw<2, false>(h, X, ldx, N, H, ldh);
+    default: return gw_pair(h) ? launch_gw<4, true>(h, X, ldx, N, H, ldh) : launch_gw<4, false>(h, X, ldx, N, H, ldh);
     }
 }
 

@@ -182,6 +182,22 @@ def test_H_written_once_and_ld_respected():
     assert np.abs(H[:, :M].cpu().numpy() - ref).max() <= H_TOL
 
 
+@pytest.mark.parametrize("arch,M,Q", [("lstm", 512, 4), ("gru", 512, 4), ("lstm", 1024, 2), ("gru", 256, 3)])
+def test_wide_pair_units_match_single(arch, M, Q, monkeypatch):
+    """Wide builders: MMA units of two chunks (N = 256, default) against single-chunk
+    units (N = 128, ELMRNN_WIDE_PAIR=0 through the testing knob read at init): the
+    same per-element K order, so H agrees to rounding (asserted 1e-6) on a ragged N."""
+    N = 2 * 128 + 77
+    X, _, _ = inputs(N, Q, 1, seed=M)
+    Xd = torch.from_numpy(X).cuda()
+    H1 = E(arch, 1, M, Q, 7).build_H(Xd)
+    monkeypatch.setenv("ELMRNN_TESTING", "1")
+    monkeypatch.setenv("ELMRNN_WIDE_PAIR", "0")
+    H0 = E(arch, 1, M, Q, 7).build_H(Xd)
+    torch.cuda.synchronize()
+    assert float((H1 - H0).abs().max()) <= 1e-6
+
+
 @pytest.mark.parametrize("arch,M,Q,S", [("lstm", 256, 12, 1), ("lstm", 128, 10, 2), ("gru", 128, 10, 4),
                                         ("lstm", 512, 4, 1), ("gru", 256, 4, 1), ("fc", 128, 6, 1)])
 def test_x_staging_layouts_bitwise(arch, M, Q, S):
@@ -283,6 +299,7 @@ WELL_COND = [
     ("gru", 128, 10, 4, 0, 2, "k_gru_tc M=128"),
     ("gru", 256, 6, 4, 0, 2, "k_gru_wide M=256"),
     ("gru", 512, 3, 4, 0, 2, "k_gru_wide M=512"),
+    ("gru", 384, 3, 4, 0, 2, "k_gru_wide M=384 (odd phase-2 chunk count: N = 128 units)"),
     ("fc", 128, 10, 4, 0, 2, "k_fc_tc M=128"),
     ("lstm", 64, 10, 4, 0, 1, "k_dense_fma LSTM"),
     ("gru", 32, 10, 4, 0, 1, "k_dense_fma GRU"),
