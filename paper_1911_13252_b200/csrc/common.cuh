@@ -32,7 +32,7 @@ struct SolveDev {
 struct Tune {
     int tsqr_wy = -1;   // ELMRNN_TSQR_WY: 1 force the blocked-WY TSQR, 0 force the per-column fold
     int wy_rows = 0;    // ELMRNN_TSQR_WY_ROWS: WY leaf tile rows (8..96)
-    int pw_mode = 1;    // ELMRNN_PW_MODE: WY leaf panel warp 0 rotate SMSPs per CTA, 1 pin to SMSP 0
+    int pw_mode = -1;   // ELMRNN_PW_MODE: WY leaf panel warp 0 rotate SMSPs per CTA, 1 pin to SMSP 0 (-1: by tile)
     int wy_nw = 0;      // ELMRNN_WY_NW: WY leaf/merge warps per CTA (4 or 8; 0 = by n)
     int max_slabs = 0;  // ELMRNN_TSQR_MAXSLABS: cap on the TSQR leaf count (0 = by size)
     int wy_2phase = 1;  // ELMRNN_WY_2PHASE: 0 = single-chain WY leaf only; 2 = two-phase also for n <= 320

@@ -1040,7 +1040,7 @@ __device__ __forceinline__ int wy_panel_warp(int* sm_slot, int mode) {
 // cap is 65536 / 384 = 168 (the 2-CTA bound of 128 spilled the panel warp's R
 // prefetch to local memory right behind its load: measured, profiles/r02).
 template <int ROWS, int NW>
-__global__ void __launch_bounds__(32 * NW, (NW == 4 && ROWS <= 32) ? 3 : 1)
+__global__ void __launch_bounds__(32 * NW, (NW == 4 && ROWS <= 32) ? 3 : ((NW <= 6 && (ROWS == 48 || ROWS == 40)) ? 2 : 1))
     k_tsqr_leaf_wy(const float* __restrict__ H, int64_t ldh, const float* __restrict__ Y, int64_t ldy, int P,
                    int64_t N, int M, double* __restrict__ Rws, int64_t rows_per_cta, int* __restrict__ flag,
                    int* sm_slot, int la_wait, int pw_mode) {
@@ -1104,7 +1104,12 @@ __global__ void __launch_bounds__(32 * NW, (NW == 4 && ROWS <= 32) ? 3 : 1)
             }
         }
         __syncthreads();
+#ifdef ELM_WY48_NO_ILP
         wy_fold<ROWS, ROWS == 32>(C, LDC, n, 0, R, Gs, Rd, cgv, cuv, pw, nullptr, nullptr, la_wait != 0);
+#else
+        wy_fold<ROWS, ROWS == 32 || ROWS == 48 || ROWS == 40>(C, LDC, n, 0, R, Gs, Rd, cgv, cuv, pw, nullptr, nullptr,
+                                                               la_wait != 0);
+#endif
     }
     if (bad) atomicOr(flag, 1);
 }
@@ -1317,15 +1322,18 @@ static bool use_wy_h(const elmrnn* h) { return h->nrhs > 1 || use_wy(h, h->M + h
 static bool wide_solve(const elmrnn* h) { return h->nrhs > 1 || h->M + h->nrhs > kWideN; }
 static int wy_rows(const elmrnn* h, int n) {
     if (const int r = h->tune.wy_rows) {   // testing knob (elmrnn_init_ex)
-        if ((r == 96 || r == 64 || r == 32 || r == 24 || r == 16 || r == 8) && wy_smem_bytes(r, n) <= 220 * 1024)
+        if ((r == 96 || r == 64 || r == 48 || r == 40 || r == 32 || r == 24 || r == 16 || r == 8) &&
+            wy_smem_bytes(r, n) <= 220 * 1024)
             return r;
     }
-    // 32-row tiles, 2-3 CTAs per SM (their panels overlap each other's trailing updates)
     // n <= 160: 64-row tiles (measured M = 128 x 2M rows: 12.9 vs 14.3 ms with 32);
-    // larger n: 32-row tiles, 2-3 CTAs per SM (their panels overlap each other's
-    // trailing updates; 16/24-row tiles and 4-warp CTAs measured slower at
-    // n = 257, 513, 1025: tools/wy_variants.sh)
+    // 160 < n <= ~288: 48-row tiles, two 6-warp CTAs per SM (1 panel + 5 trailing
+    // warps each, panel warps on different SM sub-partitions): C4 shape 75.5 -> 67.3 ms,
+    // 500k x 257 13.9 -> 12.2, 2M x 193 25.2 -> 24.0 (tools/qr_ab5.sh; 40-row tiles
+    // and 5-warp CTAs slower); larger n: 32-row tiles, 3 CTAs per SM (16/24-row tiles
+    // and 4-warp CTAs measured slower at n = 257, 513, 1025: tools/wy_variants.sh)
     if (n <= 160) return 64;
+    if (2 * wy_smem_bytes(48, n) <= 227 * 1024) return 48;
     return wy_smem_bytes(32, n) <= 220 * 1024 ? 32 : 16;
 }
 // Leaf dynamic shared memory: the tile + coefficients.
@@ -1333,7 +1341,9 @@ static size_t wy_leaf_smem(int rows, int n) { return std::min(wy_smem_bytes(rows
 static int wy_nw(int n) { return n <= 320 ? 4 : 8; }
 static int wy_threads(int n) { return 32 * wy_nw(n); }
 // leaf warps per CTA: by n, or the testing override
-static int wy_leaf_nw(const elmrnn* h, int n) { return (h->tune.wy_nw == 4 || h->tune.wy_nw == 8) ? h->tune.wy_nw : wy_nw(n); }
+static int wy_leaf_nw(const elmrnn* h, int n) {
+    return (h->tune.wy_nw >= 4 && h->tune.wy_nw <= 8) ? h->tune.wy_nw : wy_nw(n);
+}
 template <int RW, class F>
 static auto wy_nw_dispatch(int nw, F& f) {
     if (nw == 4) return f(std::integral_constant<int, RW>{}, std::integral_constant<int, 4>{});
@@ -1345,6 +1355,12 @@ static auto wy_dispatch(const elmrnn* h, int n, F&& f) {
     switch (wy_rows(h, n)) {
     case 96: return wy_nw_dispatch<96>(nw, f);
     case 64: return wy_nw_dispatch<64>(nw, f);
+    case 48:   // 2 CTAs x 5-6 warps
+        if (nw == 5) return f(std::integral_constant<int, 48>{}, std::integral_constant<int, 5>{});
+        return f(std::integral_constant<int, 48>{}, std::integral_constant<int, 6>{});
+    case 40:
+        if (nw == 5) return f(std::integral_constant<int, 40>{}, std::integral_constant<int, 5>{});
+        return f(std::integral_constant<int, 40>{}, std::integral_constant<int, 6>{});
     case 32: return wy_nw_dispatch<32>(nw, f);
     case 24: return wy_nw_dispatch<24>(nw, f);
     case 8: return wy_nw_dispatch<8>(nw, f);
@@ -1572,7 +1588,8 @@ cudaError_t tsqr_factor(elmrnn* h, const float* H, int64_t ldh, const float* Y, 
             }
 #endif
             k_tsqr_leaf_wy<RW, NW><<<(unsigned)slabs, 32 * NW, sm, h->stream>>>(
-                H, ldh, Y, ldy, h->nrhs, N, h->M, h->Rws, rows, h->flag, slot, wy_la_wait(n), h->tune.pw_mode);
+                H, ldh, Y, ldy, h->nrhs, N, h->M, h->Rws, rows, h->flag, slot, wy_la_wait(n),
+                h->tune.pw_mode >= 0 ? h->tune.pw_mode : (RW == 48 ? 0 : 1));
             h->launches++;
 #ifdef ELM_QR_TRACE
             if (tb) {
