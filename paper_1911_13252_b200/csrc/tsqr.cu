@@ -1107,8 +1107,8 @@ __global__ void __launch_bounds__(32 * NW, (NW == 4 && ROWS <= 32) ? 3 : ((NW <=
 #ifdef ELM_WY48_NO_ILP
         wy_fold<ROWS, ROWS == 32>(C, LDC, n, 0, R, Gs, Rd, cgv, cuv, pw, nullptr, nullptr, la_wait != 0);
 #else
-        wy_fold<ROWS, ROWS == 32 || ROWS == 48 || ROWS == 40>(C, LDC, n, 0, R, Gs, Rd, cgv, cuv, pw, nullptr, nullptr,
-                                                               la_wait != 0);
+        wy_fold<ROWS, ROWS == 32 || ROWS == 48 || ROWS == 40 || ROWS == 24>(C, LDC, n, 0, R, Gs, Rd, cgv, cuv, pw,
+                                                                             nullptr, nullptr, la_wait != 0);
 #endif
     }
     if (bad) atomicOr(flag, 1);
@@ -1320,6 +1320,8 @@ static int wy_la_wait(int n) { return n <= 320 ? 1 : 0; }
 // multi-output [H | Y_1..Y_P] (P > 1) always takes the WY leaf/merge and the wide solve
 static bool use_wy_h(const elmrnn* h) { return h->nrhs > 1 || use_wy(h, h->M + h->nrhs); }
 static bool wide_solve(const elmrnn* h) { return h->nrhs > 1 || h->M + h->nrhs > kWideN; }
+// 448 < n with a 24-row tile within shared memory: the single-chain 12-warp leaf
+static bool wide_single(int n) { return n > 448 && wy_smem_bytes(24, n) <= 220 * 1024; }
 static int wy_rows(const elmrnn* h, int n) {
     if (const int r = h->tune.wy_rows) {   // testing knob (elmrnn_init_ex)
         if ((r == 96 || r == 64 || r == 48 || r == 40 || r == 32 || r == 24 || r == 16 || r == 8) &&
@@ -1334,6 +1336,10 @@ static int wy_rows(const elmrnn* h, int n) {
     // and 4-warp CTAs measured slower at n = 257, 513, 1025: tools/wy_variants.sh)
     if (n <= 160) return 64;
     if (2 * wy_smem_bytes(48, n) <= 227 * 1024) return 48;
+    // wide n, single-chain 12-warp CTAs (one per SM) with the tallest tile that fits:
+    // 2M x 513 48 rows 135.6 vs two-phase 32-row 140.3 ms; 2M x 1025 24 rows 690 vs
+    // two-phase 16-row 849 ms (tools/qr_ab8.sh, qr_ab9.sh); n = 401 keeps the two-phase leaf
+    if (wide_single(n)) return wy_smem_bytes(48, n) <= 220 * 1024 ? 48 : 24;
     return wy_smem_bytes(32, n) <= 220 * 1024 ? 32 : 16;
 }
 // Leaf dynamic shared memory: the tile + coefficients.
@@ -1342,7 +1348,8 @@ static int wy_nw(int n) { return n <= 320 ? 4 : 8; }
 static int wy_threads(int n) { return 32 * wy_nw(n); }
 // leaf warps per CTA: by n, or the testing override
 static int wy_leaf_nw(const elmrnn* h, int n) {
-    return (h->tune.wy_nw >= 4 && h->tune.wy_nw <= 8) ? h->tune.wy_nw : wy_nw(n);
+    if (h->tune.wy_nw >= 4 && h->tune.wy_nw <= 16) return h->tune.wy_nw;
+    return (wide_single(n) && !h->tune.wy_rows) ? 12 : wy_nw(n);
 }
 template <int RW, class F>
 static auto wy_nw_dispatch(int nw, F& f) {
@@ -1353,16 +1360,25 @@ template <class F>
 static auto wy_dispatch(const elmrnn* h, int n, F&& f) {
     const int nw = wy_leaf_nw(h, n);
     switch (wy_rows(h, n)) {
-    case 96: return wy_nw_dispatch<96>(nw, f);
-    case 64: return wy_nw_dispatch<64>(nw, f);
-    case 48:   // 2 CTAs x 5-6 warps
+    case 96:
+        if (nw == 12) return f(std::integral_constant<int, 96>{}, std::integral_constant<int, 12>{});
+        return wy_nw_dispatch<96>(nw, f);
+    case 64:
+        if (nw == 12) return f(std::integral_constant<int, 64>{}, std::integral_constant<int, 12>{});
+        return wy_nw_dispatch<64>(nw, f);
+    case 48:   // 2 CTAs x 5-6 warps (n <= ~280), or one 12-warp CTA
         if (nw == 5) return f(std::integral_constant<int, 48>{}, std::integral_constant<int, 5>{});
+        if (nw == 12) return f(std::integral_constant<int, 48>{}, std::integral_constant<int, 12>{});
+        if (nw == 16) return f(std::integral_constant<int, 48>{}, std::integral_constant<int, 16>{});
         return f(std::integral_constant<int, 48>{}, std::integral_constant<int, 6>{});
     case 40:
         if (nw == 5) return f(std::integral_constant<int, 40>{}, std::integral_constant<int, 5>{});
         return f(std::integral_constant<int, 40>{}, std::integral_constant<int, 6>{});
     case 32: return wy_nw_dispatch<32>(nw, f);
-    case 24: return wy_nw_dispatch<24>(nw, f);
+    case 24:
+        if (nw == 12) return f(std::integral_constant<int, 24>{}, std::integral_constant<int, 12>{});
+        if (nw == 16) return f(std::integral_constant<int, 24>{}, std::integral_constant<int, 16>{});
+        return wy_nw_dispatch<24>(nw, f);
     case 8: return wy_nw_dispatch<8>(nw, f);
     default: return wy_nw_dispatch<16>(nw, f);
     }
@@ -1386,6 +1402,7 @@ static Wy2Cfg wy2_cfg(const elmrnn* h, int n) {
     // 135.5 vs 155.1, n = 1025: 789 vs 803 (tools/wy_variants.sh)
     if (h->tune.wy_2phase == 0 || n <= 160 || h->tune.wy_rows) return {0, 0, 0};
     if (n <= 320) return h->tune.wy_2phase == 2 ? Wy2Cfg{32, 4, 2} : Wy2Cfg{0, 0, 0};
+    if (wide_single(n) && h->tune.wy_2phase != 3) return {0, 0, 0};   // 3: force two-phase (testing)
     if (wy2_smem_bytes(32, n) <= 220 * 1024) return {32, 8, 4};
     if (wy2_smem_bytes(16, n) <= 220 * 1024) return {16, 8, 4};
     return {0, 0, 0};

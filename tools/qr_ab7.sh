@@ -1,0 +1,5 @@
+#!/bin/bash
+mkdir -p gpurun_out
+python -m paper_1911_13252_b200.build > /dev/null
+python tools/qr_time.py 256 4000000 '{}' '{"ELMRNN_TSQR_WY_ROWS": "48", "ELMRNN_WY_NW": "12"}' '{"ELMRNN_TSQR_WY_ROWS": "64", "ELMRNN_WY_NW": "12"}' '{"ELMRNN_TSQR_WY_ROWS": "64", "ELMRNN_WY_NW": "8"}' '{"ELMRNN_TSQR_WY_ROWS": "96", "ELMRNN_WY_NW": "12"}' 2>&1 | tee gpurun_out/qr_ab7.jsonl
+python tools/qr_time.py 512 2000000 '{}' '{"ELMRNN_WY_2PHASE": "0", "ELMRNN_TSQR_WY_ROWS": "48", "ELMRNN_WY_NW": "12"}' '{"ELMRNN_WY_2PHASE": "0", "ELMRNN_TSQR_WY_ROWS": "32", "ELMRNN_WY_NW": "8"}' '{"ELMRNN_WY_2PHASE": "0", "ELMRNN_TSQR_WY_ROWS": "48", "ELMRNN_WY_NW": "8"}' 2>&1 | tee -a gpurun_out/qr_ab7.jsonl
