@@ -1225,10 +1225,12 @@ __global__ void __launch_bounds__(32 * (NWA + NWB), (NWA + NWB) * 32 * 168 * 2 <
 }
 
 template <int ROWS, int NW>
-__global__ void __launch_bounds__(32 * NW, (NW == 4 && ROWS <= 32) ? 3 : 1) k_tsqr_merge_wy(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n) {
+__global__ void __launch_bounds__(32 * NW, (NW == 4 && ROWS <= 32) ? 3 : 1)
+    k_tsqr_merge_wy(double* __restrict__ Rws, int64_t slabs, int64_t stride, int n, const int* gate = nullptr) {
     extern __shared__ __align__(16) double wsm[];
     const int64_t c = (int64_t)blockIdx.x * 2 * stride, partner = c + stride;
     if (partner >= slabs) return;
+    if (gate && *gate == 0) return;   // wide solve: no ridge rows to fold (rank_flag == 0)
     const int LDC = wy_ldc(n), tid = threadIdx.x, nt = blockDim.x;
     double* C = wsm;
     double* Gs = C + (size_t)ROWS * LDC;     // [2][16][16]
@@ -1387,6 +1389,10 @@ static auto wy_dispatch(const elmrnn* h, int n, F&& f) {
 template <class F>
 static auto wy_dispatch_merge(int n, F&& f) {
     const int nw = wy_nw(n);
+    // n > ~568 (no 32-row tile fits): 24-row 12-warp CTAs like the wide leaf (2M x 1025
+    // 667.5 -> 660.6 ms; at n = 513 the 32-row 8-warp merges stay: 135.5 vs 137.6 ms)
+    if (wide_single(n) && wy_smem_bytes(32, n) > 220 * 1024)
+        return f(std::integral_constant<int, 24>{}, std::integral_constant<int, 12>{});
     if (wy_smem_bytes(96, n) <= 220 * 1024) return wy_nw_dispatch<96>(nw, f);
     if (wy_smem_bytes(64, n) <= 220 * 1024) return wy_nw_dispatch<64>(nw, f);
     if (wy_smem_bytes(32, n) <= 220 * 1024) return wy_nw_dispatch<32>(nw, f);
@@ -1726,7 +1732,8 @@ cudaError_t tsqr_solve(elmrnn* h, int64_t n_total, double* beta) {
             constexpr int RW = decltype(rows)::value, NW = decltype(nwc)::value;
             const size_t sm = wy_smem_bytes(RW, n);
             cudaFuncSetAttribute(k_tsqr_merge_wy<RW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k_tsqr_merge_wy<RW, NW><<<1, wy_threads(n), sm, h->stream>>>(h->Rws, 2, 1, n);
+            // the ridge rows are folded only when k_solve_wide_prep found R rank deficient
+            k_tsqr_merge_wy<RW, NW><<<1, wy_threads(n), sm, h->stream>>>(h->Rws, 2, 1, n, &h->sdev->rank_flag);
             h->launches++;
             return cudaGetLastError();
         });
