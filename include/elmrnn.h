@@ -249,9 +249,10 @@ ELMRNN_API int64_t elmrnn_packed_r_len(elmrnn_t h);
 /* Eq. 4: Yhat[i] = sum_j beta_j H(Q)[i][j] (no output bias, R16),
  * fused into the H builders: the same kernels as
  * elmrnn_build_H run with a readout epilogue that writes no H(Q), only the fp64
- * partial products of each thread's H(Q) row segment with beta (<= max(4,
- * ceil(M/32)+1) doubles per row, a library workspace); a finish kernel sums each
- * row's partials in a fixed order (bitwise repeatable) and rounds once to fp32.
+ * partial products of each thread's H(Q) row segment with beta (a library
+ * workspace of ceil(M/32)+1 doubles per row for the flattened-cell archs, 4 for
+ * the others); a finish kernel sums each row's partials in a fixed order
+ * (bitwise repeatable) and rounds once to fp32.
  * X, Yfb as in elmrnn_build_H; beta dev fp64 [M]; Yhat dev fp32 [N].
  * Errors: ARG, SHAPE, OOM, CUDA. */
 ELMRNN_API elmrnn_status elmrnn_predict(elmrnn_t h, const float* X, int64_t ldx, const float* Yfb,

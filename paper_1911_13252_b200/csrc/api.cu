@@ -295,7 +295,7 @@ static elmrnn_status readout_impl(elmrnn* h, const float* X, int64_t ldx, const 
                                   const double* beta, float* yout, int64_t ldyo, float* w = nullptr,
                                   int64_t ldw = 0) {
     cudaError_t e;
-    const int64_t need = (int64_t)elm::ro_max_slots(h->M) * N;
+    const int64_t need = (int64_t)elm::ro_max_slots(h->arch, h->M) * N;
     if (need > h->ypws_len) {
         if (h->ypws) cudaFree(h->ypws);
         h->ypws = nullptr;

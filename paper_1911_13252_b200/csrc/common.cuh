@@ -151,7 +151,12 @@ int64_t tsqr_leaf_slabs(const elmrnn* h, int64_t N);
 
 // ---- fused readout (readout.cu) ---------------------------------------------------
 constexpr int kRoCellSlots = -1;   // slot = 32-cell group index - first group of the row
-inline int ro_max_slots(int M) { return 4 > (M + 31) / 32 + 1 ? 4 : (M + 31) / 32 + 1; }
+// slots per row: the flattened-cell builders (Elman / FC by Eq. 8 / diagonal LSTM-GRU)
+// one per 32-cell warp group the row spans; the tile builders at most 4
+inline int ro_max_slots(int arch, int M) {
+    const bool cell = arch == kArchElman || arch == kArchFCEq8 || arch == kArchLSTMDiag || arch == kArchGRUDiag;
+    return cell ? (M + 31) / 32 + 1 : 4;
+}
 // yhat_i = fp32(sum of row i's slots, in slot order); with w != null also
 // w_i <- (w_i[1:], yhat_i) (the free-running forecast step, reading R31)
 cudaError_t launch_readout_finish(elmrnn* h, const double* yp, int64_t N, int slots, float* yout, int64_t ldyo,
