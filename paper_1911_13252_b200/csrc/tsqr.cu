@@ -41,7 +41,7 @@ struct Fold {
     static constexpr int ROWS = TR * P;
     // register budget (16K registers per SM sub-partition): 2*TR registers of
     // tile per thread plus ~40; 576 threads -> 96 registers, 1024 -> 64
-    static constexpr int MAX_THREADS = (P == 2 && (TR == 24 || TR == 16)) ? 576 : 1024;
+    static constexpr int MAX_THREADS = (P == 2 && (TR == 24 || TR == 16)) ? 576 : (TR >= 32 ? 256 : 1024);
 };
 
 // Fast fp64 reciprocal / square root: hardware approximation + Newton steps
@@ -1557,6 +1557,16 @@ static cudaError_t tree(elmrnn* h, int64_t slabs) {
             }
             return cudaSuccess;
         });
+    }
+    // 48 < n <= 72 (C2: n = 65): one 72-row chunk per merge (36 rows per thread) instead
+    // of 48 + 17 rows, i.e. n column steps per tree level instead of n + (n - 48)
+    if (n > 48 && n <= 72 && h->tune.merge_small != 0) {
+        for (int64_t stride = 1; stride < slabs && stride < max_stride; stride *= 2) {
+            int64_t pairs = (slabs + 2 * stride - 1) / (2 * stride);
+            k_tsqr_merge<36, 2><<<(unsigned)pairs, threads, 0, h->stream>>>(h->Rws, slabs, stride, n);
+            h->launches++;
+        }
+        return cudaGetLastError();
     }
     return dispatch(v, [&](auto tr, auto p) {
         for (int64_t stride = 1; stride < slabs && stride < max_stride; stride *= 2) {
