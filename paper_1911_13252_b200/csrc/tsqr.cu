@@ -1333,14 +1333,14 @@ static int wy_rows(const elmrnn* h, int n) {
     // n <= 160: 64-row tiles (measured M = 128 x 2M rows: 12.9 vs 14.3 ms with 32);
     // 160 < n <= ~288: 48-row tiles, two 6-warp CTAs per SM (1 panel + 5 trailing
     // warps each, panel warps on different SM sub-partitions): C4 shape 75.5 -> 67.3 ms,
-    // 500k x 257 13.9 -> 12.2, 2M x 193 25.2 -> 24.0 (tools/qr_ab5.sh; 40-row tiles
+    // 500k x 257 13.9 -> 12.2, 2M x 193 25.2 -> 24.0 (tools/qr_time.py knobs; 40-row tiles
     // and 5-warp CTAs slower); larger n: 32-row tiles, 3 CTAs per SM (16/24-row tiles
     // and 4-warp CTAs measured slower at n = 257, 513, 1025: tools/wy_variants.sh)
     if (n <= 160) return 64;
     if (2 * wy_smem_bytes(48, n) <= 227 * 1024) return 48;
     // wide n, single-chain 12-warp CTAs (one per SM) with the tallest tile that fits:
     // 2M x 513 48 rows 135.6 vs two-phase 32-row 140.3 ms; 2M x 1025 24 rows 690 vs
-    // two-phase 16-row 849 ms (tools/qr_ab8.sh, qr_ab9.sh); n = 401 keeps the two-phase leaf
+    // two-phase 16-row 849 ms (tools/qr_time.py with the ELMRNN_TSQR_WY_ROWS / ELMRNN_WY_NW knobs); n = 401 keeps the two-phase leaf
     if (wide_single(n)) return wy_smem_bytes(48, n) <= 220 * 1024 ? 48 : 24;
     return wy_smem_bytes(32, n) <= 220 * 1024 ? 32 : 16;
 }
