@@ -35,13 +35,24 @@ constexpr int kGStageBytes = 2 * kGSliceBytes;
 constexpr int kGEpiWarps = 16;
 constexpr int kGProdWarp = kGEpiWarps, kGMmaWarp = kGEpiWarps + 1;
 constexpr int kGThreads = (kGEpiWarps + 2) * 32;
-constexpr int kGKS = kGM / 64;                  // K slices
+constexpr int kGKS = kGM / 64;                  // K slices of h(t-1) / r o h(t-1)
 constexpr int kGChunks = 3;                     // phase-1 chunks 0, 1; phase-2 chunk 2
-constexpr int kGStagesPerStep = kGChunks * kGKS;
+#ifndef ELM_GRU_XMMA
+#define ELM_GRU_XMMA 1
+#endif
+// XMMA: x(t) W + b joins the MMA as one more K-slice per chunk, A = [x(t), 1, 0..]
+// (fp16 hi|lo, an SW128 image in shared memory written by the epilogue), B = [W; b]
+// (rows of the chunk's gates, K = 0..S-1: W, K = S: b); only its first 16 K are used
+// (one k-step).  The epilogue then needs no W|b loads and no x W FMAs: C3 GRU (S = 4)
+// build 19.9 -> 10.5 ms, S = 1 7.38 -> 7.11 ms (tools/gru_ab.sh, same box).
+constexpr int kGX = ELM_GRU_XMMA ? 1 : 0;
+constexpr int kGSlices = kGKS + kGX;            // streamed B slices per chunk
+constexpr int kGStagesPerStep = kGChunks * kGSlices;
 constexpr int kGWbMax = 7168;
 constexpr uint32_t kAcc = 0, kAH = 256, kARH = 384;   // TMEM column bases (hi at +0, lo at +64)
 constexpr int kZBytes = kGEpiWarps * 32 * 32 * 4;     // z of 32 neurons per thread
-constexpr int kGSmem = 1024 + kGStages * kGStageBytes + kZBytes + 256;   // + the X block
+constexpr int kGXImg = kGX * 2 * kGSliceBytes;        // A = [x, 1] hi | lo SW128 images
+constexpr int kGSmem = 1024 + kGStages * kGStageBytes + kZBytes + kGXImg + 256;   // + the X block
 
 struct GruParams {
     const float* X;
@@ -94,7 +105,8 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stages = smem;
     float* zs = reinterpret_cast<float*>(stages + kGStages * kGStageBytes);   // [warp][item 32][lane]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(zs) + kZBytes);
+    uint8_t* ximg = reinterpret_cast<uint8_t*>(zs) + kZBytes;                 // XMMA A operand (1 KB aligned)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ximg + kGXImg);
     uint64_t* full = bars;
     uint64_t* empty = bars + kGStages;
     uint64_t* acc_full = bars + 2 * kGStages;
@@ -103,7 +115,8 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
     uint64_t* rh_ready = a_ready + kGKS; // [KS]: K-slice ks of r o h(t-1) is in TMEM
     uint64_t* x_full = rh_ready + kGKS;  // the tile's X block has landed
     uint64_t* x_empty = x_full + 1;      // every epilogue warp has read its last x(t)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 1);
+    uint64_t* xa_ready = x_empty + 1;    // XMMA: the A image holds [x(t), 1] of this step
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xa_ready + 1);
     float* xbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);   // the tile's X block
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -120,6 +133,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
         for (int i = 0; i < kGKS; ++i) ptx::mbar_init(rh_ready + i, kGEpiWarps);
         ptx::mbar_init(x_full, 1);
         ptx::mbar_init(x_empty, kGEpiWarps);
+        ptx::mbar_init(xa_ready, 4);     // the 4 warps of neuron group u = 0 (one per lane quadrant)
         ptx::fence_mbar_init();
     }
     if (warp == kGProdWarp) {
@@ -144,8 +158,9 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
             for (int c = 0; c < kGStagesPerStep; ++c) {
                 ptx::mbar_wait(empty + st, ph ^ 1);
                 if (ptx::elect_one()) {
-                    ptx::mbar_arrive_expect_tx(full + st, bytes);
-                    ptx::bulk_g2s(stages + st * kGStageBytes, p.Uimg + (size_t)c * kGStageBytes, bytes, full + st);
+                    const uint32_t cb = (kGX && c % kGSlices == kGKS) ? kGStageBytes : bytes;   // [W; b]: hi and lo
+                    ptx::mbar_arrive_expect_tx(full + st, cb);
+                    ptx::bulk_g2s(stages + st * kGStageBytes, p.Uimg + (size_t)c * kGStageBytes, cb, full + st);
                 }
                 __syncwarp();
                 if (++st == kGStages) { st = 0; ph ^= 1; }
@@ -162,13 +177,17 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + kAcc + ach * 128;
                 const uint32_t abase = tmem + (q < 2 ? kAH : kARH);
-                for (int ks = 0; ks < kGKS; ++ks) {
-                    if (q == 0) {   // h(t-1) K-slice ks is in TMEM
+                for (int ks = 0; ks < kGSlices; ++ks) {
+                    if (q == 0 && ks < kGKS) {   // h(t-1) K-slice ks is in TMEM
                         ptx::mbar_wait(a_ready + ks, (uint32_t)(s & 1));
                         ptx::tc_fence_after();
                     }
-                    if (q == 2) {   // K-slice ks of r o h(t-1) is in TMEM
+                    if (q == 2 && ks < kGKS) {   // K-slice ks of r o h(t-1) is in TMEM
                         ptx::mbar_wait(rh_ready + ks, (uint32_t)(s & 1));
+                        ptx::tc_fence_after();
+                    }
+                    if (kGX && q == 0 && ks == kGKS) {   // [x(t), 1] is in the A image
+                        ptx::mbar_wait(xa_ready, (uint32_t)(s & 1));
                         ptx::tc_fence_after();
                     }
                     ptx::mbar_wait(full + st, ph);
@@ -176,6 +195,20 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                     const uint64_t dbh = dbase + (uint64_t)((st * kGStageBytes) >> 4);
                     const uint64_t dbl = dbh + (uint64_t)(kGSliceBytes >> 4);
                     const uint32_t tah = abase + ks * 32, tal = abase + 64 + ks * 32;
+                    if (kGX && ks == kGKS) {   // x(t) W + b: one k-step, A from shared memory, 3 passes
+                        if (ptx::elect_one()) {
+                            const uint64_t axh = ptx::desc_sw128_kmajor(ptx::smem_u32(ximg));
+                            const uint64_t axl = axh + (uint64_t)(kGSliceBytes >> 4);
+                            ptx::mma_f16_ss(d, axh, dbh, idesc, 1u);
+                            ptx::mma_f16_ss(d, axl, dbh, idesc, 1u);
+                            ptx::mma_f16_ss(d, axh, dbl, idesc, 1u);
+                            ptx::mma_commit(empty + st);
+                            ptx::mma_commit(acc_full + ach);
+                        }
+                        __syncwarp();
+                        if (++st == kGStages) { st = 0; ph ^= 1; }
+                        continue;
+                    }
                     if (ptx::elect_one()) {
                         ptx::mma_f16_ts(d, tah, dbh, idesc, ks != 0);
                         if (!two) ptx::mma_f16_ts(d, tah, dbl, idesc, 1);
@@ -187,7 +220,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                             ptx::mma_f16_ts(d, tal + kk * 8, dbh + 2 * kk, idesc, 1);
                         }
                         ptx::mma_commit(empty + st);
-                        if (ks == kGKS - 1) ptx::mma_commit(acc_full + ach);
+                        if (ks == kGSlices - 1) ptx::mma_commit(acc_full + ach);
                     }
                     __syncwarp();
                     if (++st == kGStages) { st = 0; ph ^= 1; }
@@ -236,13 +269,45 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
 #pragma unroll
             for (int i = 0; i < 32; ++i) h[i] = 0.0f;
             double yacc = 0.0;   // fused readout partial
+            // XMMA: write [x(tn), 1, 0..] of this thread's row as fp16 hi|lo into the A image
+            // (neuron group u = 0 only) and release it to the MMA warp
+            auto put_x = [&](int tn) {
+                if (u == 0) {
+                    float xv[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) xv[k] = 0.0f;
+#pragma unroll
+                    for (int s = 0; s < SS; ++s)
+                        xv[s] = (valid && s < p.S)
+                                    ? (xst ? xrow[(tn - 1) * p.S + s] : __ldg(xrow + (int64_t)(tn - 1) * p.S + s))
+                                    : 0.0f;
+                    xv[p.S] = 1.0f;   // the bias column
+                    uint32_t hi[8], lo[8];
+                    split16(xv, hi, lo);
+                    uint8_t* xh = ximg;
+                    uint8_t* xl = ximg + kGSliceBytes;
+                    *reinterpret_cast<uint4*>(xh + ptx::sw128_offset((uint32_t)r, 0)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                    *reinterpret_cast<uint4*>(xh + ptx::sw128_offset((uint32_t)r, 8)) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+                    *reinterpret_cast<uint4*>(xl + ptx::sw128_offset((uint32_t)r, 0)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                    *reinterpret_cast<uint4*>(xl + ptx::sw128_offset((uint32_t)r, 8)) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(xa_ready);
+                }
+                if (xst && tn == p.Q) {   // last x(t) of this tile read: the block may be replaced
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(x_empty);
+                }
+            };
+            if (kGX) put_x(1);
             for (int t = 1; t <= p.Q; ++t) {
                 float xs[SS];
 #pragma unroll
                 for (int s = 0; s < SS; ++s)
-                    xs[s] = (valid && s < p.S) ? (xst ? xrow[(t - 1) * p.S + s] : __ldg(xrow + (int64_t)(t - 1) * p.S + s))
-                                               : 0.0f;
-                if (xst && t == p.Q) {   // last x(t) of this tile read: the block may be replaced
+                    xs[s] = (!kGX && valid && s < p.S)
+                                ? (xst ? xrow[(t - 1) * p.S + s] : __ldg(xrow + (int64_t)(t - 1) * p.S + s))
+                                : 0.0f;
+                if (!kGX && xst && t == p.Q) {   // last x(t) of this tile read: the block may be replaced
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(x_empty);
                 }
@@ -265,12 +330,15 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                         const int j = 64 * c + 16 * u + i;
                         const float* w = p.wb + j * (3 * (SS + 1));
                         // exp2 arguments k_g pre-activation; k_g folded into W|b on the host
-                        float pz = fmaf(kS, a[i >> 3][(i & 7) * 2], w[0]);
-                        float pr = fmaf(kS, a[i >> 3][(i & 7) * 2 + 1], w[SS + 1]);
+                        // (XMMA: x W + b is already in the accumulator)
+                        float pz = kGX ? kS * a[i >> 3][(i & 7) * 2] : fmaf(kS, a[i >> 3][(i & 7) * 2], w[0]);
+                        float pr = kGX ? kS * a[i >> 3][(i & 7) * 2 + 1] : fmaf(kS, a[i >> 3][(i & 7) * 2 + 1], w[SS + 1]);
+                        if (!kGX) {
 #pragma unroll
-                        for (int s = 0; s < SS; ++s) {
-                            pz = fmaf(xs[s], w[1 + s], pz);
-                            pr = fmaf(xs[s], w[SS + 2 + s], pr);
+                            for (int s = 0; s < SS; ++s) {
+                                pz = fmaf(xs[s], w[1 + s], pz);
+                                pr = fmaf(xs[s], w[SS + 2 + s], pr);
+                            }
                         }
                         my_z[(c * 16 + i) * 32] = sig_e2(pz);         // z (accurate form, DESIGN R26)
                         rh[i] = sig_e2(pr) * h[c * 16 + i];           // r o h(t-1)
@@ -296,6 +364,8 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(acc_empty + ach);
                 if (++ach == 2) { ach = 0; aph ^= 1; }
+                // this step's MMAs are complete (phase 2 was the last): the A image may take x(t+1)
+                if (kGX && t < p.Q) put_x(t + 1);
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {   // c = K-slice of the next step's A
 #pragma unroll
@@ -305,9 +375,11 @@ __global__ void __launch_bounds__(kGThreads, 1) k_gru_tc(const __grid_constant__
                         for (int k2 = 0; k2 < 2; ++k2) {
                             const int j = 64 * c + 16 * u + i + k2;
                             const float* w = p.wb + j * (3 * (SS + 1)) + 2 * (SS + 1);
-                            float pn = fmaf(kT, a2[c][i + k2], w[0]);
+                            float pn = kGX ? kT * a2[c][i + k2] : fmaf(kT, a2[c][i + k2], w[0]);
+                            if (!kGX) {
 #pragma unroll
-                            for (int s = 0; s < SS; ++s) pn = fmaf(xs[s], w[1 + s], pn);
+                                for (int s = 0; s < SS; ++s) pn = fmaf(xs[s], w[1 + s], pn);
+                            }
                             dn[k2] = tanh_e2_sig(pn);
                         }
                         const float n0 = dn[0], n1 = dn[1];
@@ -363,7 +435,7 @@ __global__ void k_pack_u_gru(const float* __restrict__ U, float scale, uint8_t* 
         const float v = U[(size_t)(64 * ks + kk) * (3 * kGM) + col] * scale;
         const __half hi = __float2half_rn(v);
         const __half lo = __float2half_rn(v - __half2float(hi));
-        uint8_t* base = img + (size_t)((q * kGKS + ks) * 2) * kGSliceBytes;
+        uint8_t* base = img + (size_t)((q * kGSlices + ks) * 2) * kGSliceBytes;   // kGSlices per chunk (XMMA: + [W; b])
         const uint32_t off = ptx::sw128_offset(nrow, kk);
         *reinterpret_cast<__half*>(base + off) = hi;
         *reinterpret_cast<__half*>(base + kGSliceBytes + off) = lo;
@@ -406,6 +478,7 @@ cudaError_t gru_tc_prepare(elmrnn* h) {
     cudaError_t e;
     const size_t bytes = (size_t)kGStagesPerStep * kGStageBytes;
     if ((e = cudaMalloc(&h->tc_ops, bytes))) return e;
+    if ((e = cudaMemsetAsync(h->tc_ops, 0, bytes, h->stream))) return e;
     h->tc_ops_bytes = bytes;
     const int sigma = h->rec_scale == 1 ? 0 : (int)std::floor(std::log2(std::sqrt((double)kGM)));
     const float scale = std::ldexp(1.0f, sigma);
@@ -428,7 +501,30 @@ cudaError_t gru_tc_prepare(elmrnn* h) {
     k_pack_u_gru<<<(int)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, h->stream>>>(
         h->rec, scale, static_cast<uint8_t*>(h->tc_ops));
     h->launches++;
-    return cudaGetLastError();
+    if ((e = cudaGetLastError())) return e;
+    if (kGX) {   // XMMA B slices: [W; b] x 2^sigma of each chunk's gate rows, K = s (W_s), K = S (b)
+        std::vector<uint8_t> xs((size_t)kGChunks * kGStageBytes, 0);
+        for (int q = 0; q < kGChunks; ++q)
+            for (int nrow = 0; nrow < 128; ++nrow) {
+                const int g = q < 2 ? (nrow & 1) : 2, j = q < 2 ? 64 * q + (nrow >> 1) : nrow;
+                for (int k = 0; k <= S; ++k) {
+                    const float v = (k < S ? W[(size_t)k * GM + g * kGM + j] : b[g * kGM + j]) * scale;
+                    const __half hi = __float2half_rn(v);
+                    const __half lo = __float2half_rn(v - __half2float(hi));
+                    uint8_t* base = xs.data() + (size_t)q * kGStageBytes;
+                    const uint32_t off = ptx::sw128_offset((uint32_t)nrow, (uint32_t)k);
+                    *reinterpret_cast<__half*>(base + off) = hi;
+                    *reinterpret_cast<__half*>(base + kGSliceBytes + off) = lo;
+                }
+            }
+        for (int q = 0; q < kGChunks; ++q)
+            if ((e = cudaMemcpyAsync(static_cast<uint8_t*>(h->tc_ops) + ((size_t)q * kGSlices + kGKS) * kGStageBytes,
+                                     xs.data() + (size_t)q * kGStageBytes, kGStageBytes, cudaMemcpyHostToDevice,
+                                     h->stream)))
+                return e;
+        if ((e = cudaStreamSynchronize(h->stream))) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_gru_tc(elmrnn* h, const float* X, int64_t ldx, int64_t N, float* H, int64_t ldh) {
