@@ -14,6 +14,9 @@
 // by phase 2), A_h after phase 2 (only read by the next step's phase 1).
 // Epilogue thread = (row, u): neurons 16u..16u+15 and 64+16u..64+16u+15; it
 // keeps h(t) of its 32 neurons in registers and z in shared memory.
+// The input term x W + b is one more K-step of every chunk's MMA chain (XMMA,
+// below): A = [x(t), 1] from a shared-memory SW128 image, B = [W; b] streamed
+// with the U slices, so the accumulator holds the whole pre-activation.
 #include <cuda_fp16.h>
 
 #include <algorithm>
