@@ -45,6 +45,9 @@ constexpr int kTcRows = 128;
 #ifndef ELM_TC256_STAGES
 #define ELM_TC256_STAGES 3
 #endif
+#ifndef ELM_TC_XMMA
+#define ELM_TC_XMMA 1
+#endif
 #ifndef ELM_TC_HOLD
 #define ELM_TC_HOLD 1   // hold the last K-slice of h(t) in registers (0: stage it like the others)
 #endif
@@ -80,6 +83,13 @@ struct TcCfg {
     static constexpr int STAGES = M == 256 ? ELM_TC256_STAGES : 3;   // U ring depth
     static constexpr int NCH = M / 32;
     static constexpr int KS = M / 64;
+    // XM (M = 128): x(t) W + b as one more K-step per chunk (as the GRU builder): A = [x, 1]
+    // fp16 hi|lo SW128 image in shared memory, B = [W; b] an extra streamed slice.  At
+    // M = 128 the epilogue paces the kernel (MMA per chunk ~1.5k cycles); at M = 256 the
+    // MMAs do, and the extra K-step would cost more than the epilogue saves.
+    static constexpr int XM = (M == 128 && ELM_TC_XMMA) ? 1 : 0;
+    static constexpr int SLICES = KS + XM;                 // streamed B slices per chunk
+    static constexpr int XIMG = XM * kTcStageBytes;        // the [x, 1] image, hi | lo
     // staged words per epilogue thread: h(t) hi|lo of chunks 0 .. NCH-3.  The last
     // K-slice bypasses the staging area (chunk NCH-2 waits in 8 registers for the
     // last chunk's MMAs to finish, chunk NCH-1 goes straight into TMEM), which
@@ -87,7 +97,7 @@ struct TcCfg {
     static constexpr int HOLD = ELM_TC_HOLD ? 2 : 0;   // chunks held in registers
     static constexpr int ITEMS = (NCH - HOLD) * 8;
     static constexpr int STG_BYTES = kTcEpiWarps * ITEMS * 32 * 4;
-    static constexpr int SMEM = 1024 + STAGES * kTcStageBytes + STG_BYTES + 256;   // + the X block
+    static constexpr int SMEM = 1024 + STAGES * kTcStageBytes + XIMG + STG_BYTES + 256;   // + the X block
     static constexpr int TMEM_COLS = 512;
     static constexpr int A_HI = 256;                       // TMEM columns of A = h(t-1): hi parts
     static constexpr int A_LO = 256 + M / 2;               //   lo parts (2 fp16 per 32-bit column)
@@ -134,7 +144,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int kTcStages = C::STAGES;
     uint8_t* stages = smem;                                                     // U ring
-    uint32_t* stg = reinterpret_cast<uint32_t*>(stages + kTcStages * kTcStageBytes);  // h(t) hi|lo staging
+    uint8_t* ximg = stages + kTcStages * kTcStageBytes;                              // XM: [x, 1] image (1 KB aligned)
+    uint32_t* stg = reinterpret_cast<uint32_t*>(ximg + C::XIMG);                     // h(t) hi|lo staging
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + C::STG_BYTES);
     float* xbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);   // the tile's X block
     uint64_t* full = bars;                       // [kTcStages]
@@ -145,7 +156,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
     uint64_t* a_free = a_ready + C::KS;          // [KS]: the last chunk's MMAs no longer read A slice ks
     uint64_t* x_full = a_free + C::KS;           // the tile's X block has landed
     uint64_t* x_empty = x_full + 1;              // every epilogue warp has read its last x(t)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 1);
+    uint64_t* xa_ready = x_empty + 1;            // XM: the [x, 1] image holds this step's x(t)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xa_ready + 1);
     uint32_t* trace_cnt = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -162,6 +174,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
         for (int i = 0; i < C::KS; ++i) ptx::mbar_init(a_free + i, 1);
         ptx::mbar_init(x_full, 1);
         ptx::mbar_init(x_empty, kTcEpiWarps);
+        ptx::mbar_init(xa_ready, 4);   // the 4 warps of neuron group u = 0
         *trace_cnt = 0;
         ptx::fence_mbar_init();
     }
@@ -187,14 +200,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                 if (ptx::xstage_tile(p.xbytes, tile, p.N))
                     ptx::xstage_issue(xbuf, p.X, p.ldx, tile, p.xbytes, x_full, x_empty, xph);
             }
-            for (int c = 0; c < C::NCH * C::KS; ++c) {
+            for (int c = 0; c < C::NCH * C::SLICES; ++c) {
                 ptx::mbar_wait(empty + st, ph ^ 1);
                 if (ptx::elect_one()) {
+                    // XM's [W; b] slice: hi and lo always (W, b are not on the fp16 grid)
+                    const uint32_t cb = (C::XM && c % C::SLICES == C::KS) ? (uint32_t)kTcStageBytes : bytes;
                     if (p.debug_no_u && s > 0) {   // timing experiment only (results invalid)
                         ptx::mbar_arrive(full + st);
                     } else {
-                        ptx::mbar_arrive_expect_tx(full + st, bytes);
-                        ptx::bulk_g2s(stages + st * kTcStageBytes, p.Uimg + (size_t)c * kTcStageBytes, bytes,
+                        ptx::mbar_arrive_expect_tx(full + st, cb);
+                        ptx::bulk_g2s(stages + st * kTcStageBytes, p.Uimg + (size_t)c * kTcStageBytes, cb,
                                       full + st);
                     }
                 }
@@ -242,7 +257,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                         ptx::mma_commit(empty + st);                  // frees the U stage
                         // last chunk of the step: A slice ks is free for h(t) once these MMAs retire
                         if (n == C::NCH - 1 && ks < C::KS - 1) ptx::mma_commit(a_free + ks);
-                        if (ks == C::KS - 1) ptx::mma_commit(acc_full + ach);   // chunk accumulator ready
+                        if (!C::XM && ks == C::KS - 1) ptx::mma_commit(acc_full + ach);   // chunk accumulator ready
+                    }
+                    __syncwarp();
+                    if (++st == kTcStages) { st = 0; ph ^= 1; }
+                }
+                if constexpr (C::XM != 0) {   // x(t) W + b: one k-step, A = [x, 1] from shared memory
+                    if (n == 0) {
+                        ptx::mbar_wait(xa_ready, (uint32_t)(s & 1));
+                        ptx::tc_fence_after();
+                    }
+                    ptx::mbar_wait(full + st, ph);
+                    ptx::tc_fence_after();
+                    const uint64_t dbh = dbase + (uint64_t)((st * kTcStageBytes) >> 4);
+                    const uint64_t dbl = dbh + (uint64_t)(kTcSliceBytes >> 4);
+                    if (ptx::elect_one()) {
+                        const uint64_t axh = ptx::desc_sw128_kmajor(ptx::smem_u32(ximg));
+                        const uint64_t axl = axh + (uint64_t)(kTcSliceBytes >> 4);
+                        ptx::mma_f16_ss(d, axh, dbh, idesc, 1u);
+                        ptx::mma_f16_ss(d, axl, dbh, idesc, 1u);
+                        ptx::mma_f16_ss(d, axh, dbl, idesc, 1u);
+                        ptx::mma_commit(empty + st);
+                        ptx::mma_commit(acc_full + ach);
                     }
                     __syncwarp();
                     if (++st == kTcStages) { st = 0; ph ^= 1; }
@@ -307,6 +343,48 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                 ptx::mbar_wait(x_full, xph);
                 xph ^= 1;
             }
+            // XM: write [x(tn), 1, 0..] of this row (fp16 hi|lo) into the A image (group u = 0)
+            auto put_x = [&](int tn) {
+                if (u == 0) {
+                    float xv[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) xv[k] = 0.0f;
+#pragma unroll
+                    for (int s = 0; s < SS; ++s)
+                        xv[s] = (valid && s < p.S)
+                                    ? (xst ? xrow[(tn - 1) * p.S + s] : __ldg(xrow + (int64_t)(tn - 1) * p.S + s))
+                                    : 0.0f;
+                    xv[p.S] = 1.0f;   // the bias column
+                    uint32_t hi[8], lo[8];
+#pragma unroll
+                    for (int q8 = 0; q8 < 2; ++q8) {
+                        float h8[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) h8[i] = xv[8 * q8 + i];
+                        uint32_t h4[4], l4[4];
+                        split_h8(h8, h4, l4);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            hi[4 * q8 + i] = h4[i];
+                            lo[4 * q8 + i] = l4[i];
+                        }
+                    }
+                    *reinterpret_cast<uint4*>(ximg + ptx::sw128_offset((uint32_t)r, 0)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                    *reinterpret_cast<uint4*>(ximg + ptx::sw128_offset((uint32_t)r, 8)) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+                    *reinterpret_cast<uint4*>(ximg + kTcSliceBytes + ptx::sw128_offset((uint32_t)r, 0)) =
+                        make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                    *reinterpret_cast<uint4*>(ximg + kTcSliceBytes + ptx::sw128_offset((uint32_t)r, 8)) =
+                        make_uint4(lo[4], lo[5], lo[6], lo[7]);
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(xa_ready);
+                }
+                if (xst && tn == p.Q) {   // last x(t) of this tile read: the block may be replaced
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(x_empty);
+                }
+            };
+            if constexpr (C::XM != 0) put_x(1);
 #pragma unroll
             for (int i = 0; i < C::NCH * 8; ++i) c[i] = 0.0f;
             double yacc = 0.0;   // fused readout partial
@@ -314,9 +392,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                 float xs[SS];
 #pragma unroll
                 for (int s = 0; s < SS; ++s)
-                    xs[s] = (valid && s < p.S) ? (xst ? xrow[(t - 1) * p.S + s] : __ldg(xrow + (int64_t)(t - 1) * p.S + s))
-                                               : 0.0f;
-                if (xst && t == p.Q) {   // last x(t) of this tile read: the block may be replaced
+                    xs[s] = (!C::XM && valid && s < p.S)
+                                ? (xst ? xrow[(t - 1) * p.S + s] : __ldg(xrow + (int64_t)(t - 1) * p.S + s))
+                                : 0.0f;
+                if (!C::XM && xst && t == p.Q) {   // last x(t) of this tile read: the block may be replaced
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(x_empty);
                 }
@@ -347,6 +426,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                         ptx::tmem_st4(lane_base + C::A_HI + (C::NCH - 2) * 16 + 4 * u, hi);
                         ptx::tmem_st4(lane_base + C::A_LO + (C::NCH - 2) * 16 + 4 * u, lo);
                     }
+                    // XM: every MMA of step t has completed (the last chunk's included): the
+                    // A image may take x(t+1) for the next step
+                    if (C::XM && n == C::NCH - 1 && t < p.Q) put_x(t + 1);
                     if (e == 0 && lane == 0) trace_ev(p, trace_cnt, 4, t, n);
                     float a[2][16];   // 2 groups x 4 neurons x (o, c, lambda, in), scaled domain
                     tmem_ld16(lane_base + ach * 128 + (8 * u) * 4, a[0]);
@@ -369,10 +451,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
                             float arg[4];
 #pragma unroll
                             for (int g = 0; g < 4; ++g) {
-                                float v = fmaf(g == 1 ? kT : kS, a[g4][nb * 4 + g], w[g * (SS + 1)]);
+                                if constexpr (C::XM != 0) {   // x W + b is in the accumulator
+                                    arg[g] = (g == 1 ? kT : kS) * a[g4][nb * 4 + g];
+                                } else {
+                                    float v = fmaf(g == 1 ? kT : kS, a[g4][nb * 4 + g], w[g * (SS + 1)]);
 #pragma unroll
-                                for (int s = 0; s < SS; ++s) v = fmaf(xs[s], w[g * (SS + 1) + 1 + s], v);
-                                arg[g] = v;
+                                    for (int s = 0; s < SS; ++s) v = fmaf(xs[s], w[g * (SS + 1) + 1 + s], v);
+                                    arg[g] = v;
+                                }
                             }
                             const float so = sig_e2(arg[0]);   // o
                             const float tc = tanh_e2(arg[1]);  // c~
@@ -452,7 +538,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lstm_tc(const __grid_constant
 // image[(n*KS + s)*2 + part][sw128(nrow = jj*4 + g, kk)] for neuron n*32+jj, gate g, K = 64s + kk.
 // pair = 1 (wide LSTM with N = 256 MMA units): chunks 2m, 2m+1 of a K-slice are adjacent
 // 16 KB tiles, i.e. one 256-row SW128 tile: image[((m*KS + s)*2 + part)][chunk % 2][16 KB]
-__global__ void k_pack_u(const float* __restrict__ U, int M, float scale, uint8_t* __restrict__ img, int pair) {
+// slices: streamed slices per chunk in the non-pair layout (KS, or KS + 1 with the XM [W; b] slice)
+__global__ void k_pack_u(const float* __restrict__ U, int M, float scale, uint8_t* __restrict__ img, int pair,
+                         int slices) {
     const int KS = M / 64, NCH = M / 32;
     const int64_t total = (int64_t)NCH * KS * 128 * 64;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -465,7 +553,7 @@ __global__ void k_pack_u(const float* __restrict__ U, int M, float scale, uint8_
         __half hi = __float2half_rn(v);
         __half lo = __float2half_rn(v - __half2float(hi));
         uint8_t* base = pair ? img + (size_t)(((n >> 1) * KS + s) * 2) * 2 * kTcSliceBytes + (size_t)(n & 1) * kTcSliceBytes
-                             : img + (size_t)((n * KS + s) * 2) * kTcSliceBytes;
+                             : img + (size_t)((n * slices + s) * 2) * kTcSliceBytes;
         uint32_t off = ptx::sw128_offset(nrow, kk);
         *reinterpret_cast<__half*>(base + off) = hi;
         *reinterpret_cast<__half*>(base + (pair ? 2 : 1) * kTcSliceBytes + off) = lo;
@@ -543,11 +631,14 @@ cudaError_t tc_prepare(elmrnn* h) {
     if (h->arch == kArchFC) return fc_tc_prepare(h);
     const int M = h->M;
     const bool wide = lstm_wide_supported(h);
-    size_t bytes = (size_t)(M / 32) * (M / 64) * kTcStageBytes;
+    const int xm = (!wide && M == 128) ? TcCfg<128>::XM : 0;   // the XM [W; b] slice per chunk
+    const int slices = M / 64 + xm;
+    size_t bytes = (size_t)(M / 32) * slices * kTcStageBytes;
     if (wide) bytes += sizeof(float) * (size_t)M * 4 * (tc_padded_s(h->S) + 1);   // W | b in global memory
     cudaError_t e;
     if ((e = cudaMalloc(&h->tc_ops, bytes))) return e;
     h->tc_ops_bytes = bytes;
+    if ((e = cudaMemsetAsync(h->tc_ops, 0, bytes, h->stream))) return e;
     // sigma: largest power of two keeping |U| * 2^sigma < 1 (exact scaling)
     int sigma = h->rec_scale == 1 ? 0 : (int)std::floor(std::log2(std::sqrt((double)M)));
     float scale = std::ldexp(1.0f, sigma);
@@ -576,9 +667,33 @@ cudaError_t tc_prepare(elmrnn* h) {
     int64_t total = (int64_t)(M / 32) * (M / 64) * 128 * 64;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
     k_pack_u<<<blocks, 256, 0, h->stream>>>(h->rec, M, scale, static_cast<uint8_t*>(h->tc_ops),
-                                            wide && lstm_wide_pair(h) ? 1 : 0);
+                                            wide && lstm_wide_pair(h) ? 1 : 0, slices);
     h->launches++;
-    return cudaGetLastError();
+    if ((e = cudaGetLastError())) return e;
+    if (xm) {   // XM B slices: [W; b] x 2^sigma of each chunk's gate rows (nrow = jj*4 + g), K = s (W_s), K = S (b)
+        const int NCH = M / 32;
+        std::vector<uint8_t> xs((size_t)NCH * kTcStageBytes, 0);
+        for (int n = 0; n < NCH; ++n)
+            for (int nrow = 0; nrow < 128; ++nrow) {
+                const int jj = nrow >> 2, g = nrow & 3, j = n * 32 + jj;
+                for (int k = 0; k <= S; ++k) {
+                    const float v = (k < S ? W[(size_t)k * GM + g * M + j] : b[g * M + j]) * scale;
+                    const __half hi = __float2half_rn(v);
+                    const __half lo = __float2half_rn(v - __half2float(hi));
+                    uint8_t* base = xs.data() + (size_t)n * kTcStageBytes;
+                    const uint32_t off = ptx::sw128_offset((uint32_t)nrow, (uint32_t)k);
+                    *reinterpret_cast<__half*>(base + off) = hi;
+                    *reinterpret_cast<__half*>(base + kTcSliceBytes + off) = lo;
+                }
+            }
+        for (int n = 0; n < NCH; ++n)
+            if ((e = cudaMemcpyAsync(static_cast<uint8_t*>(h->tc_ops) + ((size_t)n * slices + M / 64) * kTcStageBytes,
+                                     xs.data() + (size_t)n * kTcStageBytes, kTcStageBytes, cudaMemcpyHostToDevice,
+                                     h->stream)))
+                return e;
+        if ((e = cudaStreamSynchronize(h->stream))) return e;
+    }
+    return cudaSuccess;
 }
 
 template <int M>
